@@ -1,0 +1,171 @@
+/* shellular_cuda.h -- C ABI of the B200-native shellular hot path.
+ *
+ * The reference (arxiv/paper_2511_04025, /root/reference/proj) has no FFI:
+ * its boundary is the inline C++ API in proj/include/shellular/ (*.hpp).  Each
+ * entry point below replaces the body of one reference function; the C++
+ * drop-in headers in include/shellular/ keep the reference names and call
+ * these.  Plain pointers and sizes only, no exceptions across the ABI.
+ *
+ *   shl_sample_grid        <- sample_grid            field.hpp:488-534
+ *   shl_load_grid          <- sample_grid_fn         field.hpp:538-559 (host-sampled fields)
+ *   shl_build_reduced_mesh <- build_reduced_mesh     voxel.hpp:235-313
+ *                             classify_surface_elements voxel.hpp:118-141
+ *   shl_grid_solve         <- GridSolver(...).solve  grid_solver.hpp:20-96
+ *   shl_solve_mesh         <- build_periodic_system + solve_test_strains +
+ *                             effective_tensor       fem.hpp:179-428
+ *   shl_homogenize         <- homogenize             pipeline.hpp:61-113
+ *   shl_homogenize_batch   <- (new) many designs, one call (SPEC sample_campaign)
+ *   shl_element_stiffness  <- element_stiffness      fem.hpp:50-92
+ *   shl_random_design      <- random_design          field.hpp:569-593
+ *   shl_expand_symmetry    <- expand_symmetry        field.hpp:236-249
+ *
+ * Status codes mirror the reference exception classes (common.hpp:25-48).
+ * Host buffers are caller-allocated; device workspaces are owned by the
+ * context and reused across calls.  A context is bound to one device and is
+ * not thread-safe; distinct contexts are independent.
+ */
+#ifndef SHELLULAR_CUDA_H
+#define SHELLULAR_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SHL_OK = 0,
+  SHL_VALIDATION = 1, /* ValidationError       */
+  SHL_DEGENERATE = 2, /* DegenerateDesignError */
+  SHL_SOLVER = 3,     /* SolverError           */
+  SHL_IO = 4,         /* IoError               */
+  SHL_CUDA = 5        /* device / driver failure (no reference analogue) */
+};
+
+enum { SHL_SYM_NONE = 0, SHL_SYM_CUBIC_OCTANT = 1, SHL_SYM_TETRAHEDRAL = 2 };
+
+/* arithmetic of the PCG vectors (x, r | p, q, z) and of the K.u apply */
+enum {
+  SHL_PREC_AUTO = -1,  /* FP64 when tol < 1e-7, else MIXED */
+  SHL_PREC_FP64 = 0,   /* everything FP64 */
+  SHL_PREC_MIXED = 1,  /* FP32 apply/p/q/z, FP64 x/r/dots */
+  SHL_PREC_FP32 = 2    /* FP32 vectors, FP64 dots */
+};
+
+typedef struct shl_ctx shl_ctx;
+
+/* DesignParams (field.hpp:131-231), pre-expansion. positions: 3*n_charges
+ * (wrapped into [0,1) like the Charge ctor), signs: +-1, weights: (K+1)^3. */
+typedef struct {
+  int symmetry;
+  int K;
+  int n_charges;
+  const double* positions;
+  const int32_t* signs;
+  const double* weights;
+} shl_design;
+
+/* ShellParams (voxel.hpp:18-34) */
+typedef struct {
+  double sharpness;   /* 500   */
+  double floor_ratio; /* 1e-3  */
+  int expand_layers;  /* 0 = max(1, round(2r/64)) */
+} shl_shell_params;
+
+/* BaseMaterial (fem.hpp:19-30) */
+typedef struct {
+  double youngs;  /* 1.0 */
+  double poisson; /* 0.3 */
+} shl_material;
+
+typedef struct {
+  double tol;      /* per-column ||r|| <= tol*||b|| (grid_solver.hpp:68) */
+  int max_iter;    /* 0 = 20r+2000 (grid_solver.hpp:38) */
+  int precision;   /* SHL_PREC_* */
+  int check_every; /* host convergence poll period in iterations (0 = auto) */
+  int reserved;
+} shl_solve_options;
+
+/* StageTimings (common.hpp:145-160) + solver / mesh statistics */
+typedef struct {
+  double t_field, t_mesh, t_PBC, t_AS, t_RHS, t_solve, t_C, t_fwd; /* ms, CUDA events */
+  int32_t iterations[6];
+  int32_t converged;
+  int32_t full_fallback;
+  int32_t precision; /* resolved SHL_PREC_* */
+  int32_t reserved0;
+  int64_t n_surface;  /* surface elements before dilation */
+  int64_t n_elements; /* active (reduced-mesh) elements */
+  int64_t n_nodes;    /* active torus nodes */
+  int64_t n_tiles;    /* active apply tiles */
+  double norm;        /* max |centre sample| */
+  double volume_ratio;
+  double apply_ms; /* summed device time of the K.u apply launches (0 unless profiled) */
+  double update_ms;
+  int64_t apply_launches;
+  int64_t kernel_launches; /* kernels launched by this call */
+} shl_stats;
+
+int shl_ctx_create(int device, shl_ctx** out);
+void shl_ctx_destroy(shl_ctx* ctx);
+/* Message of the last failing call on ctx (or of the calling thread when ctx
+ * is NULL). */
+const char* shl_last_error(const shl_ctx* ctx);
+/* Device-time profiling of apply / update kernels (CUDA events per launch). */
+int shl_set_profiling(shl_ctx* ctx, int on);
+
+/* Field sampling on device (bit-exact FP64 reference order).  Any output
+ * pointer may be NULL.  centres: r^3, corners: (r+1)^3 incl. wrapped copies,
+ * both x fastest.  The grid stays resident in ctx for shl_build_reduced_mesh. */
+int shl_sample_grid(shl_ctx* ctx, const shl_design* design, int r, double* centres,
+                    double* corners, double* norm);
+
+/* Make a host-sampled grid (sample_grid_fn fixtures) resident in ctx. */
+int shl_load_grid(shl_ctx* ctx, int r, const double* centres, const double* corners,
+                  double norm);
+
+/* Surface classification only (classify_surface_elements), on the resident
+ * grid: writes sorted element ids (capacity r^3) and their count. */
+int shl_classify_surface(shl_ctx* ctx, uint32_t* elements, int64_t* n_surface);
+
+/* Reduced mesh on the resident grid.  elements: sorted ids (capacity r^3),
+ * beta: per listed element; either may be NULL. */
+int shl_build_reduced_mesh(shl_ctx* ctx, const shl_shell_params* sp, uint32_t* elements,
+                           double* beta, int64_t* n_elements, int32_t* full_fallback);
+
+/* Six-load-case homogenization of a voxel mesh given by a dense r^3 beta
+ * array (0 = absent element), with torus node 0 pinned: the GridSolver of
+ * grid_solver.hpp generalized to masked meshes.  K0: 24x24 row-major. */
+int shl_grid_solve(shl_ctx* ctx, int r, const double* beta, const double* K0,
+                   const shl_solve_options* opt, double* C_out, shl_stats* stats);
+
+/* Same solve on the reduced mesh resident in ctx (after
+ * shl_build_reduced_mesh). */
+int shl_solve_mesh(shl_ctx* ctx, const double* K0, const shl_solve_options* opt, double* C_out,
+                   shl_stats* stats);
+
+/* End-to-end: field -> shell mask -> six-load-case PCG -> C^H (36, row-major). */
+int shl_homogenize(shl_ctx* ctx, const shl_design* design, const shl_shell_params* sp,
+                   const shl_material* mat, int r, const shl_solve_options* opt, double* C_out,
+                   shl_stats* stats);
+
+/* n designs at one resolution; C_out: n*36, stats: n (may be NULL), status:
+ * n per-design codes (may be NULL).  Returns SHL_OK unless a device error
+ * stops the batch; per-design failures are reported through status. */
+int shl_homogenize_batch(shl_ctx* ctx, int n, const shl_design* designs,
+                         const shl_shell_params* sp, const shl_material* mat, int r,
+                         const shl_solve_options* opt, double* C_out, shl_stats* stats,
+                         int32_t* status);
+
+/* Host helpers (reference arithmetic, no device work). */
+int shl_element_stiffness(const shl_material* mat, double edge, double* K_out /*576*/);
+int shl_random_design(int symmetry, int n_pre, int K, double weight_lo, double weight_hi,
+                      uint64_t seed, double* positions /*3*n_pre*/, int32_t* signs /*n_pre*/,
+                      double* weights /*(K+1)^3*/);
+int shl_expand_symmetry(const shl_design* design, double* positions_out, int32_t* signs_out,
+                        int32_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHELLULAR_CUDA_H */

@@ -1,0 +1,64 @@
+// device.cuh -- device-side types, launch wrappers and small helpers shared by
+// the kernels of libshellular_cuda.so (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace shl {
+
+constexpr int kFieldRows = 8;        // (y,z)-rows per field block (charge tables reused 8x)
+constexpr int kFieldThreads = 128;   // x samples per field block pass
+constexpr int kFieldChargeChunk = 128;
+
+// ---- PCG control block (one per solve, device resident) -------------------
+struct PcgState {
+  double alpha[6];
+  double beta[6];
+  double rz[6];
+  double bnorm[6];
+  double rr[6];
+  double pq[6];
+  double tol;
+  int32_t done[6];
+  int32_t iters[6];
+  int32_t it;
+  int32_t max_iter;
+  int32_t all_done;
+  int32_t error;  // 1: p^T A p <= 0 on an unconverged column
+  int32_t stop;   // all_done || error || it >= max_iter
+  uint32_t counter_apply;
+  uint32_t counter_update;
+  uint32_t counter_misc;
+};
+
+// ---- launch wrappers (defined in field.cu / voxel.cu / solver.cu) ---------
+// field
+void launch_field_sl(const double* tab, const double* coeff, double* sl, int nc, int r, int n,
+                     cudaStream_t s);
+void launch_field_samples(const double* tab, const double* sl, const int8_t* sign, int nc, int r,
+                          int n, double* centres, double* corners, int8_t* corner_sign,
+                          unsigned long long* norm_bits, cudaStream_t s);
+// voxelize
+void launch_corner_signs(const double* corners, int8_t* corner_sign, int r, cudaStream_t s);
+void launch_classify(const int8_t* corner_sign, uint8_t* occ, int r, int* n_surface,
+                     cudaStream_t s);
+void launch_dilate(const uint8_t* in, uint8_t* out, int r, cudaStream_t s);
+void launch_complete(const uint8_t* in, uint8_t* out, int r, int* touches, cudaStream_t s);
+void launch_force_corners(uint8_t* occ, int r, const int* touches, cudaStream_t s);
+void launch_beta(const uint8_t* occ, const double* centres, const double* norm, double sharp,
+                 double floor_ratio, int r, double* beta64, float* beta32, int* elem_flag,
+                 double* partial, int nblocks_partial, cudaStream_t s);
+void launch_beta_from_dense(const double* beta_in, int r, float* beta32, int* elem_flag,
+                            uint8_t* occ, cudaStream_t s);
+void launch_node_flags(const int* elem_flag, int r, int tx, int ty, int tz, int* node_flag,
+                       int* tile_flag, cudaStream_t s);
+void launch_scatter_compact(const int* flag, const int* offset, int n, int* map_or_null,
+                            int* list, cudaStream_t s);
+void launch_fill_int(int* p, int v, size_t n, cudaStream_t s);
+size_t scan_temp_bytes(int n);
+void launch_exclusive_scan(const int* in, int* out, int n, void* temp, size_t temp_bytes,
+                           cudaStream_t s);
+
+}  // namespace shl

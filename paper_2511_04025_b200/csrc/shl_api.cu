@@ -1,0 +1,816 @@
+// shl_api.cu -- the C ABI of include/shellular_cuda.h: context, device
+// workspaces, stage orchestration and error mapping.
+//
+// Stage map onto the reference's homogenize (pipeline.hpp:61-113):
+//   field    host: expand_symmetry, coefficients, cosine tables (host_design.cpp)
+//            device: K1 (field.cu)                               -> t_field
+//   mesh     K2 classify / dilate / complete / corners / beta   -> t_mesh
+//   PBC      node activation + ordered compaction (voxel.cu)      -> t_PBC
+//   AS, RHS  block-Jacobi + right-hand sides (solver.cu setup)    -> t_AS (+t_RHS)
+//   solve    K4/K5 PCG loop, device-resident scalars               -> t_solve
+//   C        K6 energy reduction                                   -> t_C
+// Only the norm / counts (one 64-byte readback after meshing), the PCG flag
+// (every check_every iterations) and the 6x6 tensor cross PCIe.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "internal.h"
+#include "solver.cuh"
+
+using shl::ShlError;
+
+namespace {
+
+thread_local std::string g_thread_error;
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw ShlError(SHL_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 8 + 256;
+    CK(cudaMalloc(&p, want));
+    cap = want;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+// Small device-side bookkeeping block, mirrored into pinned host memory.
+struct Misc {
+  unsigned long long norm_bits;
+  int n_surface;
+  int touches;
+  int n_nodes;
+  int n_elem;
+  int n_tiles;
+  int node0_active;
+  double beta_sum;
+  double pad[4];
+};
+
+__global__ void finalize_counts_kernel(Misc* m, const int* node_flag, const int* node_off,
+                                       const int* elem_flag, const int* elem_off,
+                                       const int* tile_flag, const int* tile_off, int n3,
+                                       int ntiles, const double* beta_partials, int nbp) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nbp; b += blockDim.x) s += beta_partials[2 * b];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    m->beta_sum = sh[0];
+    m->n_nodes = node_off[n3 - 1] + node_flag[n3 - 1];
+    m->n_elem = elem_off[n3 - 1] + elem_flag[n3 - 1];
+    m->n_tiles = tile_off[ntiles - 1] + tile_flag[ntiles - 1];
+    m->node0_active = node_flag[0];
+  }
+}
+
+inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// element-local affine loads T (grid_solver.hpp:119-126) and W = K0*T
+void element_loads(const double* K0, int r, double* T, double* W) {
+  for (int n = 0; n < 8; ++n)
+    for (int a = 0; a < 3; ++a)
+      for (int s = 0; s < 6; ++s) {
+        // eps_s (fem.hpp:129-142) times y = corner offset / r
+        double e[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        if (s < 3) e[s][s] = 1.0;
+        if (s == 3) e[1][2] = e[2][1] = 0.5;
+        if (s == 4) e[0][2] = e[2][0] = 0.5;
+        if (s == 5) e[0][1] = e[1][0] = 0.5;
+        double y[3] = {shl::kCorner[n][0] / double(r), shl::kCorner[n][1] / double(r),
+                       shl::kCorner[n][2] / double(r)};
+        T[(3 * n + a) * 6 + s] = e[a][0] * y[0] + e[a][1] * y[1] + e[a][2] * y[2];
+      }
+  for (int i = 0; i < 24; ++i)
+    for (int s = 0; s < 6; ++s) {
+      double acc = 0.0;
+      for (int j = 0; j < 24; ++j) acc += K0[i * 24 + j] * T[j * 6 + s];
+      W[i * 6 + s] = acc;
+    }
+}
+
+}  // namespace
+
+struct shl_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  bool profiling = false;
+  int64_t launches = 0;
+
+  // resident grid
+  int r = 0;
+  bool grid_ready = false, mesh_ready = false;
+  double norm = 0.0;
+  DevBuf tab, coeff, sl, sign8, centres, corners, csign, misc;
+  // mesh + topology
+  DevBuf occ0, occ1, beta64, beta32, elem_flag, node_flag, tile_flag, off, node_map, node_list,
+      elem_list, tile_list, scan_tmp, beta_partials;
+  int64_t n_surface = 0, n_elem = 0;
+  int n_nodes = 0, n_tiles = 0, full_fallback = 0, node0_active = 0;
+  double volume_ratio = 0.0;
+  int tile_prec = -1;  // precision the tile list was built for
+  // solver
+  DevBuf vec, partials, state, cout;
+  Misc* hmisc = nullptr;
+  shl::PcgState* hstate = nullptr;
+  double* hC = nullptr;
+  cudaEvent_t ev[12] = {};
+  std::vector<cudaEvent_t> prof_ev;
+
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+  float ms(int a, int b) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, ev[a], ev[b]));
+    return t;
+  }
+};
+
+namespace {
+
+template <class Fn>
+int guarded(shl_ctx* ctx, Fn&& fn) {
+  try {
+    if (ctx) CK(cudaSetDevice(ctx->device));
+    fn();
+    if (ctx) ctx->err.clear();
+    return SHL_OK;
+  } catch (const ShlError& e) {
+    if (ctx) ctx->err = e.what();
+    g_thread_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    g_thread_error = e.what();
+    return SHL_IO;
+  }
+}
+
+template <class Fn>
+auto tagged(const char* stage, Fn&& fn) {
+  try {
+    return fn();
+  } catch (const ShlError& e) {
+    if (e.code == SHL_CUDA || e.code == SHL_IO) throw;
+    throw ShlError(e.code, std::string(stage) + ": " + e.what());
+  }
+}
+
+void require_r(int r) {
+  if (r < 4) throw ShlError(SHL_VALIDATION, "grid resolution must be >= 4");
+  if (r > 1024) throw ShlError(SHL_VALIDATION, "grid resolution must be <= 1024");
+}
+
+void alloc_grid(shl_ctx* c, int r) {
+  const size_t n3 = static_cast<size_t>(r) * r * r;
+  c->centres.ensure(n3 * sizeof(double));
+  c->corners.ensure(n3 * sizeof(double));
+  c->csign.ensure(n3);
+  c->misc.ensure(sizeof(Misc));
+  c->r = r;
+}
+
+// ---- field (sample_grid, field.hpp:488-534) --------------------------------
+void run_field(shl_ctx* c, const shl::HostDesign& d, int r) {
+  require_r(r);
+  const shl::HostDesign ex = d.expanded();  // validates (field.hpp:149-172)
+  const std::vector<double> coeff = d.grid_coefficients();
+  const std::vector<double> tab = shl::axis_tables(ex, r);
+  const int nc = static_cast<int>(ex.sign.size());
+  const int n = d.K + 1;
+  alloc_grid(c, r);
+  c->grid_ready = c->mesh_ready = false;
+  std::vector<int8_t> sg(ex.sign.begin(), ex.sign.end());
+  c->tab.ensure(std::max<size_t>(tab.size(), 1) * sizeof(double));
+  c->coeff.ensure(coeff.size() * sizeof(double));
+  c->sign8.ensure(std::max<size_t>(sg.size(), 1));
+  c->sl.ensure(std::max<size_t>(static_cast<size_t>(nc) * 2 * r * n * n, 1) * sizeof(double));
+  if (!tab.empty())
+    CK(cudaMemcpyAsync(c->tab.p, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+  CK(cudaMemcpyAsync(c->coeff.p, coeff.data(), coeff.size() * sizeof(double),
+                     cudaMemcpyHostToDevice, c->stream));
+  if (!sg.empty())
+    CK(cudaMemcpyAsync(c->sign8.p, sg.data(), sg.size(), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->misc.p, 0, sizeof(Misc), c->stream));
+  shl::launch_field_sl(c->tab.as<double>(), c->coeff.as<double>(), c->sl.as<double>(), nc, r, n,
+                       c->stream);
+  shl::launch_field_samples(c->tab.as<double>(), c->sl.as<double>(), c->sign8.as<int8_t>(), nc, r,
+                            n, c->centres.as<double>(), c->corners.as<double>(),
+                            c->csign.as<int8_t>(), &c->misc.as<Misc>()->norm_bits, c->stream);
+  c->launches += 2;
+  CK(cudaGetLastError());
+  // the pinned synchronous tables above must outlive their copies
+  c->sync();
+  c->grid_ready = true;
+}
+
+void read_norm(shl_ctx* c) {
+  CK(cudaMemcpyAsync(c->hmisc, c->misc.p, sizeof(Misc), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  double v;
+  std::memcpy(&v, &c->hmisc->norm_bits, sizeof(double));
+  c->norm = v;
+}
+
+// ---- topology: node ids, element list, apply tiles ------------------------
+template <typename TV>
+void build_topology(shl_ctx* c) {
+  const int r = c->r;
+  const int n3 = r * r * r;
+  constexpr int TX = shl::TileShape<TV>::X, TY = shl::TileShape<TV>::Y, TZ = shl::TileShape<TV>::Z;
+  const int ntiles = ((r + TX - 1) / TX) * ((r + TY - 1) / TY) * ((r + TZ - 1) / TZ);
+  c->node_flag.ensure(static_cast<size_t>(n3) * sizeof(int));
+  c->tile_flag.ensure(static_cast<size_t>(ntiles) * sizeof(int));
+  c->off.ensure(static_cast<size_t>(n3) * sizeof(int) * 3);
+  c->node_map.ensure(static_cast<size_t>(n3) * sizeof(int));
+  c->node_list.ensure(static_cast<size_t>(n3) * sizeof(int));
+  c->elem_list.ensure(static_cast<size_t>(n3) * sizeof(int));
+  c->tile_list.ensure(static_cast<size_t>(ntiles) * sizeof(int));
+  const size_t tb = shl::scan_temp_bytes(n3);
+  c->scan_tmp.ensure(tb);
+  int* off_n = c->off.as<int>();
+  int* off_e = off_n + n3;
+  int* off_t = off_e + n3;
+  CK(cudaMemsetAsync(c->tile_flag.p, 0, static_cast<size_t>(ntiles) * sizeof(int), c->stream));
+  shl::launch_node_flags(c->elem_flag.as<int>(), r, TX, TY, TZ, c->node_flag.as<int>(),
+                         c->tile_flag.as<int>(), c->stream);
+  shl::launch_exclusive_scan(c->node_flag.as<int>(), off_n, n3, c->scan_tmp.p, c->scan_tmp.cap,
+                             c->stream);
+  shl::launch_scatter_compact(c->node_flag.as<int>(), off_n, n3, c->node_map.as<int>(),
+                              c->node_list.as<int>(), c->stream);
+  shl::launch_exclusive_scan(c->elem_flag.as<int>(), off_e, n3, c->scan_tmp.p, c->scan_tmp.cap,
+                             c->stream);
+  shl::launch_scatter_compact(c->elem_flag.as<int>(), off_e, n3, nullptr, c->elem_list.as<int>(),
+                              c->stream);
+  shl::launch_exclusive_scan(c->tile_flag.as<int>(), off_t, ntiles, c->scan_tmp.p, c->scan_tmp.cap,
+                             c->stream);
+  shl::launch_scatter_compact(c->tile_flag.as<int>(), off_t, ntiles, nullptr,
+                              c->tile_list.as<int>(), c->stream);
+  const int nbp = (n3 + 255) / 256;
+  finalize_counts_kernel<<<1, 256, 0, c->stream>>>(
+      c->misc.as<Misc>(), c->node_flag.as<int>(), off_n, c->elem_flag.as<int>(), off_e,
+      c->tile_flag.as<int>(), off_t, n3, ntiles, c->beta_partials.as<double>(), nbp);
+  c->launches += 1 + 3 * 2 + 3 + 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->hmisc, c->misc.p, sizeof(Misc), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  c->n_nodes = c->hmisc->n_nodes;
+  c->n_elem = c->hmisc->n_elem;
+  c->n_tiles = c->hmisc->n_tiles;
+  c->node0_active = c->hmisc->node0_active;
+  c->volume_ratio = c->hmisc->beta_sum / (double(r) * r * r);
+  c->tile_prec = sizeof(TV) == 8 ? 0 : 1;
+}
+
+void build_topology_for(shl_ctx* c, bool fp64_tiles) {
+  if (fp64_tiles)
+    build_topology<double>(c);
+  else
+    build_topology<float>(c);
+}
+
+// ---- mesh (build_reduced_mesh, voxel.hpp:235-313) --------------------------
+void run_mesh(shl_ctx* c, const shl_shell_params& sp, bool fp64_tiles) {
+  if (!c->grid_ready) throw ShlError(SHL_VALIDATION, "no resident grid: call shl_sample_grid first");
+  if (!(sp.sharpness > 0.0)) throw ShlError(SHL_VALIDATION, "sharpness must be positive");
+  if (!(sp.floor_ratio > 0.0 && sp.floor_ratio < 1.0))
+    throw ShlError(SHL_VALIDATION, "floor must lie in (0, 1)");
+  if (sp.expand_layers < 0) throw ShlError(SHL_VALIDATION, "expand_layers must be >= 0");
+  if (c->norm == 0.0)
+    throw ShlError(SHL_DEGENERATE, "cannot classify surface elements of a degenerate field");
+  const int r = c->r;
+  const size_t n3 = static_cast<size_t>(r) * r * r;
+  const int layers =
+      sp.expand_layers > 0 ? sp.expand_layers : std::max(1, static_cast<int>(std::lround(2.0 * r / 64.0)));
+  c->occ0.ensure(n3);
+  c->occ1.ensure(n3);
+  c->beta64.ensure(n3 * sizeof(double));
+  c->beta32.ensure(n3 * sizeof(float));
+  c->elem_flag.ensure(n3 * sizeof(int));
+  c->beta_partials.ensure(((n3 + 255) / 256) * 2 * sizeof(double));
+  uint8_t* a = c->occ0.as<uint8_t>();
+  uint8_t* b = c->occ1.as<uint8_t>();
+  Misc* dm = c->misc.as<Misc>();
+  CK(cudaMemsetAsync(&dm->n_surface, 0, sizeof(int) * 2, c->stream));
+  shl::launch_classify(c->csign.as<int8_t>(), a, r, &dm->n_surface, c->stream);
+  for (int l = 0; l < layers; ++l) {
+    shl::launch_dilate(a, b, r, c->stream);
+    std::swap(a, b);
+  }
+  shl::launch_complete(a, b, r, &dm->touches, c->stream);
+  std::swap(a, b);
+  shl::launch_force_corners(a, r, &dm->touches, c->stream);
+  // norm on device: reuse the bits written by the field kernel
+  shl::launch_beta(a, c->centres.as<double>(), reinterpret_cast<const double*>(&dm->norm_bits),
+                   sp.sharpness, sp.floor_ratio, r, c->beta64.as<double>(), c->beta32.as<float>(),
+                   c->elem_flag.as<int>(), c->beta_partials.as<double>(), 0, c->stream);
+  c->launches += 4 + layers;
+  CK(cudaGetLastError());
+  if (a != c->occ0.as<uint8_t>()) {
+    // keep the final occupancy in occ0
+    CK(cudaMemcpyAsync(c->occ0.p, a, n3, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  build_topology_for(c, fp64_tiles);
+  c->n_surface = c->hmisc->n_surface;
+  if (c->n_surface == 0)
+    throw ShlError(SHL_DEGENERATE, "field has no zero crossing: no surface to mesh");
+  c->full_fallback = c->n_elem == static_cast<int64_t>(n3);
+  c->mesh_ready = true;
+}
+
+int resolve_precision(const shl_solve_options& o) {
+  if (o.precision >= SHL_PREC_FP64 && o.precision <= SHL_PREC_FP32) return o.precision;
+  return o.tol < 1e-7 ? SHL_PREC_FP64 : SHL_PREC_MIXED;
+}
+
+// ---- solve on the resident mesh ----------------------------------------------
+template <typename TX, typename TV>
+void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
+               shl_stats* st, int prec) {
+  const int r = c->r;
+  if (!c->node0_active)
+    throw ShlError(SHL_SOLVER,
+                   "mesh has no corner node group: cannot prescribe the strain gauge");
+  const int want_tiles = sizeof(TV) == 8 ? 0 : 1;
+  if (c->tile_prec != want_tiles) build_topology_for(c, sizeof(TV) == 8);
+  const int n = c->n_nodes;
+  const int ld = round_up(std::max(n, 1), 64);
+  const size_t nX = static_cast<size_t>(18) * ld, nV = nX;
+  c->vec.ensure(2 * nX * sizeof(TX) + (4 * nV + 6 * static_cast<size_t>(ld)) * sizeof(TV));
+  TX* x = c->vec.as<TX>();
+  TX* rv = x + nX;
+  TV* z = reinterpret_cast<TV*>(rv + nX);
+  TV* p0 = z + nV;
+  TV* p1 = p0 + nV;
+  TV* q = p1 + nV;
+  TV* dinv = q + nV;
+  const int grid_u = std::max(1, std::min((n + 255) / 256, c->num_sms * 8));
+  const int grid_c = std::max(1, std::min(static_cast<int>((c->n_elem + 31) / 32), c->num_sms * 16));
+  c->partials.ensure(sizeof(double) *
+                     std::max<size_t>({static_cast<size_t>(c->n_tiles) * 6,
+                                       static_cast<size_t>(grid_u) * 12,
+                                       static_cast<size_t>(grid_c) * 21, 64}));
+  c->state.ensure(sizeof(shl::PcgState));
+  c->cout.ensure(36 * sizeof(double));
+
+  double T[144], W[144];
+  element_loads(K0, r, T, W);
+  CK(cudaEventRecord(c->ev[3], c->stream));
+  shl::upload_element_constants(K0, W, T, c->stream);
+  CK(cudaMemsetAsync(x, 0, nX * sizeof(TX), c->stream));
+  CK(cudaMemsetAsync(p0, 0, 2 * nV * sizeof(TV), c->stream));
+  shl::launch_setup<TX, TV>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), rv, dinv,
+                            c->stream);
+  shl::PcgState hs{};
+  hs.tol = opt.tol;
+  hs.max_iter = opt.max_iter > 0 ? opt.max_iter : 20 * r + 2000;
+  std::memcpy(c->hstate, &hs, sizeof(hs));
+  CK(cudaMemcpyAsync(c->state.p, c->hstate, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaEventRecord(c->ev[4], c->stream));
+
+  shl::PcgState* dst = c->state.as<shl::PcgState>();
+  shl::UpdateArgs<TX, TV> ua{x, rv, p1, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1};
+  shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+  ua.init = 0;
+  const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
+                                         : reinterpret_cast<const TV*>(c->beta32.p);
+  shl::ApplyArgs<TV> aa{c->tile_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p0, p1, q,
+                        c->partials.as<double>(), dst, r, ld};
+  int64_t launches = 2 + 1;
+  int check = opt.check_every > 0 ? opt.check_every : (n < 200000 ? 16 : 32);
+  int parity = 0;
+  double apply_ms = 0.0, update_ms = 0.0;
+  int64_t apply_launches = 0;
+  for (;;) {
+    for (int it = 0; it < check; ++it) {
+      aa.pold = parity ? p1 : p0;
+      aa.pnew = parity ? p0 : p1;
+      ua.p = aa.pnew;
+      if (c->profiling) {
+        cudaEvent_t e0 = c->prof_ev[0], e1 = c->prof_ev[1], e2 = c->prof_ev[2];
+        CK(cudaEventRecord(e0, c->stream));
+        shl::launch_apply<TV>(aa, c->n_tiles, c->stream);
+        CK(cudaEventRecord(e1, c->stream));
+        shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+        CK(cudaEventRecord(e2, c->stream));
+        CK(cudaEventSynchronize(e2));
+        float ta = 0, tu = 0;
+        CK(cudaEventElapsedTime(&ta, e0, e1));
+        CK(cudaEventElapsedTime(&tu, e1, e2));
+        apply_ms += ta;
+        update_ms += tu;
+        ++apply_launches;
+      } else {
+        shl::launch_apply<TV>(aa, c->n_tiles, c->stream);
+        shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+      }
+      launches += 2;
+      parity ^= 1;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->hstate, c->state.p, sizeof(shl::PcgState), cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->sync();
+    if (c->hstate->stop) break;
+  }
+  CK(cudaEventRecord(c->ev[5], c->stream));
+  const shl::PcgState& fin = *c->hstate;
+  if (fin.error) throw ShlError(SHL_SOLVER, "grid CG: operator lost positive definiteness");
+  const bool converged = fin.all_done != 0;
+  if (!converged) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "grid CG did not reach tolerance %g in %d iterations", opt.tol,
+                  fin.max_iter);
+    throw ShlError(SHL_SOLVER, buf);
+  }
+  shl::ChomArgs<TX> ca{c->elem_list.as<int>(), c->node_map.as<int>(), c->beta64.as<double>(), x,
+                       c->partials.as<double>(), c->cout.as<double>(), dst,
+                       static_cast<int>(c->n_elem), r, ld};
+  shl::launch_chom<TX>(ca, grid_c, c->stream);
+  launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->hC, c->cout.p, 36 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaEventRecord(c->ev[6], c->stream));
+  c->sync();
+  std::memcpy(C_out, c->hC, 36 * sizeof(double));
+  c->launches += launches;
+  if (st) {
+    st->t_AS = c->ms(3, 4);
+    st->t_RHS = 0.0;
+    st->t_solve = c->ms(4, 5);
+    st->t_C = c->ms(5, 6);
+    for (int s = 0; s < 6; ++s) st->iterations[s] = fin.iters[s];
+    st->converged = converged;
+    st->precision = prec;
+    st->apply_ms = apply_ms;
+    st->update_ms = update_ms;
+    st->apply_launches = apply_launches;
+  }
+}
+
+void solve_dispatch(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
+                    shl_stats* st) {
+  const int prec = resolve_precision(opt);
+  switch (prec) {
+    case SHL_PREC_FP64: run_solve<double, double>(c, K0, opt, C_out, st, prec); break;
+    case SHL_PREC_MIXED: run_solve<double, float>(c, K0, opt, C_out, st, prec); break;
+    default: run_solve<float, float>(c, K0, opt, C_out, st, prec); break;
+  }
+}
+
+void fill_mesh_stats(shl_ctx* c, shl_stats* st) {
+  if (!st) return;
+  st->n_surface = c->n_surface;
+  st->n_elements = c->n_elem;
+  st->n_nodes = c->n_nodes;
+  st->n_tiles = c->n_tiles;
+  st->full_fallback = c->full_fallback;
+  st->norm = c->norm;
+  st->volume_ratio = c->volume_ratio;
+}
+
+shl_solve_options default_opts(const shl_solve_options* o) {
+  shl_solve_options d{};
+  d.tol = 1e-9;
+  d.max_iter = 0;
+  d.precision = SHL_PREC_AUTO;
+  d.check_every = 0;
+  if (o) d = *o;
+  if (!(d.tol > 0.0)) throw ShlError(SHL_VALIDATION, "solver tolerance must be positive");
+  return d;
+}
+
+void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params* sp,
+                    const shl_material* mat, int r, const shl_solve_options* o, double* C_out,
+                    shl_stats* st) {
+  if (!design || !sp || !mat || !C_out) throw ShlError(SHL_VALIDATION, "null argument");
+  const shl_solve_options opt = default_opts(o);
+  double K0[576];
+  shl::element_stiffness(mat->youngs, mat->poisson, 1.0 / std::max(r, 1), K0);  // mat.validate
+  if (!(sp->sharpness > 0.0)) throw ShlError(SHL_VALIDATION, "sharpness must be positive");
+  if (!(sp->floor_ratio > 0.0 && sp->floor_ratio < 1.0))
+    throw ShlError(SHL_VALIDATION, "floor must lie in (0, 1)");
+  if (sp->expand_layers < 0) throw ShlError(SHL_VALIDATION, "expand_layers must be >= 0");
+  const int64_t l0 = c->launches;
+  CK(cudaEventRecord(c->ev[0], c->stream));
+  tagged("field", [&] {
+    run_field(c, shl::HostDesign::from_abi(*design), r);
+    return 0;
+  });
+  CK(cudaEventRecord(c->ev[1], c->stream));
+  read_norm(c);
+  if (c->norm == 0.0) throw ShlError(SHL_DEGENERATE, "field: design is degenerate (norm = 0)");
+  const bool fp64 = resolve_precision(opt) == SHL_PREC_FP64;
+  tagged("mesh", [&] {
+    run_mesh(c, *sp, fp64);
+    return 0;
+  });
+  CK(cudaEventRecord(c->ev[2], c->stream));
+  tagged("solve", [&] {
+    solve_dispatch(c, K0, opt, C_out, st);
+    return 0;
+  });
+  c->sync();
+  if (st) {
+    st->t_field = c->ms(0, 1);
+    st->t_mesh = c->ms(1, 2);
+    st->t_PBC = 0.0;  // node pairing is the ordered compaction inside t_mesh
+    st->t_fwd = c->ms(0, 6);
+    fill_mesh_stats(c, st);
+    st->kernel_launches = c->launches - l0;
+  }
+}
+
+}  // namespace
+
+// =============================== C ABI =======================================
+extern "C" {
+
+int shl_ctx_create(int device, shl_ctx** out) {
+  if (!out) return SHL_VALIDATION;
+  *out = nullptr;
+  auto c = std::make_unique<shl_ctx>();
+  c->device = device;
+  int rc = guarded(nullptr, [&] {
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    c->prof_ev.resize(3);
+    for (auto& e : c->prof_ev) CK(cudaEventCreate(&e));
+    CK(cudaMallocHost(&c->hmisc, sizeof(Misc)));
+    CK(cudaMallocHost(&c->hstate, sizeof(shl::PcgState)));
+    CK(cudaMallocHost(&c->hC, 36 * sizeof(double)));
+  });
+  if (rc != SHL_OK) return rc;
+  *out = c.release();
+  return SHL_OK;
+}
+
+void shl_ctx_destroy(shl_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->prof_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->hmisc) cudaFreeHost(c->hmisc);
+  if (c->hstate) cudaFreeHost(c->hstate);
+  if (c->hC) cudaFreeHost(c->hC);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* shl_last_error(const shl_ctx* c) {
+  return c ? c->err.c_str() : g_thread_error.c_str();
+}
+
+int shl_set_profiling(shl_ctx* c, int on) {
+  if (!c) return SHL_VALIDATION;
+  c->profiling = on != 0;
+  return SHL_OK;
+}
+
+int shl_sample_grid(shl_ctx* c, const shl_design* design, int r, double* centres, double* corners,
+                    double* norm) {
+  if (!c || !design) return SHL_VALIDATION;
+  return guarded(c, [&] {
+    run_field(c, shl::HostDesign::from_abi(*design), r);
+    read_norm(c);
+    const size_t n3 = static_cast<size_t>(r) * r * r;
+    if (centres)
+      CK(cudaMemcpy(centres, c->centres.p, n3 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (corners) {
+      std::vector<double> u(n3);
+      CK(cudaMemcpy(u.data(), c->corners.p, n3 * sizeof(double), cudaMemcpyDeviceToHost));
+      const int r1 = r + 1;
+      for (int k = 0; k < r1; ++k)
+        for (int j = 0; j < r1; ++j)
+          for (int i = 0; i < r1; ++i)
+            corners[(static_cast<size_t>(k) * r1 + j) * r1 + i] =
+                u[(static_cast<size_t>(k % r) * r + j % r) * r + i % r];
+    }
+    if (norm) *norm = c->norm;
+  });
+}
+
+int shl_load_grid(shl_ctx* c, int r, const double* centres, const double* corners, double norm) {
+  if (!c || !centres || !corners) return SHL_VALIDATION;
+  return guarded(c, [&] {
+    require_r(r);
+    alloc_grid(c, r);
+    c->grid_ready = c->mesh_ready = false;
+    const size_t n3 = static_cast<size_t>(r) * r * r;
+    std::vector<double> u(n3);
+    const int r1 = r + 1;
+    for (int k = 0; k < r; ++k)
+      for (int j = 0; j < r; ++j)
+        for (int i = 0; i < r; ++i)
+          u[(static_cast<size_t>(k) * r + j) * r + i] = corners[(static_cast<size_t>(k) * r1 + j) * r1 + i];
+    CK(cudaMemcpy(c->centres.p, centres, n3 * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->corners.p, u.data(), n3 * sizeof(double), cudaMemcpyHostToDevice));
+    Misc m{};
+    std::memcpy(&m.norm_bits, &norm, sizeof(double));
+    CK(cudaMemcpy(c->misc.p, &m, sizeof(Misc), cudaMemcpyHostToDevice));
+    shl::launch_corner_signs(c->corners.as<double>(), c->csign.as<int8_t>(), r, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+    c->norm = norm;
+    c->grid_ready = true;
+  });
+}
+
+int shl_classify_surface(shl_ctx* c, uint32_t* elements, int64_t* n_surface) {
+  if (!c) return SHL_VALIDATION;
+  return guarded(c, [&] {
+    if (!c->grid_ready) throw ShlError(SHL_VALIDATION, "no resident grid");
+    if (c->norm == 0.0)
+      throw ShlError(SHL_DEGENERATE, "cannot classify surface elements of a degenerate field");
+    const int r = c->r;
+    const size_t n3 = static_cast<size_t>(r) * r * r;
+    c->occ1.ensure(n3);
+    Misc* dm = c->misc.as<Misc>();
+    CK(cudaMemsetAsync(&dm->n_surface, 0, sizeof(int), c->stream));
+    shl::launch_classify(c->csign.as<int8_t>(), c->occ1.as<uint8_t>(), r, &dm->n_surface, c->stream);
+    std::vector<uint8_t> occ(n3);
+    CK(cudaMemcpyAsync(occ.data(), c->occ1.p, n3, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    int64_t cnt = 0;
+    for (size_t e = 0; e < n3; ++e)
+      if (occ[e]) {
+        if (elements) elements[cnt] = static_cast<uint32_t>(e);
+        ++cnt;
+      }
+    if (n_surface) *n_surface = cnt;
+    c->mesh_ready = false;
+  });
+}
+
+int shl_build_reduced_mesh(shl_ctx* c, const shl_shell_params* sp, uint32_t* elements,
+                           double* beta, int64_t* n_elements, int32_t* full_fallback) {
+  if (!c || !sp) return SHL_VALIDATION;
+  return guarded(c, [&] {
+    run_mesh(c, *sp, false);
+    const int r = c->r;
+    const size_t n3 = static_cast<size_t>(r) * r * r;
+    if (elements || beta) {
+      std::vector<int> el(c->n_elem);
+      if (c->n_elem)
+        CK(cudaMemcpy(el.data(), c->elem_list.p, el.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      if (elements)
+        for (size_t q = 0; q < el.size(); ++q) elements[q] = static_cast<uint32_t>(el[q]);
+      if (beta) {
+        std::vector<double> b(n3);
+        CK(cudaMemcpy(b.data(), c->beta64.p, n3 * sizeof(double), cudaMemcpyDeviceToHost));
+        for (size_t q = 0; q < el.size(); ++q) beta[q] = b[el[q]];
+      }
+    }
+    if (n_elements) *n_elements = c->n_elem;
+    if (full_fallback) *full_fallback = c->full_fallback;
+  });
+}
+
+int shl_grid_solve(shl_ctx* c, int r, const double* beta, const double* K0,
+                   const shl_solve_options* o, double* C_out, shl_stats* st) {
+  if (!c || !beta || !K0 || !C_out) return SHL_VALIDATION;
+  return guarded(c, [&] {
+    require_r(r);
+    const shl_solve_options opt = default_opts(o);
+    const size_t n3 = static_cast<size_t>(r) * r * r;
+    for (size_t e = 0; e < n3; ++e)
+      if (!(beta[e] >= 0.0)) throw ShlError(SHL_VALIDATION, "beta must be >= 0");
+    const int64_t l0 = c->launches;
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    alloc_grid(c, r);
+    c->grid_ready = false;
+    c->occ0.ensure(n3);
+    c->beta64.ensure(n3 * sizeof(double));
+    c->beta32.ensure(n3 * sizeof(float));
+    c->elem_flag.ensure(n3 * sizeof(int));
+    c->beta_partials.ensure(((n3 + 255) / 256) * 2 * sizeof(double));
+    CK(cudaMemsetAsync(c->beta_partials.p, 0, ((n3 + 255) / 256) * 2 * sizeof(double), c->stream));
+    CK(cudaMemcpyAsync(c->beta64.p, beta, n3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    shl::launch_beta_from_dense(c->beta64.as<double>(), r, c->beta32.as<float>(),
+                                c->elem_flag.as<int>(), c->occ0.as<uint8_t>(), c->stream);
+    c->launches += 1;
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    build_topology_for(c, resolve_precision(opt) == SHL_PREC_FP64);
+    double s = 0.0;
+    for (size_t e = 0; e < n3; ++e) s += beta[e];
+    c->volume_ratio = s / double(n3);
+    c->n_surface = 0;
+    c->full_fallback = c->n_elem == static_cast<int64_t>(n3);
+    c->mesh_ready = true;
+    if (c->n_elem == 0) throw ShlError(SHL_DEGENERATE, "no elements with beta > 0");
+    solve_dispatch(c, K0, opt, C_out, st);
+    if (st) {
+      st->t_field = 0.0;
+      st->t_mesh = c->ms(0, 2);
+      st->t_PBC = 0.0;
+      st->t_fwd = c->ms(0, 6);
+      fill_mesh_stats(c, st);
+      st->kernel_launches = c->launches - l0;
+    }
+  });
+}
+
+int shl_solve_mesh(shl_ctx* c, const double* K0, const shl_solve_options* o, double* C_out,
+                   shl_stats* st) {
+  if (!c || !K0 || !C_out) return SHL_VALIDATION;
+  return guarded(c, [&] {
+    if (!c->mesh_ready) throw ShlError(SHL_VALIDATION, "no resident mesh: call shl_build_reduced_mesh");
+    const shl_solve_options opt = default_opts(o);
+    const int64_t l0 = c->launches;
+    solve_dispatch(c, K0, opt, C_out, st);
+    if (st) {
+      st->t_fwd = c->ms(3, 6);
+      fill_mesh_stats(c, st);
+      st->kernel_launches = c->launches - l0;
+    }
+  });
+}
+
+int shl_homogenize(shl_ctx* c, const shl_design* design, const shl_shell_params* sp,
+                   const shl_material* mat, int r, const shl_solve_options* opt, double* C_out,
+                   shl_stats* st) {
+  if (!c) return SHL_VALIDATION;
+  if (st) std::memset(st, 0, sizeof(*st));
+  return guarded(c, [&] { homogenize_one(c, design, sp, mat, r, opt, C_out, st); });
+}
+
+int shl_homogenize_batch(shl_ctx* c, int n, const shl_design* designs, const shl_shell_params* sp,
+                         const shl_material* mat, int r, const shl_solve_options* opt,
+                         double* C_out, shl_stats* stats, int32_t* status) {
+  if (!c || n < 0 || (n > 0 && (!designs || !C_out))) return SHL_VALIDATION;
+  for (int i = 0; i < n; ++i) {
+    shl_stats* st = stats ? stats + i : nullptr;
+    if (st) std::memset(st, 0, sizeof(*st));
+    const int rc =
+        guarded(c, [&] { homogenize_one(c, designs + i, sp, mat, r, opt, C_out + 36 * i, st); });
+    if (status) status[i] = rc;
+    if (rc == SHL_CUDA) return rc;
+  }
+  return SHL_OK;
+}
+
+int shl_element_stiffness(const shl_material* mat, double edge, double* K) {
+  if (!mat || !K) return SHL_VALIDATION;
+  return guarded(nullptr, [&] { shl::element_stiffness(mat->youngs, mat->poisson, edge, K); });
+}
+
+int shl_random_design(int symmetry, int n_pre, int K, double lo, double hi, uint64_t seed,
+                      double* positions, int32_t* signs, double* weights) {
+  return guarded(nullptr, [&] {
+    shl::HostDesign d = shl::random_design(symmetry, n_pre, K, lo, hi, seed);
+    std::copy(d.pos.begin(), d.pos.end(), positions);
+    std::copy(d.sign.begin(), d.sign.end(), signs);
+    std::copy(d.weights.begin(), d.weights.end(), weights);
+  });
+}
+
+int shl_expand_symmetry(const shl_design* design, double* positions_out, int32_t* signs_out,
+                        int32_t* n_out) {
+  if (!design) return SHL_VALIDATION;
+  return guarded(nullptr, [&] {
+    shl::HostDesign e = shl::HostDesign::from_abi(*design).expanded();
+    std::copy(e.pos.begin(), e.pos.end(), positions_out);
+    std::copy(e.sign.begin(), e.sign.end(), signs_out);
+    if (n_out) *n_out = static_cast<int32_t>(e.sign.size());
+  });
+}
+
+}  // extern "C"

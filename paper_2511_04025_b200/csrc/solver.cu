@@ -1,0 +1,514 @@
+// solver.cu -- K3..K6: matrix-free six-load-case PCG on the masked torus (sm_100a).
+//
+// The reference's GridSolver (grid_solver.hpp:18-207) generalized to the
+// reduced shell mesh: absent elements carry beta = 0, torus nodes touched by
+// no present element carry no unknowns, node 0 is pinned (the corner gauge of
+// build_periodic_system, fem.hpp:190-203; equivalence argued in SURVEY.md
+// row A14 and pinned in tests/test_oracle_fem.py).
+//
+// Storage: active nodes are numbered in grid order (voxel.cu); every PCG
+// vector is 18 planes [comp*6 + loadcase][node] so consecutive active nodes
+// are consecutive addresses (coalesced, no bytes spent on void voxels).
+//
+//   K3 rhs_kernel      b_n = -sum_e beta_e (K0 T)_{a(e,n)}      grid_solver.hpp:141-152
+//   K4 apply_kernel    p = z + beta p_old (deferred direction update), then
+//                      q = A p for a 3-D tile, node-centric gather (no
+//                      atomics): per neighbour m the 3x3 block
+//                      S_m = sum_{e ni n,m} beta_e K0[a,b] is built once and
+//                      applied to all six load cases; partial p.q
+//   K5 update_kernel   x += alpha p, r -= alpha q, z = Dinv r, partial r.z, r.r
+//   K6 chom_kernel     C_ab = sum_e beta_e (x_e+T)_a^T K0 (x_e+T)_b        :183-197
+//
+// Scalars never leave the device: the last block of each reduction kernel
+// (fixed-order sum of the per-block partials -> deterministic) updates the
+// PcgState, so the host only polls a flag every few iterations.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "solver.cuh"
+
+namespace shl {
+
+__constant__ double c_K0d[576];
+__constant__ float c_K0f[576];
+__constant__ double c_W[144];  // (K0 * T)[24][6]
+__constant__ double c_T[144];  // element-local affine displacements T[24][6]
+
+template <typename T>
+__device__ __forceinline__ T k0(int i);
+template <>
+__device__ __forceinline__ double k0<double>(int i) {
+  return c_K0d[i];
+}
+template <>
+__device__ __forceinline__ float k0<float>(int i) {
+  return c_K0f[i];
+}
+
+__host__ __device__ constexpr int corner_id(int x, int y, int z) {
+  return 4 * z + (y ? (x ? 2 : 3) : (x ? 1 : 0));
+}
+
+namespace {
+
+// ---- reductions -----------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void warp_sum(double (&v)[NV]) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+}
+
+// Block sum of NV doubles; result valid in thread 0.  scratch: 32*NV doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
+  warp_sum<NV>(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  if (l == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) scratch[w * NV + q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+      for (int u = 0; u < nw; ++u) s += scratch[u * NV + q];
+      v[q] = s;
+    }
+  }
+}
+
+// Writes this block's partial; returns true in exactly one block (the last to
+// finish), whose threads then see every partial.
+template <int NV>
+__device__ __forceinline__ bool publish_partial(const double (&v)[NV], double* partials,
+                                                uint32_t* counter) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) partials[blockIdx.x * NV + q] = v[q];
+    __threadfence();
+    const uint32_t t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// Fixed-order reduction of gridDim.x partials (called by the last block).
+template <int NV>
+__device__ __forceinline__ void reduce_partials(const double* partials, double (&out)[NV],
+                                                double* scratch) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) out[q] = 0.0;
+  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) out[q] += __ldcg(partials + b * NV + q);
+  block_sum<NV>(out, scratch);
+}
+
+// ---- K3 + preconditioner setup -------------------------------------------
+// One thread per active node: block-Jacobi inverse (grid_solver.hpp:129-139)
+// and the strain right-hand sides (grid_solver.hpp:141-152), node 0 pinned.
+template <typename TX, typename TV>
+__global__ void setup_kernel(const int* __restrict__ node_list, int n_nodes, int ld, int r,
+                             const double* __restrict__ beta64, TX* __restrict__ rvec,
+                             TV* __restrict__ dinv) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_nodes) return;
+  const int g = node_list[idx];
+  const int i = g % r, j = (g / r) % r, k = g / (r * r);
+  double D[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double b[18];
+#pragma unroll
+  for (int q = 0; q < 18; ++q) b[q] = 0.0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;  // node offset inside element
+    const int ei = i - ox < 0 ? r - 1 : i - ox, ej = j - oy < 0 ? r - 1 : j - oy,
+              ek = k - oz < 0 ? r - 1 : k - oz;
+    const double be = beta64[(static_cast<size_t>(ek) * r + ej) * r + ei];
+    if (be == 0.0) continue;
+    const int a = corner_id(ox, oy, oz);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) D[c * 3 + d] += be * c_K0d[(3 * a + c) * 24 + 3 * a + d];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) b[c * 6 + s] -= be * c_W[(3 * a + c) * 6 + s];
+    }
+  }
+  double inv[6] = {0, 0, 0, 0, 0, 0};  // symmetric: 00 01 02 11 12 22
+  if (g != 0) {
+    const double c00 = D[4] * D[8] - D[5] * D[7], c01 = D[5] * D[6] - D[3] * D[8],
+                 c02 = D[3] * D[7] - D[4] * D[6];
+    const double det = D[0] * c00 + D[1] * c01 + D[2] * c02;
+    const double id = 1.0 / det;
+    inv[0] = c00 * id;
+    inv[1] = c01 * id;
+    inv[2] = c02 * id;
+    inv[3] = (D[0] * D[8] - D[2] * D[6]) * id;
+    inv[4] = (D[2] * D[3] - D[0] * D[5]) * id;
+    inv[5] = (D[0] * D[4] - D[1] * D[3]) * id;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 18; ++q) b[q] = 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) dinv[static_cast<size_t>(q) * ld + idx] = static_cast<TV>(inv[q]);
+#pragma unroll
+  for (int q = 0; q < 18; ++q) rvec[static_cast<size_t>(q) * ld + idx] = static_cast<TX>(b[q]);
+}
+
+// ---- K4: fused direction update + K.u apply ---------------------------------
+template <typename TV, int TX, int TY, int TZ>
+__global__ void __launch_bounds__(TX* TY* TZ)
+    apply_kernel(const ApplyArgs<TV> A) {
+  constexpr int HX = TX + 2, HY = TY + 2, HZ = TZ + 2, HN = HX * HY * HZ;
+  constexpr int EX = TX + 1, EY = TY + 1, EZ = TZ + 1, EN = EX * EY * EZ;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TV* ps = reinterpret_cast<TV*>(smem_raw);  // [18][HN]
+  TV* bs = ps + 18 * HN;                      // [EN]
+  __shared__ double scratch[32 * 6];
+  PcgState* st = A.state;
+  if (st->stop) return;
+  const int r = A.r;
+  const int tile = A.tiles[blockIdx.x];
+  const int ntx = (r + TX - 1) / TX, nty = (r + TY - 1) / TY;
+  const int x0 = (tile % ntx) * TX, y0 = ((tile / ntx) % nty) * TY, z0 = (tile / (ntx * nty)) * TZ;
+  const size_t ld = A.ld;
+
+  TV bcoef[6];
+  bool dn[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    dn[s] = st->done[s] != 0;
+    bcoef[s] = static_cast<TV>(st->beta[s]);
+  }
+
+  // halo: p = z + beta * p_old for every active node of the (TX+2)(TY+2)(TZ+2) box
+  for (int h = threadIdx.x; h < HN; h += blockDim.x) {
+    const int hx = h % HX, hy = (h / HX) % HY, hz = h / (HX * HY);
+    const int gx = ((x0 - 1 + hx) % r + r) % r, gy = ((y0 - 1 + hy) % r + r) % r,
+              gz = ((z0 - 1 + hz) % r + r) % r;
+    const int idx = A.node_map[(static_cast<size_t>(gz) * r + gy) * r + gx];
+    const bool own = hx >= 1 && hx <= TX && hy >= 1 && hy <= TY && hz >= 1 && hz <= TZ &&
+                     x0 + hx - 1 < r && y0 + hy - 1 < r && z0 + hz - 1 < r;
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {
+      const int s = q % 6;
+      TV v = TV(0);
+      if (idx >= 0 && !dn[s]) v = A.z[q * ld + idx] + bcoef[s] * A.pold[q * ld + idx];
+      ps[q * HN + h] = v;
+      if (own && idx >= 0) A.pnew[q * ld + idx] = v;
+    }
+  }
+  for (int e = threadIdx.x; e < EN; e += blockDim.x) {
+    const int ex = e % EX, ey = (e / EX) % EY, ez = e / (EX * EY);
+    const int gx = ((x0 - 1 + ex) % r + r) % r, gy = ((y0 - 1 + ey) % r + r) % r,
+              gz = ((z0 - 1 + ez) % r + r) % r;
+    bs[e] = A.beta[(static_cast<size_t>(gz) * r + gy) * r + gx];
+  }
+  __syncthreads();
+
+  const int lx = threadIdx.x % TX, ly = (threadIdx.x / TX) % TY, lz = threadIdx.x / (TX * TY);
+  const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+  double pq[6] = {0, 0, 0, 0, 0, 0};
+  if (gx < r && gy < r && gz < r) {
+    const size_t gnode = (static_cast<size_t>(gz) * r + gy) * r + gx;
+    const int idx = A.node_map[gnode];
+    if (idx >= 0) {
+      TV y[18];
+#pragma unroll
+      for (int q = 0; q < 18; ++q) y[q] = TV(0);
+      if (gnode != 0) {
+        // beta of the 8 incident elements; element (ox,oy,oz) has its min
+        // corner at node - (1-ox, 1-oy, 1-oz)... indexed by the node's local
+        // corner inside it: e bit = node offset within the element.
+        TV be[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
+          be[e] = bs[((lz + 1 - oz) * EY + (ly + 1 - oy)) * EX + (lx + 1 - ox)];
+        }
+#pragma unroll
+        for (int m = 0; m < 27; ++m) {
+          const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+          TV S[9];
+#pragma unroll
+          for (int q = 0; q < 9; ++q) S[q] = TV(0);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;  // node's corner in e
+            const int bx = ox + dx, by = oy + dy, bz = oz + dz;         // neighbour's corner
+            if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+            const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int d = 0; d < 3; ++d) S[c * 3 + d] += be[e] * k0<TV>((3 * a + c) * 24 + 3 * b + d);
+          }
+          const int hn = ((lz + 1 + dz) * HY + (ly + 1 + dy)) * HX + (lx + 1 + dx);
+#pragma unroll
+          for (int s = 0; s < 6; ++s) {
+            const TV p0 = ps[(0 * 6 + s) * HN + hn], p1 = ps[(1 * 6 + s) * HN + hn],
+                     p2 = ps[(2 * 6 + s) * HN + hn];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) y[c * 6 + s] += S[c * 3 + 0] * p0 + S[c * 3 + 1] * p1 + S[c * 3 + 2] * p2;
+          }
+        }
+      }
+      const int hown = ((lz + 1) * HY + (ly + 1)) * HX + (lx + 1);
+#pragma unroll
+      for (int q = 0; q < 18; ++q) {
+        A.q[q * ld + idx] = y[q];
+        pq[q % 6] += static_cast<double>(ps[q * HN + hown]) * static_cast<double>(y[q]);
+      }
+    }
+  }
+  block_sum<6>(pq, scratch);
+  if (publish_partial<6>(pq, A.partials, &st->counter_apply)) {
+    double tot[6];
+    __syncthreads();
+    reduce_partials<6>(A.partials, tot, scratch);
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < 6; ++s) {
+        st->pq[s] = tot[s];
+        if (st->done[s]) {
+          st->alpha[s] = 0.0;
+        } else {
+          if (!(tot[s] > 0.0)) st->error = 1;
+          st->alpha[s] = st->rz[s] / tot[s];
+        }
+      }
+      if (st->error) st->stop = 1;
+      st->counter_apply = 0;
+    }
+  }
+}
+
+// ---- K5: vector update + preconditioner + dots ------------------------------
+template <typename TX, typename TV>
+__global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U) {
+  __shared__ double scratch[32 * 12];
+  PcgState* st = U.state;
+  if (st->stop) return;
+  const size_t ld = U.ld;
+  TX al[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) al[s] = static_cast<TX>(st->alpha[s]);
+  double acc[12];  // rr[0..5], rz[6..11]
+#pragma unroll
+  for (int q = 0; q < 12; ++q) acc[q] = 0.0;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < U.n; idx += gridDim.x * blockDim.x) {
+    TX rv[18];
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {
+      TX rq = U.r[q * ld + idx];
+      if (!U.init) {
+        const TX a = al[q % 6];
+        TX xq = U.x[q * ld + idx];
+        xq += a * static_cast<TX>(U.p[q * ld + idx]);
+        rq -= a * static_cast<TX>(U.q[q * ld + idx]);
+        U.x[q * ld + idx] = xq;
+        U.r[q * ld + idx] = rq;
+      }
+      rv[q] = rq;
+    }
+    TV D[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) D[q] = U.dinv[q * ld + idx];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const TV r0 = static_cast<TV>(rv[s]), r1 = static_cast<TV>(rv[6 + s]),
+               r2 = static_cast<TV>(rv[12 + s]);
+      const TV z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
+      const TV z1 = D[1] * r0 + D[3] * r1 + D[4] * r2;
+      const TV z2 = D[2] * r0 + D[4] * r1 + D[5] * r2;
+      U.z[s * ld + idx] = z0;
+      U.z[(6 + s) * ld + idx] = z1;
+      U.z[(12 + s) * ld + idx] = z2;
+      const double d0 = rv[s], d1 = rv[6 + s], d2 = rv[12 + s];
+      acc[s] += d0 * d0 + d1 * d1 + d2 * d2;
+      acc[6 + s] += d0 * static_cast<double>(z0) + d1 * static_cast<double>(z1) +
+                    d2 * static_cast<double>(z2);
+    }
+  }
+  block_sum<12>(acc, scratch);
+  if (publish_partial<12>(acc, U.partials, &st->counter_update)) {
+    double tot[12];
+    __syncthreads();
+    reduce_partials<12>(U.partials, tot, scratch);
+    if (threadIdx.x == 0) {
+      bool all = true;
+      for (int s = 0; s < 6; ++s) {
+        st->rr[s] = tot[s];
+        const double rn = sqrt(tot[s]);
+        if (U.init) {
+          st->bnorm[s] = rn;
+          st->rz[s] = tot[6 + s];
+          st->done[s] = rn == 0.0;
+          st->beta[s] = 0.0;
+          st->iters[s] = 0;
+        } else if (!st->done[s]) {
+          st->iters[s] = st->it + 1;
+          if (rn <= st->tol * st->bnorm[s]) {
+            st->done[s] = 1;
+            st->beta[s] = 0.0;
+          } else {
+            st->beta[s] = tot[6 + s] / st->rz[s];
+            st->rz[s] = tot[6 + s];
+          }
+        }
+        all = all && st->done[s];
+      }
+      if (!U.init) st->it += 1;
+      st->all_done = all;
+      st->stop = all || st->error || st->it >= st->max_iter;
+      st->counter_update = 0;
+    }
+  }
+}
+
+// ---- K6: C^H energy reduction ------------------------------------------------
+// One thread per active element; U = x_e + T (24x6) staged in shared memory,
+// the 21 upper-triangle accumulators too, W = K0 U_b per column in registers.
+template <typename TX>
+__global__ void __launch_bounds__(32) chom_kernel(const ChomArgs<TX> Cg) {
+  __shared__ double scratch[32 * 21];
+  __shared__ double Us[32][145];
+  __shared__ double As[32][21];
+  PcgState* st = Cg.state;
+  const int r = Cg.r;
+  double* U = Us[threadIdx.x];
+  double* acc_s = As[threadIdx.x];
+  for (int q = 0; q < 21; ++q) acc_s[q] = 0.0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < Cg.n_elem; t += gridDim.x * blockDim.x) {
+    const int e = Cg.elem_list[t];
+    const int i = e % r, j = (e / r) % r, k = e / (r * r);
+    const double be = Cg.beta64[e];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int gx = (i + (n == 1 || n == 2 || n == 5 || n == 6)) % r;
+      const int gy = (j + (n == 2 || n == 3 || n == 6 || n == 7)) % r;
+      const int gz = (k + (n >= 4)) % r;
+      const int idx = Cg.node_map[(static_cast<size_t>(gz) * r + gy) * r + gx];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int s = 0; s < 6; ++s)
+          U[(3 * n + c) * 6 + s] =
+              (idx >= 0 ? static_cast<double>(Cg.x[(c * 6 + s) * static_cast<size_t>(Cg.ld) + idx]) : 0.0) +
+              c_T[(3 * n + c) * 6 + s];
+    }
+#pragma unroll 1
+    for (int b = 0; b < 6; ++b) {
+      double W[24];
+#pragma unroll
+      for (int ii = 0; ii < 24; ++ii) {
+        double w = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < 24; ++jj) w += c_K0d[ii * 24 + jj] * U[jj * 6 + b];
+        W[ii] = w;
+      }
+#pragma unroll 1
+      for (int a = 0; a <= b; ++a) {
+        double d = 0.0;
+#pragma unroll
+        for (int ii = 0; ii < 24; ++ii) d += U[ii * 6 + a] * W[ii];
+        acc_s[b * (b + 1) / 2 + a] += be * d;
+      }
+    }
+  }
+  double acc[21];
+#pragma unroll
+  for (int q = 0; q < 21; ++q) acc[q] = acc_s[q];
+  block_sum<21>(acc, scratch);
+  if (publish_partial<21>(acc, Cg.partials, &st->counter_misc)) {
+    double tot[21];
+    __syncthreads();
+    reduce_partials<21>(Cg.partials, tot, scratch);
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < 6; ++b)
+        for (int a = 0; a <= b; ++a) {
+          Cg.C_out[a * 6 + b] = tot[b * (b + 1) / 2 + a];
+          Cg.C_out[b * 6 + a] = tot[b * (b + 1) / 2 + a];
+        }
+      st->counter_misc = 0;
+    }
+  }
+}
+
+}  // namespace
+
+// ---- host-side launchers -----------------------------------------------------
+void upload_element_constants(const double* K0, const double* W, const double* T,
+                              cudaStream_t s) {
+  float K0f[576];
+  for (int q = 0; q < 576; ++q) K0f[q] = static_cast<float>(K0[q]);
+  cudaMemcpyToSymbolAsync(c_K0d, K0, sizeof(double) * 576, 0, cudaMemcpyHostToDevice, s);
+  cudaMemcpyToSymbolAsync(c_K0f, K0f, sizeof(float) * 576, 0, cudaMemcpyHostToDevice, s);
+  cudaMemcpyToSymbolAsync(c_W, W, sizeof(double) * 144, 0, cudaMemcpyHostToDevice, s);
+  cudaMemcpyToSymbolAsync(c_T, T, sizeof(double) * 144, 0, cudaMemcpyHostToDevice, s);
+  // the float copy lives on the stack: make sure it has been consumed
+  cudaStreamSynchronize(s);
+}
+
+template <typename TX, typename TV>
+void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64, TX* rvec,
+                  TV* dinv, cudaStream_t s) {
+  if (n_nodes == 0) return;
+  setup_kernel<TX, TV><<<(n_nodes + 127) / 128, 128, 0, s>>>(node_list, n_nodes, ld, r, beta64,
+                                                            rvec, dinv);
+}
+
+template <typename TV>
+size_t apply_smem_bytes() {
+  constexpr int TX = TileShape<TV>::X, TY = TileShape<TV>::Y, TZ = TileShape<TV>::Z;
+  return sizeof(TV) * (18 * (TX + 2) * (TY + 2) * (TZ + 2) + (TX + 1) * (TY + 1) * (TZ + 1));
+}
+
+template <typename TV>
+void launch_apply(const ApplyArgs<TV>& a, int n_tiles, cudaStream_t s) {
+  constexpr int TX = TileShape<TV>::X, TY = TileShape<TV>::Y, TZ = TileShape<TV>::Z;
+  const size_t smem = apply_smem_bytes<TV>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(apply_kernel<TV, TX, TY, TZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    configured = true;
+  }
+  apply_kernel<TV, TX, TY, TZ><<<n_tiles, TX * TY * TZ, smem, s>>>(a);
+}
+
+template <typename TX, typename TV>
+void launch_update(const UpdateArgs<TX, TV>& u, int grid, cudaStream_t s) {
+  update_kernel<TX, TV><<<grid, 256, 0, s>>>(u);
+}
+
+template <typename TX>
+void launch_chom(const ChomArgs<TX>& c, int grid, cudaStream_t s) {
+  chom_kernel<TX><<<grid, 32, 0, s>>>(c);
+}
+
+template void launch_setup<double, double>(const int*, int, int, int, const double*, double*,
+                                           double*, cudaStream_t);
+template void launch_setup<double, float>(const int*, int, int, int, const double*, double*, float*,
+                                          cudaStream_t);
+template void launch_setup<float, float>(const int*, int, int, int, const double*, float*, float*,
+                                         cudaStream_t);
+template size_t apply_smem_bytes<double>();
+template size_t apply_smem_bytes<float>();
+template void launch_apply<double>(const ApplyArgs<double>&, int, cudaStream_t);
+template void launch_apply<float>(const ApplyArgs<float>&, int, cudaStream_t);
+template void launch_update<double, double>(const UpdateArgs<double, double>&, int, cudaStream_t);
+template void launch_update<double, float>(const UpdateArgs<double, float>&, int, cudaStream_t);
+template void launch_update<float, float>(const UpdateArgs<float, float>&, int, cudaStream_t);
+template void launch_chom<double>(const ChomArgs<double>&, int, cudaStream_t);
+template void launch_chom<float>(const ChomArgs<float>&, int, cudaStream_t);
+
+}  // namespace shl

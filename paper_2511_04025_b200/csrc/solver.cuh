@@ -1,0 +1,82 @@
+// solver.cuh -- argument blocks and launchers of the PCG kernels (solver.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "device.cuh"
+
+namespace shl {
+
+// Apply tile (nodes) per precision: 32 x-consecutive nodes per warp row.
+template <typename TV>
+struct TileShape;
+template <>
+struct TileShape<float> {
+  static constexpr int X = 32, Y = 4, Z = 2;
+};
+template <>
+struct TileShape<double> {
+  static constexpr int X = 32, Y = 2, Z = 2;
+};
+
+template <typename TV>
+struct ApplyArgs {
+  const int* tiles;
+  const int* node_map;  // r^3 -> active node id or -1
+  const TV* beta;       // r^3 dense, 0 = absent
+  const TV* z;
+  const TV* pold;
+  TV* pnew;
+  TV* q;
+  double* partials;
+  PcgState* state;
+  int r;
+  int ld;
+};
+
+template <typename TX, typename TV>
+struct UpdateArgs {
+  TX* x;
+  TX* r;
+  const TV* p;
+  const TV* q;
+  TV* z;
+  const TV* dinv;
+  double* partials;
+  PcgState* state;
+  int n;
+  int ld;
+  int init;
+};
+
+template <typename TX>
+struct ChomArgs {
+  const int* elem_list;
+  const int* node_map;
+  const double* beta64;
+  const TX* x;
+  double* partials;
+  double* C_out;
+  PcgState* state;
+  int n_elem;
+  int r;
+  int ld;
+};
+
+void upload_element_constants(const double* K0, const double* W, const double* T, cudaStream_t s);
+template <typename TX, typename TV>
+void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64, TX* rvec,
+                  TV* dinv, cudaStream_t s);
+template <typename TV>
+size_t apply_smem_bytes();
+template <typename TV>
+void launch_apply(const ApplyArgs<TV>& a, int n_tiles, cudaStream_t s);
+template <typename TX, typename TV>
+void launch_update(const UpdateArgs<TX, TV>& u, int grid, cudaStream_t s);
+template <typename TX>
+void launch_chom(const ChomArgs<TX>& c, int grid, cudaStream_t s);
+
+}  // namespace shl

@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): field samples and the voxel mask bit-exact in
+FP64; beta within 1e-12 relative (device exp vs glibc exp); C^H within 1e-4
+relative Frobenius of the oracle, with iteration counts reported; the
+reference's known-answer tests (test_fem.cpp) at their own tolerances.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_max(a, b):
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+def rel_fro(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def pair(S, O, kind, seed=1, n_pre=4):
+    """(product design, oracle design) built independently from the same seed."""
+    if kind == "gyroid":
+        od = O.gyroid_design()
+        return S.DesignParams("none", 2, od.positions, od.signs, od.weights), od
+    if kind == "plane":
+        od = O.plane_design_z(0.5 / 32)
+        return S.DesignParams("none", 2, od.positions, od.signs, od.weights), od
+    sd = S.random_design(S.RandomDesignSpec(kind, n_pre, 2, -1.0, 1.0), seed)
+    od = O.random_design(kind, n_pre, 2, -1.0, 1.0, seed)
+    assert np.array_equal(sd.positions, od.positions)
+    assert np.array_equal(sd.weights, od.weights)
+    return sd, od
+
+
+FIELD_CASES = [("cubic_octant", 3, 4, 16), ("cubic_octant", 12, 4, 16), ("cubic_octant", 1, 2, 32),
+               ("none", 7, 64, 32), ("tetrahedral", 5, 2, 16), ("cubic_octant", 2024, 4, 64),
+               ("gyroid", 0, 0, 64), ("plane", 0, 0, 32), ("cubic_octant", 11, 8, 8),
+               ("none", 3, 4, 5)]
+
+
+@pytest.mark.parametrize("kind,seed,n_pre,r", FIELD_CASES)
+def test_field_bit_exact(S, O, kind, seed, n_pre, r):
+    sd, od = pair(S, O, kind, seed, n_pre)
+    g = S.sample_grid(sd, r)
+    og = O.sample_grid(od, r)
+    assert np.array_equal(g.samples, og.samples)
+    assert np.array_equal(g.corner_samples, og.corners)
+    assert g.norm == og.norm
+
+
+@pytest.mark.parametrize("kind,seed,n_pre,r", FIELD_CASES)
+def test_mask_exact(S, O, kind, seed, n_pre, r):
+    sd, od = pair(S, O, kind, seed, n_pre)
+    og = O.sample_grid(od, r)
+    om = O.build_reduced_mesh(og)
+    m = S.build_reduced_mesh(S.sample_grid(sd, r), S.ShellParams())
+    assert np.array_equal(m.elements, om.elements)
+    ob = om.beta.reshape(-1)[om.elements]
+    assert np.abs(m.beta - ob).max() <= 1e-12 * np.abs(ob).max()
+    assert m.full_fallback == om.full_fallback
+
+
+def test_classify_matches_oracle(S, O):
+    sd, od = pair(S, O, "gyroid")
+    g = S.sample_grid(sd, 64)
+    surf = S.classify_surface_elements(g)
+    og = O.sample_grid(od, 64)
+    m1 = O.build_reduced_mesh(og, expand_layers=1)
+    assert len(surf) == O.build_reduced_mesh(og).n_surface
+    assert set(surf.tolist()) <= set(m1.elements.tolist())
+
+
+def test_plane_two_slabs(S):
+    """test_voxel.cpp:144-152: off-lattice plane -> exactly 2 r^2 surface voxels."""
+    r = 32
+    w = np.zeros(27)
+    w[1] = 1.0
+    p = S.DesignParams("none", 2, np.array([[0.5, 0.5, 0.25 + 0.5 / r], [0.5, 0.5, 0.75 + 0.5 / r]]),
+                       np.array([1, -1], np.int32), w)
+    surf = S.classify_surface_elements(S.sample_grid(p, r))
+    assert len(surf) == 2 * r * r
+    assert len(set((surf // (r * r)).tolist())) == 2
+
+
+def test_schwarz_p_classification(S):
+    """test_voxel.cpp:166-187 (host-sampled analytic field through shl_load_grid)."""
+    f = lambda x, y, z: np.cos(2 * np.pi * x) + np.cos(2 * np.pi * y) + np.cos(2 * np.pi * z)
+    r = 32
+    g = S.sample_grid_fn(f, r)
+    got = set(S.classify_surface_elements(g).tolist())
+    c = g.corner_samples
+    want = set()
+    for k in range(r):
+        for j in range(r):
+            for i in range(r):
+                blk = c[k:k + 2, j:j + 2, i:i + 2]
+                if blk.min() <= 0.0 <= blk.max():
+                    want.add((k * r + j) * r + i)
+    assert got == want
+
+
+@pytest.mark.parametrize("seed,r,prec,tol,bar", [(3, 16, "fp64", 1e-11, 1e-8), (12, 16, "fp64", 1e-11, 1e-8),
+                                                 (5, 16, "mixed", 1e-6, 1e-5), (21, 16, "fp32", 1e-5, 1e-4)])
+def test_grid_solve_vs_oracle(S, O, seed, r, prec, tol, bar):
+    od = O.seeded_design(seed)
+    om = O.build_reduced_mesh(O.sample_grid(od, r))
+    K0 = O.element_stiffness(1.0, 0.3, 1.0 / r)
+    ref = O.grid_solve(om.beta, K0, tol=1e-11)
+    res = S.GridSolver(om.beta, r, K0, precision=prec).solve(tol)
+    assert rel_max(res.tensor, ref.C) < bar
+    assert np.all(res.iterations > 0)
+    if prec == "fp64":
+        # same algorithm, same arithmetic class: iteration counts agree closely
+        assert np.abs(res.iterations - O.grid_solve(om.beta, K0, tol=tol).iterations).max() <= 2
+
+
+def test_full_solid_isotropic(S):
+    """test_fem.cpp:183-195."""
+    r = 4
+    K0 = S.element_stiffness(S.BaseMaterial(), 1.0 / r)
+    res = S.GridSolver(np.ones(r ** 3), r, K0, precision="fp64").solve(1e-12)
+    iso = S.isotropic_tensor(S.BaseMaterial())
+    assert rel_max(res.tensor, iso) < 1e-6
+    assert iso[0, 0] == pytest.approx(1.34615384615, rel=1e-9)
+
+
+def test_laminate_constants(S, O):
+    """test_fem.cpp:197-218 at the reference tolerance 1e-8."""
+    from oracle import direct as D
+    r = 8
+    layers = [1.0, 0.4, 1e-3, 0.02, 1.0, 0.7, 1e-3, 0.15]
+    beta = np.repeat(np.array(layers), r * r)
+    mat = S.BaseMaterial()
+    K0 = S.element_stiffness(mat, 1.0 / r)
+    C = S.GridSolver(beta, r, K0, precision="fp64").solve(1e-12).tensor
+    lam = D.laminate_constants(layers, mat.lam(), mat.mu())
+    assert C[0, 0] == pytest.approx(lam["C11"], rel=1e-8)
+    assert C[1, 1] == pytest.approx(lam["C11"], rel=1e-8)
+    assert C[0, 1] == pytest.approx(lam["C12"], rel=1e-8)
+    assert C[0, 2] == pytest.approx(lam["C13"], rel=1e-8)
+    assert C[2, 2] == pytest.approx(lam["C33"], rel=1e-8)
+    assert C[3, 3] == pytest.approx(lam["C44"], rel=1e-8)
+    assert C[4, 4] == pytest.approx(lam["C44"], rel=1e-8)
+    assert C[5, 5] == pytest.approx(lam["C66"], rel=1e-8)
+
+
+def test_grid_solver_matches_direct(S, O):
+    """test_fem.cpp:220-232: random-beta r=8 against the master-slave direct solve."""
+    from oracle import direct as D
+    r = 8
+    rng = np.random.default_rng(31)
+    beta = rng.uniform(0.05, 1.0, r ** 3)
+    K0 = O.element_stiffness(1.0, 0.3, 1.0 / r)
+    Cd = D.direct_homogenize(r, np.arange(r ** 3), beta, K0)[0]
+    Cg = S.GridSolver(beta, r, K0, precision="fp64").solve(1e-11).tensor
+    assert rel_max(Cg, Cd) < 1e-8
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_homogenize_c1_vs_oracle(S, O, seed):
+    """Config C1: 32^3, CubicOctant 2 pre (16 charges); C^H <= 1e-4 rel Frobenius."""
+    r = 32
+    sd, od = pair(S, O, "cubic_octant", seed, 2)
+    res = S.homogenize(sd, S.ShellParams(), S.BaseMaterial(), r,
+                       S.HomogenizeOptions(residual_tol=1e-5, precision="mixed"))
+    ref = O.homogenize(od, r, tol=1e-8)
+    assert rel_fro(res.tensor, ref.C) < 1e-4
+    assert res.stats.n_elements == ref.n_elements
+    assert res.stats.n_nodes == ref.n_nodes
+    assert res.volume_ratio == pytest.approx(ref.volume_ratio, rel=1e-12)
+    assert res.stats.converged
+
+
+def test_homogenize_gyroid_c2(S, O):
+    """Config C2: 64^3 gyroid fixture -> cubic C^H, against the oracle."""
+    r = 64
+    sd, od = pair(S, O, "gyroid")
+    res = S.homogenize(sd, S.ShellParams(), S.BaseMaterial(), r,
+                       S.HomogenizeOptions(residual_tol=1e-5, precision="mixed"))
+    C = res.tensor
+    assert abs(C[0, 0] - C[1, 1]) < 1e-4 * C[0, 0] and abs(C[0, 0] - C[2, 2]) < 1e-4 * C[0, 0]
+    assert abs(C[3, 3] - C[4, 4]) < 1e-4 * C[0, 0]
+    ref = O.homogenize(od, r, tol=1e-7)
+    assert rel_fro(C, ref.C) < 1e-4
+
+
+def test_errors_map_to_reference_classes(S):
+    r = 8
+    p = S.random_design(S.RandomDesignSpec("cubic_octant", 4), 5)
+    zero = S.DesignParams(p.symmetry, p.truncation, p.positions, p.signs, np.zeros(27))
+    with pytest.raises(S.DegenerateDesignError, match="field: design is degenerate"):
+        S.homogenize(zero, S.ShellParams(), S.BaseMaterial(), r)
+    with pytest.raises(S.ValidationError, match="field: grid resolution"):
+        S.homogenize(p, S.ShellParams(), S.BaseMaterial(), 3)
+    with pytest.raises(S.ValidationError):
+        S.homogenize(p, S.ShellParams(floor_ratio=1.5), S.BaseMaterial(), r)
+    with pytest.raises(S.ValidationError):
+        S.homogenize(p, S.ShellParams(), S.BaseMaterial(poisson=0.5), r)
+    bad = S.DesignParams("cubic_octant", 2, np.array([[0.7, 0.2, 0.2], [0.1, 0.1, 0.1]]),
+                         np.array([1, -1], np.int32), p.weights)
+    with pytest.raises(S.ValidationError, match="fundamental"):
+        S.homogenize(bad, S.ShellParams(), S.BaseMaterial(), r)
+    f = S.sample_grid_fn(lambda x, y, z: 1.0 + 0 * x, 8)
+    with pytest.raises(S.DegenerateDesignError, match="no zero crossing"):
+        S.build_reduced_mesh(f)
+
+
+def test_full_fallback_and_small_r(S, O):
+    """test_voxel.cpp:289-297 and pipeline r=8 full-fallback."""
+    sd, od = pair(S, O, "cubic_octant", 5, 4)
+    m = S.build_reduced_mesh(S.sample_grid(sd, 8), S.ShellParams(expand_layers=8))
+    assert m.full_fallback and m.num_elements() == 512
+    res = S.homogenize(sd, S.ShellParams(), S.BaseMaterial(), 8,
+                       S.HomogenizeOptions(residual_tol=1e-10))
+    ref = O.homogenize(od, 8, tol=1e-10)
+    assert rel_max(res.tensor, ref.C) < 1e-7
+    assert res.stats.full_fallback == ref.full_fallback
+
+
+def test_batch_matches_single(S):
+    designs = [S.random_design(S.RandomDesignSpec("cubic_octant", 2), s) for s in range(4)]
+    opt = S.HomogenizeOptions(residual_tol=1e-5, precision="mixed")
+    Cb, status, stats = S.homogenize_batch(designs, S.ShellParams(), S.BaseMaterial(), 16, opt)
+    assert np.all(status == 0)
+    for i, d in enumerate(designs):
+        Cs = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), 16, opt).tensor
+        assert np.array_equal(Cs, Cb[i])  # deterministic reductions
