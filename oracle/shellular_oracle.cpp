@@ -593,6 +593,11 @@ struct MaskedGridSolver {
   std::vector<std::uint8_t> node_on;
   std::vector<double> dinv;  // 9 per node
   double T[24][6];
+  // Diagonal ridge of the reference's singular-system path (fem.hpp:337-343):
+  // 1e-11 * mean|diag(A)|.  The reduced shell systems are semidefinite
+  // whenever a component floats; the ridge keeps p^T A p > 0 at
+  // rounding level and moves C^H by O(1e-11).
+  double ridge = 0.0;
 
   MaskedGridSolver(const std::vector<double>& b, int r_, const double* K, int thr)
       : r(r_), threads(thr), beta(b) {
@@ -638,6 +643,20 @@ struct MaskedGridSolver {
           for (int b = 0; b < 3; ++b) d[a * 3 + b] += be * K0[(3 * n + a) * 24 + 3 * n + b];
       }
     }
+    double dsum = 0.0;
+    size_t ndof = 0;
+    for (size_t n = 1; n < N; ++n)
+      if (node_on[n]) {
+        dsum += std::abs(diag[n * 9 + 0]) + std::abs(diag[n * 9 + 4]) + std::abs(diag[n * 9 + 8]);
+        ndof += 3;
+      }
+    ridge = ndof ? 1e-11 * dsum / double(ndof) : 0.0;
+    for (size_t n = 1; n < N; ++n)
+      if (node_on[n]) {
+        diag[n * 9 + 0] += ridge;
+        diag[n * 9 + 4] += ridge;
+        diag[n * 9 + 8] += ridge;
+      }
     dinv.assign(N * 9, 0.0);
     for (size_t n = 0; n < N; ++n) {
       if (!node_on[n] || n == 0) continue;
@@ -716,6 +735,8 @@ struct MaskedGridSolver {
     } else {
       for (int k = 0; k < r; ++k) work_layer(k);
     }
+    if (ridge != 0.0)
+      for (size_t q = 18; q < y.size(); ++q) y[q] += ridge * x[q];
     for (int q = 0; q < 18; ++q) y[q] = 0.0;
   }
 

@@ -1,0 +1,89 @@
+"""Generate tests/golden/*.npz from the reference's OWN field/voxel code.
+
+Run in the dev container (needs /root/reference and `make -C oracle ref`):
+
+    python tests/golden/make_golden.py
+
+oracle/_ref/libshellular_ref.so is the reference's field.hpp/voxel.hpp compiled
+unmodified (Eigen replaced by oracle/ref_shim).  The fixtures pin, bit for bit,
+random_design (field.hpp:569-593), expand_symmetry (:236-249), sample_grid
+(:488-534), classify_surface_elements (voxel.hpp:118-141), build_reduced_mesh
+(:235-313, incl. build_topology's node/group counts) and step_function
+(:38-41).  Small grids are stored whole; larger ones as SHA-256 digests.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import oracle as O  # noqa: E402
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# (name, design factory, resolutions stored whole, resolutions stored as digests)
+def cases():
+    out = []
+    for seed in (3, 12, 21, 2024):
+        out.append((f"seeded_{seed}", lambda s=seed: O.random_design("cubic_octant", 4, 2, -1, 1, s, use_ref=True),
+                    (8, 16), (32, 64) if seed == 2024 else (32,)))
+    out.append(("c1_seed1", lambda: O.random_design("cubic_octant", 2, 2, -1, 1, 1, use_ref=True), (16,), (32,)))
+    out.append(("none64_seed7", lambda: O.random_design("none", 64, 2, -1, 1, 7, use_ref=True), (8,), (32,)))
+    out.append(("tetra_seed5", lambda: O.random_design("tetrahedral", 2, 2, -1, 1, 5, use_ref=True), (8,), (16,)))
+    out.append(("c3_seed1", lambda: O.random_design("cubic_octant", 8, 2, -1, 1, 1, use_ref=True), (), (64,)))
+    out.append(("gyroid", O.gyroid_design, (16,), (32, 64)))
+    out.append(("plane_z", lambda: O.plane_design_z(0.5 / 32), (16,), (32,)))
+    return out
+
+
+def main() -> None:
+    if O.ref() is None:
+        raise SystemExit("oracle/_ref not built: make -C oracle ref (needs /root/reference)")
+    manifest = {}
+    arrays = {}
+    for name, make, whole, digest in cases():
+        d = make()
+        pe, se = O.expand_symmetry(d, use_ref=True)
+        arrays[f"{name}/positions"] = d.positions
+        arrays[f"{name}/signs"] = d.signs
+        arrays[f"{name}/weights"] = d.weights
+        arrays[f"{name}/symmetry"] = np.array([O.SYM[d.symmetry]])
+        arrays[f"{name}/expanded_positions"] = pe
+        arrays[f"{name}/expanded_signs"] = se
+        for r in tuple(whole) + tuple(digest):
+            g = O.sample_grid(d, r, use_ref=True)
+            el, be, info = O.ref_build_reduced_mesh(g)
+            key = f"{name}/r{r}"
+            if r in whole:
+                arrays[f"{key}/centres"] = g.samples
+                arrays[f"{key}/corners"] = g.corners
+                arrays[f"{key}/elements"] = el
+                arrays[f"{key}/beta"] = be
+            arrays[f"{key}/norm"] = np.array([g.norm])
+            arrays[f"{key}/info"] = np.array([info["n_elements"], info["n_nodes"], info["n_groups"],
+                                              info["corner_group"], int(info["full_fallback"]),
+                                              info["corner_group_size"]], np.int64)
+            manifest[key] = dict(centres=sha(g.samples), corners=sha(g.corners), elements=sha(el),
+                                 beta=sha(be))
+    vs = np.linspace(-0.3, 0.3, 121)
+    for sharp, fl in ((500.0, 1e-3), (140.0, 0.01), (100.0, 1e-3)):
+        arrays[f"step/{sharp}_{fl}"] = np.array([O.step_function(v, sharp, fl, use_ref=True) for v in vs])
+    arrays["step/v"] = vs
+    keys = sorted(manifest)
+    arrays["digest/keys"] = np.array(keys)
+    arrays["digest/values"] = np.array([[manifest[k][f] for f in ("centres", "corners", "elements", "beta")]
+                                        for k in keys])
+    np.savez_compressed(os.path.join(HERE, "reference_fixtures.npz"), **arrays)
+    print(f"wrote {len(arrays)} arrays, {len(keys)} grid digests")
+
+
+if __name__ == "__main__":
+    main()
