@@ -14,13 +14,15 @@ constexpr int kFieldChargeChunk = 128;
 
 // ---- PCG control block (one per solve, device resident) -------------------
 struct PcgState {
-  double alpha[6];
-  double beta[6];
-  double rz[6];
+  double alpha[6];   // step of the current iteration
+  double beta[6];    // gamma_{k+1} / gamma_k
+  double gamma[6];   // r.z of the current residual
+  double delta[6];   // z.Az
+  double pap[6];     // p.Ap (Chronopoulos-Gear recurrence)
   double bnorm[6];
   double rr[6];
-  double pq[6];
   double tol;
+  double ridge;      // diagonal ridge (fem.hpp:337-343), added to A
   int32_t done[6];
   int32_t iters[6];
   int32_t it;
@@ -52,8 +54,7 @@ void launch_beta(const uint8_t* occ, const double* centres, const double* norm, 
                  double* partial, int nblocks_partial, cudaStream_t s);
 void launch_beta_from_dense(const double* beta_in, int r, float* beta32, int* elem_flag,
                             uint8_t* occ, cudaStream_t s);
-void launch_node_flags(const int* elem_flag, int r, int tx, int ty, int tz, int* node_flag,
-                       int* tile_flag, cudaStream_t s);
+void launch_node_flags(const int* elem_flag, int r, int* node_flag, cudaStream_t s);
 void launch_scatter_compact(const int* flag, const int* offset, int n, int* map_or_null,
                             int* list, cudaStream_t s);
 void launch_fill_int(int* p, int v, size_t n, cudaStream_t s);

@@ -66,16 +66,15 @@ struct Misc {
   int touches;
   int n_nodes;
   int n_elem;
-  int n_tiles;
+  int pad0;
   int node0_active;
   double beta_sum;
   double pad[4];
 };
 
 __global__ void finalize_counts_kernel(Misc* m, const int* node_flag, const int* node_off,
-                                       const int* elem_flag, const int* elem_off,
-                                       const int* tile_flag, const int* tile_off, int n3,
-                                       int ntiles, const double* beta_partials, int nbp) {
+                                       const int* elem_flag, const int* elem_off, int n3,
+                                       const double* beta_partials, int nbp) {
   __shared__ double sh[256];
   double s = 0.0;
   for (int b = threadIdx.x; b < nbp; b += blockDim.x) s += beta_partials[2 * b];
@@ -89,7 +88,6 @@ __global__ void finalize_counts_kernel(Misc* m, const int* node_flag, const int*
     m->beta_sum = sh[0];
     m->n_nodes = node_off[n3 - 1] + node_flag[n3 - 1];
     m->n_elem = elem_off[n3 - 1] + elem_flag[n3 - 1];
-    m->n_tiles = tile_off[ntiles - 1] + tile_flag[ntiles - 1];
     m->node0_active = node_flag[0];
   }
 }
@@ -135,12 +133,11 @@ struct shl_ctx {
   double norm = 0.0;
   DevBuf tab, coeff, sl, sign8, centres, corners, csign, misc;
   // mesh + topology
-  DevBuf occ0, occ1, beta64, beta32, elem_flag, node_flag, tile_flag, off, node_map, node_list,
-      elem_list, tile_list, scan_tmp, beta_partials;
+  DevBuf occ0, occ1, beta64, beta32, elem_flag, node_flag, off, node_map, node_list, elem_list,
+      scan_tmp, beta_partials;
   int64_t n_surface = 0, n_elem = 0;
-  int n_nodes = 0, n_tiles = 0, full_fallback = 0, node0_active = 0;
-  double volume_ratio = 0.0;
-  int tile_prec = -1;  // precision the tile list was built for
+  int n_nodes = 0, full_fallback = 0, node0_active = 0;
+  double volume_ratio = 0.0, beta_sum = 0.0;
   // solver
   DevBuf vec, partials, state, cout;
   Misc* hmisc = nullptr;
@@ -244,28 +241,20 @@ void read_norm(shl_ctx* c) {
   c->norm = v;
 }
 
-// ---- topology: node ids, element list, apply tiles ------------------------
-template <typename TV>
+// ---- topology: node ids and element list (ordered compaction) ------------
 void build_topology(shl_ctx* c) {
   const int r = c->r;
   const int n3 = r * r * r;
-  constexpr int TX = shl::TileShape<TV>::X, TY = shl::TileShape<TV>::Y, TZ = shl::TileShape<TV>::Z;
-  const int ntiles = ((r + TX - 1) / TX) * ((r + TY - 1) / TY) * ((r + TZ - 1) / TZ);
   c->node_flag.ensure(static_cast<size_t>(n3) * sizeof(int));
-  c->tile_flag.ensure(static_cast<size_t>(ntiles) * sizeof(int));
-  c->off.ensure(static_cast<size_t>(n3) * sizeof(int) * 3);
+  c->off.ensure(static_cast<size_t>(n3) * sizeof(int) * 2);
   c->node_map.ensure(static_cast<size_t>(n3) * sizeof(int));
   c->node_list.ensure(static_cast<size_t>(n3) * sizeof(int));
   c->elem_list.ensure(static_cast<size_t>(n3) * sizeof(int));
-  c->tile_list.ensure(static_cast<size_t>(ntiles) * sizeof(int));
   const size_t tb = shl::scan_temp_bytes(n3);
   c->scan_tmp.ensure(tb);
   int* off_n = c->off.as<int>();
   int* off_e = off_n + n3;
-  int* off_t = off_e + n3;
-  CK(cudaMemsetAsync(c->tile_flag.p, 0, static_cast<size_t>(ntiles) * sizeof(int), c->stream));
-  shl::launch_node_flags(c->elem_flag.as<int>(), r, TX, TY, TZ, c->node_flag.as<int>(),
-                         c->tile_flag.as<int>(), c->stream);
+  shl::launch_node_flags(c->elem_flag.as<int>(), r, c->node_flag.as<int>(), c->stream);
   shl::launch_exclusive_scan(c->node_flag.as<int>(), off_n, n3, c->scan_tmp.p, c->scan_tmp.cap,
                              c->stream);
   shl::launch_scatter_compact(c->node_flag.as<int>(), off_n, n3, c->node_map.as<int>(),
@@ -274,35 +263,23 @@ void build_topology(shl_ctx* c) {
                              c->stream);
   shl::launch_scatter_compact(c->elem_flag.as<int>(), off_e, n3, nullptr, c->elem_list.as<int>(),
                               c->stream);
-  shl::launch_exclusive_scan(c->tile_flag.as<int>(), off_t, ntiles, c->scan_tmp.p, c->scan_tmp.cap,
-                             c->stream);
-  shl::launch_scatter_compact(c->tile_flag.as<int>(), off_t, ntiles, nullptr,
-                              c->tile_list.as<int>(), c->stream);
   const int nbp = (n3 + 255) / 256;
-  finalize_counts_kernel<<<1, 256, 0, c->stream>>>(
-      c->misc.as<Misc>(), c->node_flag.as<int>(), off_n, c->elem_flag.as<int>(), off_e,
-      c->tile_flag.as<int>(), off_t, n3, ntiles, c->beta_partials.as<double>(), nbp);
-  c->launches += 1 + 3 * 2 + 3 + 1;
+  finalize_counts_kernel<<<1, 256, 0, c->stream>>>(c->misc.as<Misc>(), c->node_flag.as<int>(),
+                                                   off_n, c->elem_flag.as<int>(), off_e, n3,
+                                                   c->beta_partials.as<double>(), nbp);
+  c->launches += 1 + 2 * 2 + 2 + 1;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(c->hmisc, c->misc.p, sizeof(Misc), cudaMemcpyDeviceToHost, c->stream));
   c->sync();
   c->n_nodes = c->hmisc->n_nodes;
   c->n_elem = c->hmisc->n_elem;
-  c->n_tiles = c->hmisc->n_tiles;
   c->node0_active = c->hmisc->node0_active;
-  c->volume_ratio = c->hmisc->beta_sum / (double(r) * r * r);
-  c->tile_prec = sizeof(TV) == 8 ? 0 : 1;
-}
-
-void build_topology_for(shl_ctx* c, bool fp64_tiles) {
-  if (fp64_tiles)
-    build_topology<double>(c);
-  else
-    build_topology<float>(c);
+  c->beta_sum = c->hmisc->beta_sum;
+  c->volume_ratio = c->beta_sum / (double(r) * r * r);
 }
 
 // ---- mesh (build_reduced_mesh, voxel.hpp:235-313) --------------------------
-void run_mesh(shl_ctx* c, const shl_shell_params& sp, bool fp64_tiles) {
+void run_mesh(shl_ctx* c, const shl_shell_params& sp) {
   if (!c->grid_ready) throw ShlError(SHL_VALIDATION, "no resident grid: call shl_sample_grid first");
   if (!(sp.sharpness > 0.0)) throw ShlError(SHL_VALIDATION, "sharpness must be positive");
   if (!(sp.floor_ratio > 0.0 && sp.floor_ratio < 1.0))
@@ -342,7 +319,7 @@ void run_mesh(shl_ctx* c, const shl_shell_params& sp, bool fp64_tiles) {
     // keep the final occupancy in occ0
     CK(cudaMemcpyAsync(c->occ0.p, a, n3, cudaMemcpyDeviceToDevice, c->stream));
   }
-  build_topology_for(c, fp64_tiles);
+  build_topology(c);
   c->n_surface = c->hmisc->n_surface;
   if (c->n_surface == 0)
     throw ShlError(SHL_DEGENERATE, "field has no zero crossing: no surface to mesh");
@@ -363,23 +340,21 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   if (!c->node0_active)
     throw ShlError(SHL_SOLVER,
                    "mesh has no corner node group: cannot prescribe the strain gauge");
-  const int want_tiles = sizeof(TV) == 8 ? 0 : 1;
-  if (c->tile_prec != want_tiles) build_topology_for(c, sizeof(TV) == 8);
   const int n = c->n_nodes;
-  const int ld = round_up(std::max(n, 1), 64);
+  const int ld = round_up(n + 1, 64);  // slot n of every z plane stays zero
   const size_t nX = static_cast<size_t>(18) * ld, nV = nX;
-  c->vec.ensure(2 * nX * sizeof(TX) + (4 * nV + 6 * static_cast<size_t>(ld)) * sizeof(TV));
+  c->vec.ensure(2 * nX * sizeof(TX) + (3 * nV + 6 * static_cast<size_t>(ld)) * sizeof(TV));
   TX* x = c->vec.as<TX>();
   TX* rv = x + nX;
   TV* z = reinterpret_cast<TV*>(rv + nX);
-  TV* p0 = z + nV;
-  TV* p1 = p0 + nV;
-  TV* q = p1 + nV;
+  TV* p = z + nV;
+  TV* q = p + nV;
   TV* dinv = q + nV;
   const int grid_u = std::max(1, std::min((n + 255) / 256, c->num_sms * 8));
+  const int grid_a = std::max(1, (n + 255) / 256);
   const int grid_c = std::max(1, std::min(static_cast<int>((c->n_elem + 31) / 32), c->num_sms * 16));
   c->partials.ensure(sizeof(double) *
-                     std::max<size_t>({static_cast<size_t>(c->n_tiles) * 6,
+                     std::max<size_t>({static_cast<size_t>(grid_a) * 6,
                                        static_cast<size_t>(grid_u) * 12,
                                        static_cast<size_t>(grid_c) * 21, 64}));
   c->state.ensure(sizeof(shl::PcgState));
@@ -387,57 +362,58 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
 
   double T[144], W[144];
   element_loads(K0, r, T, W);
+  // ridge 1e-11 * mean|diag A| (fem.hpp:339-341): every K0 diagonal entry is
+  // equal, so mean diag = K0[0] * (8 sum beta) / n_nodes
+  const double ridge = n > 0 ? 1e-11 * std::fabs(K0[0]) * 8.0 * c->beta_sum / double(n) : 0.0;
   CK(cudaEventRecord(c->ev[3], c->stream));
   shl::upload_element_constants(K0, W, T, c->stream);
   CK(cudaMemsetAsync(x, 0, nX * sizeof(TX), c->stream));
-  CK(cudaMemsetAsync(p0, 0, 2 * nV * sizeof(TV), c->stream));
-  shl::launch_setup<TX, TV>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), rv, dinv,
-                            c->stream);
+  CK(cudaMemsetAsync(z, 0, 3 * nV * sizeof(TV), c->stream));
+  shl::launch_setup<TX, TV>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), ridge, rv,
+                            dinv, c->stream);
   shl::PcgState hs{};
   hs.tol = opt.tol;
+  hs.ridge = ridge;
   hs.max_iter = opt.max_iter > 0 ? opt.max_iter : 20 * r + 2000;
   std::memcpy(c->hstate, &hs, sizeof(hs));
   CK(cudaMemcpyAsync(c->state.p, c->hstate, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
   CK(cudaEventRecord(c->ev[4], c->stream));
 
   shl::PcgState* dst = c->state.as<shl::PcgState>();
-  shl::UpdateArgs<TX, TV> ua{x, rv, p1, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1};
-  shl::launch_update<TX, TV>(ua, grid_u, c->stream);
-  ua.init = 0;
   const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
                                          : reinterpret_cast<const TV*>(c->beta32.p);
-  shl::ApplyArgs<TV> aa{c->tile_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p0, p1, q,
-                        c->partials.as<double>(), dst, r, ld};
-  int64_t launches = 2 + 1;
+  shl::UpdateArgs<TX, TV> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1};
+  shl::ApplyArgs<TV> aa{c->node_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p, q,
+                        c->partials.as<double>(), dst, r, n, ld};
+  // z0 = Dinv b, then w0 = A z0, p0 = z0, q0 = w0, alpha0
+  shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+  shl::launch_apply<TV>(aa, c->stream);
+  ua.init = 0;
+  int64_t launches = 2 + 2;
   int check = opt.check_every > 0 ? opt.check_every : (n < 200000 ? 16 : 32);
-  int parity = 0;
   double apply_ms = 0.0, update_ms = 0.0;
   int64_t apply_launches = 0;
   for (;;) {
     for (int it = 0; it < check; ++it) {
-      aa.pold = parity ? p1 : p0;
-      aa.pnew = parity ? p0 : p1;
-      ua.p = aa.pnew;
       if (c->profiling) {
         cudaEvent_t e0 = c->prof_ev[0], e1 = c->prof_ev[1], e2 = c->prof_ev[2];
         CK(cudaEventRecord(e0, c->stream));
-        shl::launch_apply<TV>(aa, c->n_tiles, c->stream);
-        CK(cudaEventRecord(e1, c->stream));
         shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+        CK(cudaEventRecord(e1, c->stream));
+        shl::launch_apply<TV>(aa, c->stream);
         CK(cudaEventRecord(e2, c->stream));
         CK(cudaEventSynchronize(e2));
-        float ta = 0, tu = 0;
-        CK(cudaEventElapsedTime(&ta, e0, e1));
-        CK(cudaEventElapsedTime(&tu, e1, e2));
+        float tu = 0, ta = 0;
+        CK(cudaEventElapsedTime(&tu, e0, e1));
+        CK(cudaEventElapsedTime(&ta, e1, e2));
         apply_ms += ta;
         update_ms += tu;
         ++apply_launches;
       } else {
-        shl::launch_apply<TV>(aa, c->n_tiles, c->stream);
         shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+        shl::launch_apply<TV>(aa, c->stream);
       }
       launches += 2;
-      parity ^= 1;
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->hstate, c->state.p, sizeof(shl::PcgState), cudaMemcpyDeviceToHost,
@@ -495,7 +471,7 @@ void fill_mesh_stats(shl_ctx* c, shl_stats* st) {
   st->n_surface = c->n_surface;
   st->n_elements = c->n_elem;
   st->n_nodes = c->n_nodes;
-  st->n_tiles = c->n_tiles;
+  st->n_tiles = 0;
   st->full_fallback = c->full_fallback;
   st->norm = c->norm;
   st->volume_ratio = c->volume_ratio;
@@ -532,9 +508,8 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
   CK(cudaEventRecord(c->ev[1], c->stream));
   read_norm(c);
   if (c->norm == 0.0) throw ShlError(SHL_DEGENERATE, "field: design is degenerate (norm = 0)");
-  const bool fp64 = resolve_precision(opt) == SHL_PREC_FP64;
   tagged("mesh", [&] {
-    run_mesh(c, *sp, fp64);
+    run_mesh(c, *sp);
     return 0;
   });
   CK(cudaEventRecord(c->ev[2], c->stream));
@@ -683,7 +658,7 @@ int shl_build_reduced_mesh(shl_ctx* c, const shl_shell_params* sp, uint32_t* ele
                            double* beta, int64_t* n_elements, int32_t* full_fallback) {
   if (!c || !sp) return SHL_VALIDATION;
   return guarded(c, [&] {
-    run_mesh(c, *sp, false);
+    run_mesh(c, *sp);
     const int r = c->r;
     const size_t n3 = static_cast<size_t>(r) * r * r;
     if (elements || beta) {
@@ -728,9 +703,10 @@ int shl_grid_solve(shl_ctx* c, int r, const double* beta, const double* K0,
     c->launches += 1;
     CK(cudaEventRecord(c->ev[1], c->stream));
     CK(cudaEventRecord(c->ev[2], c->stream));
-    build_topology_for(c, resolve_precision(opt) == SHL_PREC_FP64);
+    build_topology(c);
     double s = 0.0;
     for (size_t e = 0; e < n3; ++e) s += beta[e];
+    c->beta_sum = s;
     c->volume_ratio = s / double(n3);
     c->n_surface = 0;
     c->full_fallback = c->n_elem == static_cast<int64_t>(n3);

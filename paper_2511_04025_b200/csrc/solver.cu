@@ -11,11 +11,9 @@
 // are consecutive addresses (coalesced, no bytes spent on void voxels).
 //
 //   K3 rhs_kernel      b_n = -sum_e beta_e (K0 T)_{a(e,n)}      grid_solver.hpp:141-152
-//   K4 apply_kernel    p = z + beta p_old (deferred direction update), then
-//                      q = A p for a 3-D tile, node-centric gather (no
-//                      atomics): per neighbour m the 3x3 block
-//                      S_m = sum_{e ni n,m} beta_e K0[a,b] is built once and
-//                      applied to all six load cases; partial p.q
+//   K4 apply_kernel    w = A z by node-centric gather (no atomics, one thread
+//                      per active node), p = z + beta p, q = w + beta q in
+//                      place (Chronopoulos-Gear PCG), partial z.w
 //   K5 update_kernel   x += alpha p, r -= alpha q, z = Dinv r, partial r.z, r.r
 //   K6 chom_kernel     C_ab = sum_e beta_e (x_e+T)_a^T K0 (x_e+T)_b        :183-197
 //
@@ -46,6 +44,9 @@ template <>
 __device__ __forceinline__ float k0<float>(int i) {
   return c_K0f[i];
 }
+
+__device__ __forceinline__ float fma_t(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_t(double a, double b, double c) { return fma(a, b, c); }
 
 __host__ __device__ constexpr int corner_id(int x, int y, int z) {
   return 4 * z + (y ? (x ? 2 : 3) : (x ? 1 : 0));
@@ -116,7 +117,7 @@ __device__ __forceinline__ void reduce_partials(const double* partials, double (
 // and the strain right-hand sides (grid_solver.hpp:141-152), node 0 pinned.
 template <typename TX, typename TV>
 __global__ void setup_kernel(const int* __restrict__ node_list, int n_nodes, int ld, int r,
-                             const double* __restrict__ beta64, TX* __restrict__ rvec,
+                             const double* __restrict__ beta64, double ridge, TX* __restrict__ rvec,
                              TV* __restrict__ dinv) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_nodes) return;
@@ -144,6 +145,9 @@ __global__ void setup_kernel(const int* __restrict__ node_list, int n_nodes, int
   }
   double inv[6] = {0, 0, 0, 0, 0, 0};  // symmetric: 00 01 02 11 12 22
   if (g != 0) {
+    D[0] += ridge;
+    D[4] += ridge;
+    D[8] += ridge;
     const double c00 = D[4] * D[8] - D[5] * D[7], c01 = D[5] * D[6] - D[3] * D[8],
                  c02 = D[3] * D[7] - D[4] * D[6];
     const double det = D[0] * c00 + D[1] * c01 + D[2] * c02;
@@ -164,24 +168,22 @@ __global__ void setup_kernel(const int* __restrict__ node_list, int n_nodes, int
   for (int q = 0; q < 18; ++q) rvec[static_cast<size_t>(q) * ld + idx] = static_cast<TX>(b[q]);
 }
 
-// ---- K4: fused direction update + K.u apply ---------------------------------
-template <typename TV, int TX, int TY, int TZ>
-__global__ void __launch_bounds__(TX* TY* TZ)
-    apply_kernel(const ApplyArgs<TV> A) {
-  constexpr int HX = TX + 2, HY = TY + 2, HZ = TZ + 2, HN = HX * HY * HZ;
-  constexpr int EX = TX + 1, EY = TY + 1, EZ = TZ + 1, EN = EX * EY * EZ;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TV* ps = reinterpret_cast<TV*>(smem_raw);  // [18][HN]
-  TV* bs = ps + 18 * HN;                      // [EN]
+// ---- K4: w = A z by gather, fused with the direction update -------------------
+// Chronopoulos-Gear form of PCG: the operator is applied to z (the freshly
+// preconditioned residual) instead of p, so the neighbourhood gather reads one
+// vector and p, q are updated in place for the thread's own node:
+//   w = A z,  p = z + beta p,  q = w + beta q,  delta = z.w
+// One thread per ACTIVE node (no lanes spent on void voxels).  For neighbour m
+// of node n the 3x3 block S_m = sum_{e ni n,m} beta_e K0[a(n,e), b(m,e)] is
+// built once (K0 entries are immediate constant-bank operands) and applied to
+// all six load cases.  Inactive neighbours read a zero slot (index n_nodes).
+template <typename TV>
+__global__ void __launch_bounds__(256) apply_kernel(const ApplyArgs<TV> A) {
   __shared__ double scratch[32 * 6];
   PcgState* st = A.state;
   if (st->stop) return;
   const int r = A.r;
-  const int tile = A.tiles[blockIdx.x];
-  const int ntx = (r + TX - 1) / TX, nty = (r + TY - 1) / TY;
-  const int x0 = (tile % ntx) * TX, y0 = ((tile / ntx) % nty) * TY, z0 = (tile / (ntx * nty)) * TZ;
   const size_t ld = A.ld;
-
   TV bcoef[6];
   bool dn[6];
 #pragma unroll
@@ -189,101 +191,94 @@ __global__ void __launch_bounds__(TX* TY* TZ)
     dn[s] = st->done[s] != 0;
     bcoef[s] = static_cast<TV>(st->beta[s]);
   }
-
-  // halo: p = z + beta * p_old for every active node of the (TX+2)(TY+2)(TZ+2) box
-  for (int h = threadIdx.x; h < HN; h += blockDim.x) {
-    const int hx = h % HX, hy = (h / HX) % HY, hz = h / (HX * HY);
-    const int gx = ((x0 - 1 + hx) % r + r) % r, gy = ((y0 - 1 + hy) % r + r) % r,
-              gz = ((z0 - 1 + hz) % r + r) % r;
-    const int idx = A.node_map[(static_cast<size_t>(gz) * r + gy) * r + gx];
-    const bool own = hx >= 1 && hx <= TX && hy >= 1 && hy <= TY && hz >= 1 && hz <= TZ &&
-                     x0 + hx - 1 < r && y0 + hy - 1 < r && z0 + hz - 1 < r;
+  const TV ridge = static_cast<TV>(st->ridge);
+  double dl[6] = {0, 0, 0, 0, 0, 0};
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < A.n) {
+    const int g = A.node_list[idx];
+    const int rr = r * r;
+    const int i = g % r, j = (g / r) % r, k = g / rr;
+    const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
+    const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
+    const int zs[3] = {(k == 0 ? r - 1 : k - 1) * rr, k * rr, (k == r - 1 ? 0 : k + 1) * rr};
+    TV be[8];
 #pragma unroll
-    for (int q = 0; q < 18; ++q) {
-      const int s = q % 6;
-      TV v = TV(0);
-      if (idx >= 0 && !dn[s]) v = A.z[q * ld + idx] + bcoef[s] * A.pold[q * ld + idx];
-      ps[q * HN + h] = v;
-      if (own && idx >= 0) A.pnew[q * ld + idx] = v;
+    for (int e = 0; e < 8; ++e) {
+      const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;  // node's corner in e
+      be[e] = A.beta[zs[1 - oz] + ys[1 - oy] + xs[1 - ox]];
     }
-  }
-  for (int e = threadIdx.x; e < EN; e += blockDim.x) {
-    const int ex = e % EX, ey = (e / EX) % EY, ez = e / (EX * EY);
-    const int gx = ((x0 - 1 + ex) % r + r) % r, gy = ((y0 - 1 + ey) % r + r) % r,
-              gz = ((z0 - 1 + ez) % r + r) % r;
-    bs[e] = A.beta[(static_cast<size_t>(gz) * r + gy) * r + gx];
-  }
-  __syncthreads();
-
-  const int lx = threadIdx.x % TX, ly = (threadIdx.x / TX) % TY, lz = threadIdx.x / (TX * TY);
-  const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-  double pq[6] = {0, 0, 0, 0, 0, 0};
-  if (gx < r && gy < r && gz < r) {
-    const size_t gnode = (static_cast<size_t>(gz) * r + gy) * r + gx;
-    const int idx = A.node_map[gnode];
-    if (idx >= 0) {
-      TV y[18];
+    TV y[18];
 #pragma unroll
-      for (int q = 0; q < 18; ++q) y[q] = TV(0);
-      if (gnode != 0) {
-        // beta of the 8 incident elements; element (ox,oy,oz) has its min
-        // corner at node - (1-ox, 1-oy, 1-oz)... indexed by the node's local
-        // corner inside it: e bit = node offset within the element.
-        TV be[8];
+    for (int q = 0; q < 18; ++q) y[q] = TV(0);
+    if (g != 0) {
+#pragma unroll
+      for (int m = 0; m < 27; ++m) {
+        const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+        int nb = (m == 13) ? idx : A.node_map[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
+        nb = nb < 0 ? A.n : nb;
+        TV S[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) S[q] = TV(0);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
-          be[e] = bs[((lz + 1 - oz) * EY + (ly + 1 - oy)) * EX + (lx + 1 - ox)];
+          const int bx = ox + dx, by = oy + dy, bz = oz + dz;  // neighbour's corner in e
+          if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+          const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+              S[c * 3 + d] = fma_t(be[e], k0<TV>((3 * a + c) * 24 + 3 * b + d), S[c * 3 + d]);
         }
 #pragma unroll
-        for (int m = 0; m < 27; ++m) {
-          const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-          TV S[9];
+        for (int s = 0; s < 6; ++s) {
+          const TV z0 = A.z[(0 * 6 + s) * ld + nb], z1 = A.z[(1 * 6 + s) * ld + nb],
+                   z2 = A.z[(2 * 6 + s) * ld + nb];
 #pragma unroll
-          for (int q = 0; q < 9; ++q) S[q] = TV(0);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;  // node's corner in e
-            const int bx = ox + dx, by = oy + dy, bz = oz + dz;         // neighbour's corner
-            if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
-            const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-#pragma unroll
-              for (int d = 0; d < 3; ++d) S[c * 3 + d] += be[e] * k0<TV>((3 * a + c) * 24 + 3 * b + d);
-          }
-          const int hn = ((lz + 1 + dz) * HY + (ly + 1 + dy)) * HX + (lx + 1 + dx);
-#pragma unroll
-          for (int s = 0; s < 6; ++s) {
-            const TV p0 = ps[(0 * 6 + s) * HN + hn], p1 = ps[(1 * 6 + s) * HN + hn],
-                     p2 = ps[(2 * 6 + s) * HN + hn];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) y[c * 6 + s] += S[c * 3 + 0] * p0 + S[c * 3 + 1] * p1 + S[c * 3 + 2] * p2;
+          for (int c = 0; c < 3; ++c) {
+            TV v = y[c * 6 + s];
+            v = fma_t(S[c * 3 + 0], z0, v);
+            v = fma_t(S[c * 3 + 1], z1, v);
+            v = fma_t(S[c * 3 + 2], z2, v);
+            y[c * 6 + s] = v;
           }
         }
-      }
-      const int hown = ((lz + 1) * HY + (ly + 1)) * HX + (lx + 1);
-#pragma unroll
-      for (int q = 0; q < 18; ++q) {
-        A.q[q * ld + idx] = y[q];
-        pq[q % 6] += static_cast<double>(ps[q * HN + hown]) * static_cast<double>(y[q]);
       }
     }
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {
+      const int s = q % 6;
+      const size_t o = q * ld + idx;
+      const TV zq = A.z[o];
+      const TV w = g != 0 ? fma_t(ridge, zq, y[q]) : TV(0);
+      dl[s] += static_cast<double>(zq) * static_cast<double>(w);
+      TV pn = TV(0), qn = TV(0);
+      if (!dn[s]) {
+        pn = fma_t(bcoef[s], A.p[o], zq);
+        qn = fma_t(bcoef[s], A.q[o], w);
+      }
+      A.p[o] = pn;
+      A.q[o] = qn;
+    }
   }
-  block_sum<6>(pq, scratch);
-  if (publish_partial<6>(pq, A.partials, &st->counter_apply)) {
+  block_sum<6>(dl, scratch);
+  if (publish_partial<6>(dl, A.partials, &st->counter_apply)) {
     double tot[6];
     __syncthreads();
     reduce_partials<6>(A.partials, tot, scratch);
     if (threadIdx.x == 0) {
       for (int s = 0; s < 6; ++s) {
-        st->pq[s] = tot[s];
+        st->delta[s] = tot[s];
         if (st->done[s]) {
           st->alpha[s] = 0.0;
-        } else {
-          if (!(tot[s] > 0.0)) st->error = 1;
-          st->alpha[s] = st->rz[s] / tot[s];
+          continue;
         }
+        // p.Ap = delta - beta * gamma / alpha_old  (= delta on the first step)
+        const double den = st->beta[s] == 0.0 ? tot[s] : tot[s] - st->beta[s] * st->gamma[s] / st->alpha[s];
+        if (!(den > 0.0)) st->error = 1;
+        st->pap[s] = den;
+        st->alpha[s] = st->gamma[s] / den;
       }
       if (st->error) st->stop = 1;
       st->counter_apply = 0;
@@ -292,47 +287,43 @@ __global__ void __launch_bounds__(TX* TY* TZ)
 }
 
 // ---- K5: vector update + preconditioner + dots ------------------------------
+//   x += alpha p, r -= alpha q, z = Dinv r, partial r.r and r.z
 template <typename TX, typename TV>
 __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U) {
   __shared__ double scratch[32 * 12];
   PcgState* st = U.state;
   if (st->stop) return;
   const size_t ld = U.ld;
-  TX al[6];
-#pragma unroll
-  for (int s = 0; s < 6; ++s) al[s] = static_cast<TX>(st->alpha[s]);
   double acc[12];  // rr[0..5], rz[6..11]
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0.0;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < U.n; idx += gridDim.x * blockDim.x) {
-    TX rv[18];
-#pragma unroll
-    for (int q = 0; q < 18; ++q) {
-      TX rq = U.r[q * ld + idx];
-      if (!U.init) {
-        const TX a = al[q % 6];
-        TX xq = U.x[q * ld + idx];
-        xq += a * static_cast<TX>(U.p[q * ld + idx]);
-        rq -= a * static_cast<TX>(U.q[q * ld + idx]);
-        U.x[q * ld + idx] = xq;
-        U.r[q * ld + idx] = rq;
-      }
-      rv[q] = rq;
-    }
     TV D[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) D[q] = U.dinv[q * ld + idx];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      const TV r0 = static_cast<TV>(rv[s]), r1 = static_cast<TV>(rv[6 + s]),
-               r2 = static_cast<TV>(rv[12 + s]);
+      const TX a = static_cast<TX>(st->alpha[s]);
+      TX rc[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const size_t o = (c * 6 + s) * ld + idx;
+        TX rq = U.r[o];
+        if (!U.init) {
+          U.x[o] = fma_t(a, static_cast<TX>(U.p[o]), U.x[o]);
+          rq = fma_t(-a, static_cast<TX>(U.q[o]), rq);
+          U.r[o] = rq;
+        }
+        rc[c] = rq;
+      }
+      const TV r0 = static_cast<TV>(rc[0]), r1 = static_cast<TV>(rc[1]), r2 = static_cast<TV>(rc[2]);
       const TV z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
       const TV z1 = D[1] * r0 + D[3] * r1 + D[4] * r2;
       const TV z2 = D[2] * r0 + D[4] * r1 + D[5] * r2;
-      U.z[s * ld + idx] = z0;
-      U.z[(6 + s) * ld + idx] = z1;
-      U.z[(12 + s) * ld + idx] = z2;
-      const double d0 = rv[s], d1 = rv[6 + s], d2 = rv[12 + s];
+      U.z[(0 * 6 + s) * ld + idx] = z0;
+      U.z[(1 * 6 + s) * ld + idx] = z1;
+      U.z[(2 * 6 + s) * ld + idx] = z2;
+      const double d0 = rc[0], d1 = rc[1], d2 = rc[2];
       acc[s] += d0 * d0 + d1 * d1 + d2 * d2;
       acc[6 + s] += d0 * static_cast<double>(z0) + d1 * static_cast<double>(z1) +
                     d2 * static_cast<double>(z2);
@@ -350,18 +341,19 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
         const double rn = sqrt(tot[s]);
         if (U.init) {
           st->bnorm[s] = rn;
-          st->rz[s] = tot[6 + s];
+          st->gamma[s] = tot[6 + s];
           st->done[s] = rn == 0.0;
           st->beta[s] = 0.0;
+          st->alpha[s] = 0.0;
           st->iters[s] = 0;
         } else if (!st->done[s]) {
-          st->iters[s] = st->it + 1;
-          if (rn <= st->tol * st->bnorm[s]) {
+          st->iters[s] = st->it + 1;  // grid_solver.hpp:67
+          if (rn <= st->tol * st->bnorm[s]) {  // grid_solver.hpp:68-72
             st->done[s] = 1;
             st->beta[s] = 0.0;
           } else {
-            st->beta[s] = tot[6 + s] / st->rz[s];
-            st->rz[s] = tot[6 + s];
+            st->beta[s] = tot[6 + s] / st->gamma[s];
+            st->gamma[s] = tot[6 + s];
           }
         }
         all = all && st->done[s];
@@ -459,30 +451,17 @@ void upload_element_constants(const double* K0, const double* W, const double* T
 }
 
 template <typename TX, typename TV>
-void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64, TX* rvec,
-                  TV* dinv, cudaStream_t s) {
+void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64,
+                  double ridge, TX* rvec, TV* dinv, cudaStream_t s) {
   if (n_nodes == 0) return;
   setup_kernel<TX, TV><<<(n_nodes + 127) / 128, 128, 0, s>>>(node_list, n_nodes, ld, r, beta64,
-                                                            rvec, dinv);
+                                                            ridge, rvec, dinv);
 }
 
 template <typename TV>
-size_t apply_smem_bytes() {
-  constexpr int TX = TileShape<TV>::X, TY = TileShape<TV>::Y, TZ = TileShape<TV>::Z;
-  return sizeof(TV) * (18 * (TX + 2) * (TY + 2) * (TZ + 2) + (TX + 1) * (TY + 1) * (TZ + 1));
-}
-
-template <typename TV>
-void launch_apply(const ApplyArgs<TV>& a, int n_tiles, cudaStream_t s) {
-  constexpr int TX = TileShape<TV>::X, TY = TileShape<TV>::Y, TZ = TileShape<TV>::Z;
-  const size_t smem = apply_smem_bytes<TV>();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(apply_kernel<TV, TX, TY, TZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    configured = true;
-  }
-  apply_kernel<TV, TX, TY, TZ><<<n_tiles, TX * TY * TZ, smem, s>>>(a);
+void launch_apply(const ApplyArgs<TV>& a, cudaStream_t s) {
+  if (a.n == 0) return;
+  apply_kernel<TV><<<(a.n + 255) / 256, 256, 0, s>>>(a);
 }
 
 template <typename TX, typename TV>
@@ -495,16 +474,14 @@ void launch_chom(const ChomArgs<TX>& c, int grid, cudaStream_t s) {
   chom_kernel<TX><<<grid, 32, 0, s>>>(c);
 }
 
-template void launch_setup<double, double>(const int*, int, int, int, const double*, double*,
-                                           double*, cudaStream_t);
-template void launch_setup<double, float>(const int*, int, int, int, const double*, double*, float*,
-                                          cudaStream_t);
-template void launch_setup<float, float>(const int*, int, int, int, const double*, float*, float*,
-                                         cudaStream_t);
-template size_t apply_smem_bytes<double>();
-template size_t apply_smem_bytes<float>();
-template void launch_apply<double>(const ApplyArgs<double>&, int, cudaStream_t);
-template void launch_apply<float>(const ApplyArgs<float>&, int, cudaStream_t);
+template void launch_setup<double, double>(const int*, int, int, int, const double*, double,
+                                           double*, double*, cudaStream_t);
+template void launch_setup<double, float>(const int*, int, int, int, const double*, double, double*,
+                                          float*, cudaStream_t);
+template void launch_setup<float, float>(const int*, int, int, int, const double*, double, float*,
+                                         float*, cudaStream_t);
+template void launch_apply<double>(const ApplyArgs<double>&, cudaStream_t);
+template void launch_apply<float>(const ApplyArgs<float>&, cudaStream_t);
 template void launch_update<double, double>(const UpdateArgs<double, double>&, int, cudaStream_t);
 template void launch_update<double, float>(const UpdateArgs<double, float>&, int, cudaStream_t);
 template void launch_update<float, float>(const UpdateArgs<float, float>&, int, cudaStream_t);

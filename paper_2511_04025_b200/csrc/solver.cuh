@@ -10,30 +10,18 @@
 
 namespace shl {
 
-// Apply tile (nodes) per precision: 32 x-consecutive nodes per warp row.
-template <typename TV>
-struct TileShape;
-template <>
-struct TileShape<float> {
-  static constexpr int X = 32, Y = 4, Z = 2;
-};
-template <>
-struct TileShape<double> {
-  static constexpr int X = 32, Y = 2, Z = 2;
-};
-
 template <typename TV>
 struct ApplyArgs {
-  const int* tiles;
-  const int* node_map;  // r^3 -> active node id or -1
-  const TV* beta;       // r^3 dense, 0 = absent
-  const TV* z;
-  const TV* pold;
-  TV* pnew;
+  const int* node_list;  // active node -> grid id
+  const int* node_map;   // r^3 -> active node id or -1
+  const TV* beta;        // r^3 dense, 0 = absent
+  const TV* z;           // 18 planes, slot n is a zero row
+  TV* p;
   TV* q;
   double* partials;
   PcgState* state;
   int r;
+  int n;
   int ld;
 };
 
@@ -68,12 +56,10 @@ struct ChomArgs {
 
 void upload_element_constants(const double* K0, const double* W, const double* T, cudaStream_t s);
 template <typename TX, typename TV>
-void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64, TX* rvec,
-                  TV* dinv, cudaStream_t s);
+void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64,
+                  double ridge, TX* rvec, TV* dinv, cudaStream_t s);
 template <typename TV>
-size_t apply_smem_bytes();
-template <typename TV>
-void launch_apply(const ApplyArgs<TV>& a, int n_tiles, cudaStream_t s);
+void launch_apply(const ApplyArgs<TV>& a, cudaStream_t s);
 template <typename TX, typename TV>
 void launch_update(const UpdateArgs<TX, TV>& u, int grid, cudaStream_t s);
 template <typename TX>

@@ -11,7 +11,7 @@
 //   corners    8 corner voxels forced when any element touches the boundary
 //   beta       h(F_centre / norm), step_function voxel.hpp:38-41
 //   nodes      torus node active iff an incident element is active; ordered
-//              exclusive scan gives node ids (grid order) and the apply tiles
+//              exclusive scan gives node ids in grid order (node_map, node_list)
 //
 // Occupancy is one byte per voxel: at 128^3 a dilation pass moves ~2 MB, a few
 // microseconds of HBM time, so bit packing would not move the stage total.
@@ -167,8 +167,7 @@ __global__ void beta_dense_kernel(const double* __restrict__ beta_in, size_t n3,
   occ[e] = b != 0.0;
 }
 
-__global__ void node_flag_kernel(const int* __restrict__ ef, int r, int tx, int ty, int tz,
-                                 int* __restrict__ node_flag, int* __restrict__ tile_flag) {
+__global__ void node_flag_kernel(const int* __restrict__ ef, int r, int* __restrict__ node_flag) {
   const size_t n3 = static_cast<size_t>(r) * r * r;
   const size_t n = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   if (n >= n3) return;
@@ -182,10 +181,6 @@ __global__ void node_flag_kernel(const int* __restrict__ ef, int r, int tx, int 
     on |= ef[(static_cast<size_t>(ek) * r + ej) * r + ei];
   }
   node_flag[n] = on;
-  if (on) {
-    const int ntx = (r + tx - 1) / tx, nty = (r + ty - 1) / ty;
-    tile_flag[((k / tz) * nty + (j / ty)) * ntx + (i / tx)] = 1;
-  }
 }
 
 __global__ void scatter_kernel(const int* __restrict__ flag, const int* __restrict__ off, int n,
@@ -245,10 +240,9 @@ void launch_beta_from_dense(const double* beta_in, int r, float* beta32, int* el
   beta_dense_kernel<<<blocks(n3, 256), 256, 0, s>>>(beta_in, n3, beta32, elem_flag, occ);
 }
 
-void launch_node_flags(const int* elem_flag, int r, int tx, int ty, int tz, int* node_flag,
-                       int* tile_flag, cudaStream_t s) {
+void launch_node_flags(const int* elem_flag, int r, int* node_flag, cudaStream_t s) {
   const size_t n3 = static_cast<size_t>(r) * r * r;
-  node_flag_kernel<<<blocks(n3, 256), 256, 0, s>>>(elem_flag, r, tx, ty, tz, node_flag, tile_flag);
+  node_flag_kernel<<<blocks(n3, 256), 256, 0, s>>>(elem_flag, r, node_flag);
 }
 
 void launch_scatter_compact(const int* flag, const int* off, int n, int* map, int* list,
