@@ -104,6 +104,8 @@ typedef struct {
   double update_ms;
   int64_t apply_launches;
   int64_t kernel_launches; /* kernels launched by this call */
+  int64_t h2d_bytes;       /* host->device bytes moved by this call */
+  int64_t d2h_bytes;       /* device->host bytes moved by this call */
 } shl_stats;
 
 int shl_ctx_create(int device, shl_ctx** out);

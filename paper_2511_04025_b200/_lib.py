@@ -44,7 +44,8 @@ class shl_stats(C.Structure):
                 ("n_surface", C.c_int64), ("n_elements", C.c_int64), ("n_nodes", C.c_int64),
                 ("n_tiles", C.c_int64), ("norm", C.c_double), ("volume_ratio", C.c_double),
                 ("apply_ms", C.c_double), ("update_ms", C.c_double),
-                ("apply_launches", C.c_int64), ("kernel_launches", C.c_int64)]
+                ("apply_launches", C.c_int64), ("kernel_launches", C.c_int64),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 # every symbol include/shellular_cuda.h declares (checked by tests/test_abi.py)

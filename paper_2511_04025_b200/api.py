@@ -352,6 +352,8 @@ class SolveStats:
     update_ms: float
     apply_launches: int
     kernel_launches: int
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
     @classmethod
     def from_abi(cls, s: L.shl_stats) -> "SolveStats":
@@ -359,7 +361,7 @@ class SolveStats:
                    bool(s.converged), PRECISION_NAME.get(s.precision, "?"), s.n_surface,
                    s.n_elements, s.n_nodes, s.n_tiles, s.norm, s.volume_ratio,
                    bool(s.full_fallback), s.apply_ms, s.update_ms, s.apply_launches,
-                   s.kernel_launches)
+                   s.kernel_launches, s.h2d_bytes, s.d2h_bytes)
 
 
 class GridSolver:

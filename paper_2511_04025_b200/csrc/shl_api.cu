@@ -126,6 +126,7 @@ struct shl_ctx {
   std::string err;
   bool profiling = false;
   int64_t launches = 0;
+  int64_t h2d = 0, d2h = 0;  // bytes across PCIe (counted at each copy)
 
   // resident grid
   int r = 0;
@@ -199,27 +200,45 @@ void alloc_grid(shl_ctx* c, int r) {
 }
 
 // ---- field (sample_grid, field.hpp:488-534) --------------------------------
-void run_field(shl_ctx* c, const shl::HostDesign& d, int r) {
+// Host half: reference arithmetic that must match glibc bit for bit
+// (expansion, coefficients, cosine tables).  Device half: K1.
+struct FieldInputs {
+  int r = 0, nc = 0, n = 0;
+  std::vector<double> coeff, tab;
+  std::vector<int8_t> sign;
+  size_t h2d_bytes() const { return (coeff.size() + tab.size()) * sizeof(double) + sign.size(); }
+};
+
+FieldInputs prepare_field(const shl::HostDesign& d, int r) {
   require_r(r);
+  FieldInputs f;
   const shl::HostDesign ex = d.expanded();  // validates (field.hpp:149-172)
-  const std::vector<double> coeff = d.grid_coefficients();
-  const std::vector<double> tab = shl::axis_tables(ex, r);
-  const int nc = static_cast<int>(ex.sign.size());
-  const int n = d.K + 1;
+  f.r = r;
+  f.coeff = d.grid_coefficients();
+  f.tab = shl::axis_tables(ex, r);
+  f.nc = static_cast<int>(ex.sign.size());
+  f.n = d.K + 1;
+  f.sign.assign(ex.sign.begin(), ex.sign.end());
+  return f;
+}
+
+void run_field(shl_ctx* c, const FieldInputs& f) {
+  const int r = f.r, nc = f.nc, n = f.n;
   alloc_grid(c, r);
   c->grid_ready = c->mesh_ready = false;
-  std::vector<int8_t> sg(ex.sign.begin(), ex.sign.end());
-  c->tab.ensure(std::max<size_t>(tab.size(), 1) * sizeof(double));
-  c->coeff.ensure(coeff.size() * sizeof(double));
-  c->sign8.ensure(std::max<size_t>(sg.size(), 1));
+  c->tab.ensure(std::max<size_t>(f.tab.size(), 1) * sizeof(double));
+  c->coeff.ensure(f.coeff.size() * sizeof(double));
+  c->sign8.ensure(std::max<size_t>(f.sign.size(), 1));
   c->sl.ensure(std::max<size_t>(static_cast<size_t>(nc) * 2 * r * n * n, 1) * sizeof(double));
-  if (!tab.empty())
-    CK(cudaMemcpyAsync(c->tab.p, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice,
-                       c->stream));
-  CK(cudaMemcpyAsync(c->coeff.p, coeff.data(), coeff.size() * sizeof(double),
+  // pageable sources: the copies are staged before cudaMemcpyAsync returns
+  c->h2d += static_cast<int64_t>(f.h2d_bytes());
+  if (!f.tab.empty())
+    CK(cudaMemcpyAsync(c->tab.p, f.tab.data(), f.tab.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->coeff.p, f.coeff.data(), f.coeff.size() * sizeof(double),
                      cudaMemcpyHostToDevice, c->stream));
-  if (!sg.empty())
-    CK(cudaMemcpyAsync(c->sign8.p, sg.data(), sg.size(), cudaMemcpyHostToDevice, c->stream));
+  if (!f.sign.empty())
+    CK(cudaMemcpyAsync(c->sign8.p, f.sign.data(), f.sign.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->misc.p, 0, sizeof(Misc), c->stream));
   shl::launch_field_sl(c->tab.as<double>(), c->coeff.as<double>(), c->sl.as<double>(), nc, r, n,
                        c->stream);
@@ -228,12 +247,11 @@ void run_field(shl_ctx* c, const shl::HostDesign& d, int r) {
                             c->csign.as<int8_t>(), &c->misc.as<Misc>()->norm_bits, c->stream);
   c->launches += 2;
   CK(cudaGetLastError());
-  // the pinned synchronous tables above must outlive their copies
-  c->sync();
   c->grid_ready = true;
 }
 
 void read_norm(shl_ctx* c) {
+  c->d2h += sizeof(Misc);
   CK(cudaMemcpyAsync(c->hmisc, c->misc.p, sizeof(Misc), cudaMemcpyDeviceToHost, c->stream));
   c->sync();
   double v;
@@ -269,6 +287,7 @@ void build_topology(shl_ctx* c) {
                                                    c->beta_partials.as<double>(), nbp);
   c->launches += 1 + 2 * 2 + 2 + 1;
   CK(cudaGetLastError());
+  c->d2h += sizeof(Misc);
   CK(cudaMemcpyAsync(c->hmisc, c->misc.p, sizeof(Misc), cudaMemcpyDeviceToHost, c->stream));
   c->sync();
   c->n_nodes = c->hmisc->n_nodes;
@@ -376,6 +395,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   hs.ridge = ridge;
   hs.max_iter = opt.max_iter > 0 ? opt.max_iter : 20 * r + 2000;
   std::memcpy(c->hstate, &hs, sizeof(hs));
+  c->h2d += sizeof(hs) + 576 * 12 + 144 * 16;  // state + element constants
   CK(cudaMemcpyAsync(c->state.p, c->hstate, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
   CK(cudaEventRecord(c->ev[4], c->stream));
 
@@ -393,33 +413,46 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   int check = opt.check_every > 0 ? opt.check_every : (n < 200000 ? 16 : 32);
   double apply_ms = 0.0, update_ms = 0.0;
   int64_t apply_launches = 0;
+  int64_t issued = 0;
   for (;;) {
     for (int it = 0; it < check; ++it) {
       if (c->profiling) {
-        cudaEvent_t e0 = c->prof_ev[0], e1 = c->prof_ev[1], e2 = c->prof_ev[2];
-        CK(cudaEventRecord(e0, c->stream));
+        const size_t need = static_cast<size_t>(3 * (issued + 1));
+        while (c->prof_ev.size() < need) {
+          cudaEvent_t e;
+          CK(cudaEventCreate(&e));
+          c->prof_ev.push_back(e);
+        }
+        CK(cudaEventRecord(c->prof_ev[3 * issued], c->stream));
         shl::launch_update<TX, TV>(ua, grid_u, c->stream);
-        CK(cudaEventRecord(e1, c->stream));
+        CK(cudaEventRecord(c->prof_ev[3 * issued + 1], c->stream));
         shl::launch_apply<TV>(aa, c->stream);
-        CK(cudaEventRecord(e2, c->stream));
-        CK(cudaEventSynchronize(e2));
-        float tu = 0, ta = 0;
-        CK(cudaEventElapsedTime(&tu, e0, e1));
-        CK(cudaEventElapsedTime(&ta, e1, e2));
-        apply_ms += ta;
-        update_ms += tu;
-        ++apply_launches;
+        CK(cudaEventRecord(c->prof_ev[3 * issued + 2], c->stream));
       } else {
         shl::launch_update<TX, TV>(ua, grid_u, c->stream);
         shl::launch_apply<TV>(aa, c->stream);
       }
+      ++issued;
       launches += 2;
     }
     CK(cudaGetLastError());
+    c->d2h += sizeof(shl::PcgState);
     CK(cudaMemcpyAsync(c->hstate, c->state.p, sizeof(shl::PcgState), cudaMemcpyDeviceToHost,
                        c->stream));
     c->sync();
     if (c->hstate->stop) break;
+  }
+  if (c->profiling) {
+    // per-launch device time of the iterations that did work (later launches exit early)
+    const int64_t real = std::min<int64_t>(issued, c->hstate->it);
+    for (int64_t i = 0; i < real; ++i) {
+      float tu = 0, ta = 0;
+      CK(cudaEventElapsedTime(&tu, c->prof_ev[3 * i], c->prof_ev[3 * i + 1]));
+      CK(cudaEventElapsedTime(&ta, c->prof_ev[3 * i + 1], c->prof_ev[3 * i + 2]));
+      update_ms += tu;
+      apply_ms += ta;
+    }
+    apply_launches = real;
   }
   CK(cudaEventRecord(c->ev[5], c->stream));
   const shl::PcgState& fin = *c->hstate;
@@ -437,6 +470,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   shl::launch_chom<TX>(ca, grid_c, c->stream);
   launches += 1;
   CK(cudaGetLastError());
+  c->d2h += 36 * sizeof(double);
   CK(cudaMemcpyAsync(c->hC, c->cout.p, 36 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaEventRecord(c->ev[6], c->stream));
   c->sync();
@@ -499,10 +533,11 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
   if (!(sp->floor_ratio > 0.0 && sp->floor_ratio < 1.0))
     throw ShlError(SHL_VALIDATION, "floor must lie in (0, 1)");
   if (sp->expand_layers < 0) throw ShlError(SHL_VALIDATION, "expand_layers must be >= 0");
-  const int64_t l0 = c->launches;
+  const int64_t l0 = c->launches, h0 = c->h2d, d0 = c->d2h;
+  FieldInputs fin = tagged("field", [&] { return prepare_field(shl::HostDesign::from_abi(*design), r); });
   CK(cudaEventRecord(c->ev[0], c->stream));
   tagged("field", [&] {
-    run_field(c, shl::HostDesign::from_abi(*design), r);
+    run_field(c, fin);
     return 0;
   });
   CK(cudaEventRecord(c->ev[1], c->stream));
@@ -525,6 +560,8 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
     st->t_fwd = c->ms(0, 6);
     fill_mesh_stats(c, st);
     st->kernel_launches = c->launches - l0;
+    st->h2d_bytes = c->h2d - h0;
+    st->d2h_bytes = c->d2h - d0;
   }
 }
 
@@ -543,8 +580,6 @@ int shl_ctx_create(int device, shl_ctx** out) {
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
-    c->prof_ev.resize(3);
-    for (auto& e : c->prof_ev) CK(cudaEventCreate(&e));
     CK(cudaMallocHost(&c->hmisc, sizeof(Misc)));
     CK(cudaMallocHost(&c->hstate, sizeof(shl::PcgState)));
     CK(cudaMallocHost(&c->hC, 36 * sizeof(double)));
@@ -583,7 +618,7 @@ int shl_sample_grid(shl_ctx* c, const shl_design* design, int r, double* centres
                     double* norm) {
   if (!c || !design) return SHL_VALIDATION;
   return guarded(c, [&] {
-    run_field(c, shl::HostDesign::from_abi(*design), r);
+    run_field(c, prepare_field(shl::HostDesign::from_abi(*design), r));
     read_norm(c);
     const size_t n3 = static_cast<size_t>(r) * r * r;
     if (centres)

@@ -178,10 +178,15 @@ __global__ void setup_kernel(const int* __restrict__ node_list, int n_nodes, int
 // built once (K0 entries are immediate constant-bank operands) and applied to
 // all six load cases.  Inactive neighbours read a zero slot (index n_nodes).
 template <typename TV>
-__global__ void __launch_bounds__(256) apply_kernel(const ApplyArgs<TV> A) {
+__global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(const ApplyArgs<TV> A) {
   __shared__ double scratch[32 * 6];
   PcgState* st = A.state;
   if (st->stop) return;
+  const TV* __restrict__ zv = A.z;
+  const TV* __restrict__ betav = A.beta;
+  const int* __restrict__ nmap = A.node_map;
+  TV* __restrict__ pv = A.p;
+  TV* __restrict__ qv = A.q;
   const int r = A.r;
   const size_t ld = A.ld;
   TV bcoef[6];
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(256) apply_kernel(const ApplyArgs<TV> A) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;  // node's corner in e
-      be[e] = A.beta[zs[1 - oz] + ys[1 - oy] + xs[1 - ox]];
+      be[e] = betav[zs[1 - oz] + ys[1 - oy] + xs[1 - ox]];
     }
     TV y[18];
 #pragma unroll
@@ -214,7 +219,7 @@ __global__ void __launch_bounds__(256) apply_kernel(const ApplyArgs<TV> A) {
 #pragma unroll
       for (int m = 0; m < 27; ++m) {
         const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-        int nb = (m == 13) ? idx : A.node_map[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
+        int nb = (m == 13) ? idx : nmap[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
         nb = nb < 0 ? A.n : nb;
         TV S[9];
 #pragma unroll
@@ -233,8 +238,8 @@ __global__ void __launch_bounds__(256) apply_kernel(const ApplyArgs<TV> A) {
         }
 #pragma unroll
         for (int s = 0; s < 6; ++s) {
-          const TV z0 = A.z[(0 * 6 + s) * ld + nb], z1 = A.z[(1 * 6 + s) * ld + nb],
-                   z2 = A.z[(2 * 6 + s) * ld + nb];
+          const TV z0 = zv[(0 * 6 + s) * ld + nb], z1 = zv[(1 * 6 + s) * ld + nb],
+                   z2 = zv[(2 * 6 + s) * ld + nb];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             TV v = y[c * 6 + s];
@@ -250,16 +255,16 @@ __global__ void __launch_bounds__(256) apply_kernel(const ApplyArgs<TV> A) {
     for (int q = 0; q < 18; ++q) {
       const int s = q % 6;
       const size_t o = q * ld + idx;
-      const TV zq = A.z[o];
+      const TV zq = zv[o];
       const TV w = g != 0 ? fma_t(ridge, zq, y[q]) : TV(0);
       dl[s] += static_cast<double>(zq) * static_cast<double>(w);
       TV pn = TV(0), qn = TV(0);
       if (!dn[s]) {
-        pn = fma_t(bcoef[s], A.p[o], zq);
-        qn = fma_t(bcoef[s], A.q[o], w);
+        pn = fma_t(bcoef[s], pv[o], zq);
+        qn = fma_t(bcoef[s], qv[o], w);
       }
-      A.p[o] = pn;
-      A.q[o] = qn;
+      pv[o] = pn;
+      qv[o] = qn;
     }
   }
   block_sum<6>(dl, scratch);
@@ -294,25 +299,34 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
   PcgState* st = U.state;
   if (st->stop) return;
   const size_t ld = U.ld;
+  TX* __restrict__ xv = U.x;
+  TX* __restrict__ rv = U.r;
+  const TV* __restrict__ pv = U.p;
+  const TV* __restrict__ qv = U.q;
+  TV* __restrict__ zv = U.z;
+  const TV* __restrict__ dv = U.dinv;
+  TX al[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) al[s] = static_cast<TX>(st->alpha[s]);
   double acc[12];  // rr[0..5], rz[6..11]
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0.0;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < U.n; idx += gridDim.x * blockDim.x) {
     TV D[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) D[q] = U.dinv[q * ld + idx];
+    for (int q = 0; q < 6; ++q) D[q] = dv[q * ld + idx];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      const TX a = static_cast<TX>(st->alpha[s]);
+      const TX a = al[s];
       TX rc[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const size_t o = (c * 6 + s) * ld + idx;
-        TX rq = U.r[o];
+        TX rq = rv[o];
         if (!U.init) {
-          U.x[o] = fma_t(a, static_cast<TX>(U.p[o]), U.x[o]);
-          rq = fma_t(-a, static_cast<TX>(U.q[o]), rq);
-          U.r[o] = rq;
+          xv[o] = fma_t(a, static_cast<TX>(pv[o]), xv[o]);
+          rq = fma_t(-a, static_cast<TX>(qv[o]), rq);
+          rv[o] = rq;
         }
         rc[c] = rq;
       }
@@ -320,9 +334,9 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
       const TV z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
       const TV z1 = D[1] * r0 + D[3] * r1 + D[4] * r2;
       const TV z2 = D[2] * r0 + D[4] * r1 + D[5] * r2;
-      U.z[(0 * 6 + s) * ld + idx] = z0;
-      U.z[(1 * 6 + s) * ld + idx] = z1;
-      U.z[(2 * 6 + s) * ld + idx] = z2;
+      zv[(0 * 6 + s) * ld + idx] = z0;
+      zv[(1 * 6 + s) * ld + idx] = z1;
+      zv[(2 * 6 + s) * ld + idx] = z2;
       const double d0 = rc[0], d1 = rc[1], d2 = rc[2];
       acc[s] += d0 * d0 + d1 * d1 + d2 * d2;
       acc[6 + s] += d0 * static_cast<double>(z0) + d1 * static_cast<double>(z1) +

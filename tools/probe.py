@@ -11,7 +11,8 @@ prof = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 ctx = S.default_context(0)
 ctx.set_profiling(bool(prof))
 spec = S.RandomDesignSpec("cubic_octant", 8, 2, -1.0, 1.0)
-for seed in [1, 1, 2]:
+seeds = [int(x) for x in sys.argv[5].split(",")] if len(sys.argv) > 5 else [1, 1, 2]
+for seed in seeds:
     d = S.random_design(spec, seed)
     t = time.perf_counter()
     res = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, S.HomogenizeOptions(residual_tol=tol, precision=prec), ctx=ctx)
