@@ -360,7 +360,8 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
     throw ShlError(SHL_SOLVER,
                    "mesh has no corner node group: cannot prescribe the strain gauge");
   const int n = c->n_nodes;
-  const int ld = round_up(n + 1, 64);  // slot n of every z plane stays zero
+  // 32-node blocked vectors (solver.cu vbase); node n is an always-zero row
+  const int ld = round_up(n + 1, 32);
   const size_t nX = static_cast<size_t>(18) * ld, nV = nX;
   c->vec.ensure(2 * nX * sizeof(TX) + (3 * nV + 6 * static_cast<size_t>(ld)) * sizeof(TV));
   TX* x = c->vec.as<TX>();
@@ -369,12 +370,13 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   TV* p = z + nV;
   TV* q = p + nV;
   TV* dinv = q + nV;
-  const int grid_u = std::max(1, std::min((n + 255) / 256, c->num_sms * 8));
-  const int grid_a = std::max(1, (n + 255) / 256);
+  // update: (node block, load case) blocks; apply: grid-stride over active nodes
+  const int grid_u = 6 * std::max(1, std::min((n + 255) / 256, c->num_sms * 2));
+  const int grid_a = std::max(1, std::min((n + 255) / 256, c->num_sms * (sizeof(TV) == 4 ? 3 : 2)));
   const int grid_c = std::max(1, std::min(static_cast<int>((c->n_elem + 31) / 32), c->num_sms * 16));
   c->partials.ensure(sizeof(double) *
                      std::max<size_t>({static_cast<size_t>(grid_a) * 6,
-                                       static_cast<size_t>(grid_u) * 12,
+                                       static_cast<size_t>(grid_u) * 2,
                                        static_cast<size_t>(grid_c) * 21, 64}));
   c->state.ensure(sizeof(shl::PcgState));
   c->cout.ensure(36 * sizeof(double));
@@ -407,7 +409,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
                         c->partials.as<double>(), dst, r, n, ld};
   // z0 = Dinv b, then w0 = A z0, p0 = z0, q0 = w0, alpha0
   shl::launch_update<TX, TV>(ua, grid_u, c->stream);
-  shl::launch_apply<TV>(aa, c->stream);
+  shl::launch_apply<TV>(aa, grid_a, c->stream);
   ua.init = 0;
   int64_t launches = 2 + 2;
   int check = opt.check_every > 0 ? opt.check_every : (n < 200000 ? 16 : 32);
@@ -426,11 +428,11 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
         CK(cudaEventRecord(c->prof_ev[3 * issued], c->stream));
         shl::launch_update<TX, TV>(ua, grid_u, c->stream);
         CK(cudaEventRecord(c->prof_ev[3 * issued + 1], c->stream));
-        shl::launch_apply<TV>(aa, c->stream);
+        shl::launch_apply<TV>(aa, grid_a, c->stream);
         CK(cudaEventRecord(c->prof_ev[3 * issued + 2], c->stream));
       } else {
         shl::launch_update<TX, TV>(ua, grid_u, c->stream);
-        shl::launch_apply<TV>(aa, c->stream);
+        shl::launch_apply<TV>(aa, grid_a, c->stream);
       }
       ++issued;
       launches += 2;

@@ -48,6 +48,14 @@ __device__ __forceinline__ float k0<float>(int i) {
 __device__ __forceinline__ float fma_t(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fma_t(double a, double b, double c) { return fma(a, b, c); }
 
+// PCG vectors are stored in 32-node blocks, [idx/32][q][idx%32]: a warp's
+// access to one component q of 32 consecutive nodes is one 128-byte line (FP32)
+// and every component offset is an immediate (q*32 elements) from the node's
+// base address.
+__host__ __device__ __forceinline__ size_t vbase(int idx, int nq) {
+  return static_cast<size_t>(idx >> 5) * (nq * 32) + (idx & 31);
+}
+
 __host__ __device__ constexpr int corner_id(int x, int y, int z) {
   return 4 * z + (y ? (x ? 2 : 3) : (x ? 1 : 0));
 }
@@ -163,9 +171,9 @@ __global__ void setup_kernel(const int* __restrict__ node_list, int n_nodes, int
     for (int q = 0; q < 18; ++q) b[q] = 0.0;
   }
 #pragma unroll
-  for (int q = 0; q < 6; ++q) dinv[static_cast<size_t>(q) * ld + idx] = static_cast<TV>(inv[q]);
+  for (int q = 0; q < 6; ++q) dinv[vbase(idx, 6) + q * 32] = static_cast<TV>(inv[q]);
 #pragma unroll
-  for (int q = 0; q < 18; ++q) rvec[static_cast<size_t>(q) * ld + idx] = static_cast<TX>(b[q]);
+  for (int q = 0; q < 18; ++q) rvec[vbase(idx, 18) + q * 32] = static_cast<TX>(b[q]);
 }
 
 // ---- K4: w = A z by gather, fused with the direction update -------------------
@@ -175,8 +183,67 @@ __global__ void setup_kernel(const int* __restrict__ node_list, int n_nodes, int
 //   w = A z,  p = z + beta p,  q = w + beta q,  delta = z.w
 // One thread per ACTIVE node (no lanes spent on void voxels).  For neighbour m
 // of node n the 3x3 block S_m = sum_{e ni n,m} beta_e K0[a(n,e), b(m,e)] is
-// built once (K0 entries are immediate constant-bank operands) and applied to
-// all six load cases.  Inactive neighbours read a zero slot (index n_nodes).
+// built once (K0 entries are constant-bank operands, single-issue FFMA) and
+// applied to all six load cases.  In FP32 the application runs on packed
+// FFMA2 over load-case pairs (S scalar broadcast x (z_s, z_s+1)), halving the
+// 3-register FFMAs that bound this kernel.  Inactive neighbours read a zero
+// slot (index n_nodes).
+template <typename TV>
+struct GatherAcc;
+
+template <>
+struct GatherAcc<float> {
+  float2 y[9];  // [comp][loadcase pair]
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) y[q] = make_float2(0.f, 0.f);
+  }
+  __device__ __forceinline__ void add(const float (&S)[9], const float* __restrict__ zn) {
+#pragma unroll
+    for (int sp = 0; sp < 3; ++sp) {
+      const float2 z0 = make_float2(zn[(0 * 6 + 2 * sp) * 32], zn[(0 * 6 + 2 * sp + 1) * 32]);
+      const float2 z1 = make_float2(zn[(1 * 6 + 2 * sp) * 32], zn[(1 * 6 + 2 * sp + 1) * 32]);
+      const float2 z2 = make_float2(zn[(2 * 6 + 2 * sp) * 32], zn[(2 * 6 + 2 * sp + 1) * 32]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float2 v = y[c * 3 + sp];
+        v = __ffma2_rn(make_float2(S[c * 3 + 0], S[c * 3 + 0]), z0, v);
+        v = __ffma2_rn(make_float2(S[c * 3 + 1], S[c * 3 + 1]), z1, v);
+        v = __ffma2_rn(make_float2(S[c * 3 + 2], S[c * 3 + 2]), z2, v);
+        y[c * 3 + sp] = v;
+      }
+    }
+  }
+  __device__ __forceinline__ float get(int q) const {  // q = c*6 + s
+    const float2 v = y[(q / 6) * 3 + (q % 6) / 2];
+    return (q & 1) ? v.y : v.x;
+  }
+};
+
+template <>
+struct GatherAcc<double> {
+  double y[18];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < 18; ++q) y[q] = 0.0;
+  }
+  __device__ __forceinline__ void add(const double (&S)[9], const double* __restrict__ zn) {
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const double z0 = zn[(0 * 6 + s) * 32], z1 = zn[(1 * 6 + s) * 32], z2 = zn[(2 * 6 + s) * 32];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double v = y[c * 6 + s];
+        v = fma(S[c * 3 + 0], z0, v);
+        v = fma(S[c * 3 + 1], z1, v);
+        v = fma(S[c * 3 + 2], z2, v);
+        y[c * 6 + s] = v;
+      }
+    }
+  }
+  __device__ __forceinline__ double get(int q) const { return y[q]; }
+};
+
 template <typename TV>
 __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(const ApplyArgs<TV> A) {
   __shared__ double scratch[32 * 6];
@@ -198,10 +265,10 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
   }
   const TV ridge = static_cast<TV>(st->ridge);
   double dl[6] = {0, 0, 0, 0, 0, 0};
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < A.n) {
+  const int rr = r * r;
+  (void)ld;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < A.n; idx += gridDim.x * blockDim.x) {
     const int g = A.node_list[idx];
-    const int rr = r * r;
     const int i = g % r, j = (g / r) % r, k = g / rr;
     const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
     const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
@@ -212,9 +279,8 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
       const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;  // node's corner in e
       be[e] = betav[zs[1 - oz] + ys[1 - oy] + xs[1 - ox]];
     }
-    TV y[18];
-#pragma unroll
-    for (int q = 0; q < 18; ++q) y[q] = TV(0);
+    GatherAcc<TV> acc;
+    acc.zero();
     if (g != 0) {
 #pragma unroll
       for (int m = 0; m < 27; ++m) {
@@ -236,27 +302,16 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
             for (int d = 0; d < 3; ++d)
               S[c * 3 + d] = fma_t(be[e], k0<TV>((3 * a + c) * 24 + 3 * b + d), S[c * 3 + d]);
         }
-#pragma unroll
-        for (int s = 0; s < 6; ++s) {
-          const TV z0 = zv[(0 * 6 + s) * ld + nb], z1 = zv[(1 * 6 + s) * ld + nb],
-                   z2 = zv[(2 * 6 + s) * ld + nb];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            TV v = y[c * 6 + s];
-            v = fma_t(S[c * 3 + 0], z0, v);
-            v = fma_t(S[c * 3 + 1], z1, v);
-            v = fma_t(S[c * 3 + 2], z2, v);
-            y[c * 6 + s] = v;
-          }
-        }
+        acc.add(S, zv + vbase(nb, 18));
       }
     }
+    const size_t ob = vbase(idx, 18);
 #pragma unroll
     for (int q = 0; q < 18; ++q) {
       const int s = q % 6;
-      const size_t o = q * ld + idx;
+      const size_t o = ob + q * 32;
       const TV zq = zv[o];
-      const TV w = g != 0 ? fma_t(ridge, zq, y[q]) : TV(0);
+      const TV w = g != 0 ? fma_t(ridge, zq, acc.get(q)) : TV(0);
       dl[s] += static_cast<double>(zq) * static_cast<double>(w);
       TV pn = TV(0), qn = TV(0);
       if (!dn[s]) {
@@ -293,84 +348,91 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
 
 // ---- K5: vector update + preconditioner + dots ------------------------------
 //   x += alpha p, r -= alpha q, z = Dinv r, partial r.r and r.z
+// One thread per (node, load case): 3 components of x, r, p, q, z and the 6
+// Dinv entries -> ~30 registers, full occupancy, every access a coalesced
+// 32-node plane segment.  blockIdx.x = node_block * 6 + s so the six blocks
+// of a node block run together and Dinv is re-read from L2, not DRAM.
 template <typename TX, typename TV>
 __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U) {
-  __shared__ double scratch[32 * 12];
+  __shared__ double scratch[32 * 2];
   PcgState* st = U.state;
   if (st->stop) return;
-  const size_t ld = U.ld;
   TX* __restrict__ xv = U.x;
   TX* __restrict__ rv = U.r;
   const TV* __restrict__ pv = U.p;
   const TV* __restrict__ qv = U.q;
   TV* __restrict__ zv = U.z;
   const TV* __restrict__ dv = U.dinv;
-  TX al[6];
+  const int s = blockIdx.x % 6;
+  const int nbx = gridDim.x / 6;
+  const TX a = static_cast<TX>(st->alpha[s]);
+  double acc[2] = {0.0, 0.0};  // r.r, r.z for load case s
+  for (int idx = (blockIdx.x / 6) * blockDim.x + threadIdx.x; idx < U.n; idx += nbx * blockDim.x) {
+    const size_t ob = vbase(idx, 18);
+    TX rc[3];
 #pragma unroll
-  for (int s = 0; s < 6; ++s) al[s] = static_cast<TX>(st->alpha[s]);
-  double acc[12];  // rr[0..5], rz[6..11]
-#pragma unroll
-  for (int q = 0; q < 12; ++q) acc[q] = 0.0;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < U.n; idx += gridDim.x * blockDim.x) {
+    for (int c = 0; c < 3; ++c) {
+      const size_t o = ob + (c * 6 + s) * 32;
+      TX rq = rv[o];
+      if (!U.init) {
+        xv[o] = fma_t(a, static_cast<TX>(pv[o]), xv[o]);
+        rq = fma_t(-a, static_cast<TX>(qv[o]), rq);
+        rv[o] = rq;
+      }
+      rc[c] = rq;
+    }
     TV D[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) D[q] = dv[q * ld + idx];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      const TX a = al[s];
-      TX rc[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const size_t o = (c * 6 + s) * ld + idx;
-        TX rq = rv[o];
-        if (!U.init) {
-          xv[o] = fma_t(a, static_cast<TX>(pv[o]), xv[o]);
-          rq = fma_t(-a, static_cast<TX>(qv[o]), rq);
-          rv[o] = rq;
-        }
-        rc[c] = rq;
-      }
-      const TV r0 = static_cast<TV>(rc[0]), r1 = static_cast<TV>(rc[1]), r2 = static_cast<TV>(rc[2]);
-      const TV z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
-      const TV z1 = D[1] * r0 + D[3] * r1 + D[4] * r2;
-      const TV z2 = D[2] * r0 + D[4] * r1 + D[5] * r2;
-      zv[(0 * 6 + s) * ld + idx] = z0;
-      zv[(1 * 6 + s) * ld + idx] = z1;
-      zv[(2 * 6 + s) * ld + idx] = z2;
-      const double d0 = rc[0], d1 = rc[1], d2 = rc[2];
-      acc[s] += d0 * d0 + d1 * d1 + d2 * d2;
-      acc[6 + s] += d0 * static_cast<double>(z0) + d1 * static_cast<double>(z1) +
-                    d2 * static_cast<double>(z2);
-    }
+    for (int q = 0; q < 6; ++q) D[q] = dv[vbase(idx, 6) + q * 32];
+    const TV r0 = static_cast<TV>(rc[0]), r1 = static_cast<TV>(rc[1]), r2 = static_cast<TV>(rc[2]);
+    const TV z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
+    const TV z1 = D[1] * r0 + D[3] * r1 + D[4] * r2;
+    const TV z2 = D[2] * r0 + D[4] * r1 + D[5] * r2;
+    zv[ob + (0 * 6 + s) * 32] = z0;
+    zv[ob + (1 * 6 + s) * 32] = z1;
+    zv[ob + (2 * 6 + s) * 32] = z2;
+    const double d0 = rc[0], d1 = rc[1], d2 = rc[2];
+    acc[0] += d0 * d0 + d1 * d1 + d2 * d2;
+    acc[1] += d0 * static_cast<double>(z0) + d1 * static_cast<double>(z1) + d2 * static_cast<double>(z2);
   }
-  block_sum<12>(acc, scratch);
-  if (publish_partial<12>(acc, U.partials, &st->counter_update)) {
-    double tot[12];
+  block_sum<2>(acc, scratch);
+  if (publish_partial<2>(acc, U.partials, &st->counter_update)) {
     __syncthreads();
-    reduce_partials<12>(U.partials, tot, scratch);
+    // fixed-order reduction per load case: partials[(b*6 + s)*2 + {0,1}]
+    double tot[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) tot[q] = 0.0;
+    for (int b = threadIdx.x; b < nbx; b += blockDim.x)
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        tot[t] += __ldcg(U.partials + (b * 6 + t) * 2 + 0);
+        tot[6 + t] += __ldcg(U.partials + (b * 6 + t) * 2 + 1);
+      }
+    __shared__ double scratch12[32 * 12];
+    block_sum<12>(tot, scratch12);
     if (threadIdx.x == 0) {
       bool all = true;
-      for (int s = 0; s < 6; ++s) {
-        st->rr[s] = tot[s];
-        const double rn = sqrt(tot[s]);
+      for (int t = 0; t < 6; ++t) {
+        st->rr[t] = tot[t];
+        const double rn = sqrt(tot[t]);
         if (U.init) {
-          st->bnorm[s] = rn;
-          st->gamma[s] = tot[6 + s];
-          st->done[s] = rn == 0.0;
-          st->beta[s] = 0.0;
-          st->alpha[s] = 0.0;
-          st->iters[s] = 0;
-        } else if (!st->done[s]) {
-          st->iters[s] = st->it + 1;  // grid_solver.hpp:67
-          if (rn <= st->tol * st->bnorm[s]) {  // grid_solver.hpp:68-72
-            st->done[s] = 1;
-            st->beta[s] = 0.0;
+          st->bnorm[t] = rn;
+          st->gamma[t] = tot[6 + t];
+          st->done[t] = rn == 0.0;
+          st->beta[t] = 0.0;
+          st->alpha[t] = 0.0;
+          st->iters[t] = 0;
+        } else if (!st->done[t]) {
+          st->iters[t] = st->it + 1;  // grid_solver.hpp:67
+          if (rn <= st->tol * st->bnorm[t]) {  // grid_solver.hpp:68-72
+            st->done[t] = 1;
+            st->beta[t] = 0.0;
           } else {
-            st->beta[s] = tot[6 + s] / st->gamma[s];
-            st->gamma[s] = tot[6 + s];
+            st->beta[t] = tot[6 + t] / st->gamma[t];
+            st->gamma[t] = tot[6 + t];
           }
         }
-        all = all && st->done[s];
+        all = all && st->done[t];
       }
       if (!U.init) st->it += 1;
       st->all_done = all;
@@ -408,7 +470,7 @@ __global__ void __launch_bounds__(32) chom_kernel(const ChomArgs<TX> Cg) {
 #pragma unroll
         for (int s = 0; s < 6; ++s)
           U[(3 * n + c) * 6 + s] =
-              (idx >= 0 ? static_cast<double>(Cg.x[(c * 6 + s) * static_cast<size_t>(Cg.ld) + idx]) : 0.0) +
+              (idx >= 0 ? static_cast<double>(Cg.x[vbase(idx, 18) + (c * 6 + s) * 32]) : 0.0) +
               c_T[(3 * n + c) * 6 + s];
     }
 #pragma unroll 1
@@ -473,9 +535,8 @@ void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double
 }
 
 template <typename TV>
-void launch_apply(const ApplyArgs<TV>& a, cudaStream_t s) {
-  if (a.n == 0) return;
-  apply_kernel<TV><<<(a.n + 255) / 256, 256, 0, s>>>(a);
+void launch_apply(const ApplyArgs<TV>& a, int grid, cudaStream_t s) {
+  apply_kernel<TV><<<grid, 256, 0, s>>>(a);
 }
 
 template <typename TX, typename TV>
@@ -494,8 +555,8 @@ template void launch_setup<double, float>(const int*, int, int, int, const doubl
                                           float*, cudaStream_t);
 template void launch_setup<float, float>(const int*, int, int, int, const double*, double, float*,
                                          float*, cudaStream_t);
-template void launch_apply<double>(const ApplyArgs<double>&, cudaStream_t);
-template void launch_apply<float>(const ApplyArgs<float>&, cudaStream_t);
+template void launch_apply<double>(const ApplyArgs<double>&, int, cudaStream_t);
+template void launch_apply<float>(const ApplyArgs<float>&, int, cudaStream_t);
 template void launch_update<double, double>(const UpdateArgs<double, double>&, int, cudaStream_t);
 template void launch_update<double, float>(const UpdateArgs<double, float>&, int, cudaStream_t);
 template void launch_update<float, float>(const UpdateArgs<float, float>&, int, cudaStream_t);

@@ -59,7 +59,7 @@ template <typename TX, typename TV>
 void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64,
                   double ridge, TX* rvec, TV* dinv, cudaStream_t s);
 template <typename TV>
-void launch_apply(const ApplyArgs<TV>& a, cudaStream_t s);
+void launch_apply(const ApplyArgs<TV>& a, int grid, cudaStream_t s);
 template <typename TX, typename TV>
 void launch_update(const UpdateArgs<TX, TV>& u, int grid, cudaStream_t s);
 template <typename TX>
