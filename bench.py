@@ -268,8 +268,9 @@ def run_ours(args, rank, world, local):
     achieved = alg_bytes / avg_launch_s / 1e9
     nt = ncu_traffic()
     traffic = None
-    if nt and nt.get("kernel", "").split(" ")[0] == kname.split(" ")[0] and nt.get("per_node_bytes"):
-        traffic = nt["per_node_bytes"] * nodes
+    kn = kname.split(" ")[0]
+    if nt and kn in nt.get("kernels", {}):
+        traffic = nt["kernels"][kn]["per_node_bytes"] * nodes
     iter_bytes = (bytes_apply + bytes_update) * nodes
     iter_s = (apply_ms + update_ms) / 1e3 / max(launches_apply, 1)
 

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libshellular_cuda.so")
+LIB_PATH = os.environ.get("SHL_LIB") or os.path.join(HERE, "libshellular_cuda.so")
 
 SHL_OK, SHL_VALIDATION, SHL_DEGENERATE, SHL_SOLVER, SHL_IO, SHL_CUDA = range(6)
 PREC_AUTO, PREC_FP64, PREC_MIXED, PREC_FP32 = -1, 0, 1, 2

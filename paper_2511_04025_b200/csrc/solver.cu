@@ -368,29 +368,44 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
   const TX a = static_cast<TX>(st->alpha[s]);
   double acc[2] = {0.0, 0.0};  // r.r, r.z for load case s
   for (int idx = (blockIdx.x / 6) * blockDim.x + threadIdx.x; idx < U.n; idx += nbx * blockDim.x) {
-    const size_t ob = vbase(idx, 18);
-    TX rc[3];
+    const size_t ob = vbase(idx, 18) + s * 32;
+    const size_t od = vbase(idx, 6);
+    // all loads first (keeps ~15 independent requests in flight per thread)
+    TX xc[3], rc[3];
+    TV pc[3], qc[3], D[6];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const size_t o = ob + (c * 6 + s) * 32;
-      TX rq = rv[o];
-      if (!U.init) {
-        xv[o] = fma_t(a, static_cast<TX>(pv[o]), xv[o]);
-        rq = fma_t(-a, static_cast<TX>(qv[o]), rq);
-        rv[o] = rq;
+    for (int c = 0; c < 3; ++c) rc[c] = rv[ob + c * 192];
+    if (!U.init) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xc[c] = xv[ob + c * 192];
+        pc[c] = pv[ob + c * 192];
+        qc[c] = qv[ob + c * 192];
       }
-      rc[c] = rq;
     }
-    TV D[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) D[q] = dv[vbase(idx, 6) + q * 32];
+    for (int q = 0; q < 6; ++q) D[q] = dv[od + q * 32];
+    if (!U.init) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xc[c] = fma_t(a, static_cast<TX>(pc[c]), xc[c]);
+        rc[c] = fma_t(-a, static_cast<TX>(qc[c]), rc[c]);
+      }
+    }
     const TV r0 = static_cast<TV>(rc[0]), r1 = static_cast<TV>(rc[1]), r2 = static_cast<TV>(rc[2]);
     const TV z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
     const TV z1 = D[1] * r0 + D[3] * r1 + D[4] * r2;
     const TV z2 = D[2] * r0 + D[4] * r1 + D[5] * r2;
-    zv[ob + (0 * 6 + s) * 32] = z0;
-    zv[ob + (1 * 6 + s) * 32] = z1;
-    zv[ob + (2 * 6 + s) * 32] = z2;
+    if (!U.init) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xv[ob + c * 192] = xc[c];
+        rv[ob + c * 192] = rc[c];
+      }
+    }
+    zv[ob + 0 * 192] = z0;
+    zv[ob + 1 * 192] = z1;
+    zv[ob + 2 * 192] = z2;
     const double d0 = rc[0], d1 = rc[1], d2 = rc[2];
     acc[0] += d0 * d0 + d1 * d1 + d2 * d2;
     acc[1] += d0 * static_cast<double>(z0) + d1 * static_cast<double>(z1) + d2 * static_cast<double>(z2);
