@@ -15,6 +15,8 @@
  *                             effective_tensor       fem.hpp:179-428
  *   shl_homogenize         <- homogenize             pipeline.hpp:61-113
  *   shl_homogenize_batch   <- (new) many designs, one call (SPEC sample_campaign)
+ *   shl_homogenize_slabs / shl_homogenize_zslab
+ *                          <- (new) z-slab decomposition of one design (C5)
  *   shl_element_stiffness  <- element_stiffness      fem.hpp:50-92
  *   shl_random_design      <- random_design          field.hpp:569-593
  *   shl_expand_symmetry    <- expand_symmetry        field.hpp:236-249
@@ -158,6 +160,24 @@ int shl_homogenize_batch(shl_ctx* ctx, int n, const shl_design* designs,
                          const shl_shell_params* sp, const shl_material* mat, int r,
                          const shl_solve_options* opt, double* C_out, shl_stats* stats,
                          int32_t* status);
+
+/* z-slab decomposition of one design's solve (config C5, SURVEY.md §8 e):
+ * the torus is split into n_slabs slabs of whole z-planes with one ghost
+ * plane per side; per PCG iteration one ghost exchange of z and two small
+ * cross-slab sums.
+ *   shl_homogenize_slabs : all slabs in this context on one device (the
+ *                          exchange is a device copy) -- parity/testing
+ *   shl_homogenize_zslab : one slab per rank over NCCL (libnccl dlopen'ed);
+ *                          nccl_id from shl_nccl_unique_id on rank 0,
+ *                          broadcast by the caller (e.g. torch.distributed). */
+int shl_homogenize_slabs(shl_ctx* ctx, int n_slabs, const shl_design* design,
+                         const shl_shell_params* sp, const shl_material* mat, int r,
+                         const shl_solve_options* opt, double* C_out, shl_stats* stats);
+int shl_nccl_unique_id(uint8_t* id_out /*128 bytes*/);
+int shl_homogenize_zslab(shl_ctx* ctx, const uint8_t* nccl_id, int rank, int nranks,
+                         const shl_design* design, const shl_shell_params* sp,
+                         const shl_material* mat, int r, const shl_solve_options* opt,
+                         double* C_out, shl_stats* stats);
 
 /* Host helpers (reference arithmetic, no device work). */
 int shl_element_stiffness(const shl_material* mat, double edge, double* K_out /*576*/);

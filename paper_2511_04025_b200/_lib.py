@@ -54,6 +54,7 @@ EXPORTS = (
     "shl_sample_grid", "shl_load_grid", "shl_classify_surface", "shl_build_reduced_mesh",
     "shl_grid_solve", "shl_solve_mesh", "shl_homogenize", "shl_homogenize_batch",
     "shl_element_stiffness", "shl_random_design", "shl_expand_symmetry",
+    "shl_homogenize_slabs", "shl_nccl_unique_id", "shl_homogenize_zslab",
 )
 
 _lib = None
@@ -93,5 +94,12 @@ def lib() -> C.CDLL:
     L.shl_random_design.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                     C.c_uint64, vp, vp, vp]
     L.shl_expand_symmetry.argtypes = [P(shl_design), vp, vp, P(C.c_int32)]
+    L.shl_homogenize_slabs.argtypes = [vp, C.c_int, P(shl_design), P(shl_shell_params),
+                                       P(shl_material), C.c_int, P(shl_solve_options), vp,
+                                       P(shl_stats)]
+    L.shl_nccl_unique_id.argtypes = [vp]
+    L.shl_homogenize_zslab.argtypes = [vp, vp, C.c_int, C.c_int, P(shl_design),
+                                       P(shl_shell_params), P(shl_material), C.c_int,
+                                       P(shl_solve_options), vp, P(shl_stats)]
     _lib = L
     return L

@@ -467,3 +467,50 @@ def homogenize_batch(designs: Sequence[DesignParams], sp: ShellParams, mat: Base
            ctx)
     return (Cm[: 36 * n].reshape(n, 6, 6), status[:n].copy(),
             [SolveStats.from_abi(stats[i]) for i in range(n)])
+
+
+# ---- z-slab decomposition of one design (config C5) -----------------------------
+def homogenize_slabs(params: DesignParams, sp: ShellParams, mat: BaseMaterial, r: int,
+                     n_slabs: int, opt: HomogenizeOptions = HomogenizeOptions(),
+                     ctx: Context | None = None) -> HomogenizationResult:
+    """The z-slab solver with all `n_slabs` slabs in one context (device-copy
+    ghost exchange, fixed-order cross-slab sums) -- the multi-rank code path
+    exercised on a single GPU."""
+    ctx = ctx or default_context()
+    d, keep = params._abi()
+    spa, ma, oa = sp._abi(), mat._abi(), opt._abi()
+    Cm = np.zeros(36)
+    st = L.shl_stats()
+    _check(L.lib().shl_homogenize_slabs(ctx.handle, int(n_slabs), C.byref(d), C.byref(spa),
+                                        C.byref(ma), int(r), C.byref(oa), Cm.ctypes.data,
+                                        C.byref(st)), ctx)
+    s = SolveStats.from_abi(st)
+    return HomogenizationResult(Cm.reshape(6, 6), int(r), s.timings, s.volume_ratio,
+                                s.n_elements / float(r) ** 3, f"device_pcg_{s.precision}_zslab{n_slabs}",
+                                s.iterations, s)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(L.lib().shl_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def homogenize_zslab(params: DesignParams, sp: ShellParams, mat: BaseMaterial, r: int,
+                     nccl_id: bytes, rank: int, nranks: int,
+                     opt: HomogenizeOptions = HomogenizeOptions(),
+                     ctx: Context | None = None) -> HomogenizationResult:
+    """One z-slab per rank over NCCL (every rank passes the same nccl_id)."""
+    ctx = ctx or default_context()
+    d, keep = params._abi()
+    spa, ma, oa = sp._abi(), mat._abi(), opt._abi()
+    idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+    Cm = np.zeros(36)
+    st = L.shl_stats()
+    _check(L.lib().shl_homogenize_zslab(ctx.handle, idb, int(rank), int(nranks), C.byref(d),
+                                        C.byref(spa), C.byref(ma), int(r), C.byref(oa),
+                                        Cm.ctypes.data, C.byref(st)), ctx)
+    s = SolveStats.from_abi(st)
+    return HomogenizationResult(Cm.reshape(6, 6), int(r), s.timings, s.volume_ratio,
+                                s.n_elements / float(r) ** 3, f"device_pcg_{s.precision}_zslab",
+                                s.iterations, s)

@@ -1,0 +1,165 @@
+// context.h -- the shl_ctx device context and the host-side stage helpers
+// shared by shl_api.cu (single-device pipeline) and slab.cu (z-slab
+// decomposition).  Internal; not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "internal.h"
+#include "solver.cuh"
+
+using shl::ShlError;
+
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw ShlError(SHL_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace shl {
+namespace host {
+
+extern thread_local std::string g_thread_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 8 + 256;
+    CK(cudaMalloc(&p, want));
+    cap = want;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+// Small device-side bookkeeping block, mirrored into pinned host memory.
+struct Misc {
+  unsigned long long norm_bits;
+  int n_surface;
+  int touches;
+  int n_nodes;
+  int n_elem;
+  int pad0;
+  int node0_active;
+  double beta_sum;
+  double pad[4];
+};
+
+inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+}  // namespace host
+}  // namespace shl
+
+struct shl_ctx {
+  using DevBuf = shl::host::DevBuf;
+  using Misc = shl::host::Misc;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  bool profiling = false;
+  int64_t launches = 0;
+  int64_t h2d = 0, d2h = 0;  // bytes across PCIe (counted at each copy)
+
+  // resident grid
+  int r = 0;
+  bool grid_ready = false, mesh_ready = false;
+  double norm = 0.0;
+  DevBuf tab, coeff, sl, sign8, centres, corners, csign, misc;
+  // mesh + topology
+  DevBuf occ0, occ1, beta64, beta32, elem_flag, node_flag, off, node_map, node_list, elem_list,
+      scan_tmp, beta_partials;
+  int64_t n_surface = 0, n_elem = 0;
+  int n_nodes = 0, full_fallback = 0, node0_active = 0;
+  double volume_ratio = 0.0, beta_sum = 0.0;
+  // solver
+  DevBuf vec, partials, state, cout;
+  Misc* hmisc = nullptr;
+  shl::PcgState* hstate = nullptr;
+  double* hC = nullptr;
+  cudaEvent_t ev[12] = {};
+  void* nccl = nullptr;  // z-slab communicator (slab.cu), created on demand
+  void (*nccl_deleter)(void*) = nullptr;
+  std::vector<cudaEvent_t> prof_ev;
+
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+  float ms(int a, int b) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, ev[a], ev[b]));
+    return t;
+  }
+};
+
+namespace shl {
+namespace host {
+
+template <class Fn>
+int guarded(shl_ctx* ctx, Fn&& fn) {
+  try {
+    if (ctx) CK(cudaSetDevice(ctx->device));
+    fn();
+    if (ctx) ctx->err.clear();
+    return SHL_OK;
+  } catch (const ShlError& e) {
+    if (ctx) ctx->err = e.what();
+    g_thread_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    g_thread_error = e.what();
+    return SHL_IO;
+  }
+}
+
+template <class Fn>
+auto tagged(const char* stage, Fn&& fn) {
+  try {
+    return fn();
+  } catch (const ShlError& e) {
+    if (e.code == SHL_CUDA || e.code == SHL_IO) throw;
+    throw ShlError(e.code, std::string(stage) + ": " + e.what());
+  }
+}
+
+struct FieldInputs {
+  int r = 0, nc = 0, n = 0;
+  std::vector<double> coeff, tab;
+  std::vector<int8_t> sign;
+  size_t h2d_bytes() const { return (coeff.size() + tab.size()) * sizeof(double) + sign.size(); }
+};
+
+void require_r(int r);
+void alloc_grid(shl_ctx* c, int r);
+FieldInputs prepare_field(const HostDesign& d, int r);
+void run_field(shl_ctx* c, const FieldInputs& f);
+void read_norm(shl_ctx* c);
+void build_topology(shl_ctx* c);
+void run_mesh(shl_ctx* c, const shl_shell_params& sp);
+int resolve_precision(const shl_solve_options& o);
+void element_loads(const double* K0, int r, double* T, double* W);
+void fill_mesh_stats(shl_ctx* c, shl_stats* st);
+shl_solve_options default_opts(const shl_solve_options* o);
+void validate_inputs(const shl_design* design, const shl_shell_params* sp, const shl_material* mat,
+                     int r, double* K0_out);
+
+}  // namespace host
+}  // namespace shl

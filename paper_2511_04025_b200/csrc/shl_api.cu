@@ -21,56 +21,14 @@
 #include <string>
 #include <vector>
 
-#include "device.cuh"
-#include "internal.h"
-#include "solver.cuh"
+#include "context.h"
 
 using shl::ShlError;
 
-namespace {
+namespace shl {
+namespace host {
 
 thread_local std::string g_thread_error;
-
-#define CK(call)                                                                      \
-  do {                                                                                \
-    cudaError_t e_ = (call);                                                          \
-    if (e_ != cudaSuccess)                                                            \
-      throw ShlError(SHL_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  void ensure(size_t bytes) {
-    if (bytes <= cap) return;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-    size_t want = bytes + bytes / 8 + 256;
-    CK(cudaMalloc(&p, want));
-    cap = want;
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
-};
-
-// Small device-side bookkeeping block, mirrored into pinned host memory.
-struct Misc {
-  unsigned long long norm_bits;
-  int n_surface;
-  int touches;
-  int n_nodes;
-  int n_elem;
-  int pad0;
-  int node0_active;
-  double beta_sum;
-  double pad[4];
-};
 
 __global__ void finalize_counts_kernel(Misc* m, const int* node_flag, const int* node_off,
                                        const int* elem_flag, const int* elem_off, int n3,
@@ -92,7 +50,6 @@ __global__ void finalize_counts_kernel(Misc* m, const int* node_flag, const int*
   }
 }
 
-inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // element-local affine loads T (grid_solver.hpp:119-126) and W = K0*T
 void element_loads(const double* K0, int r, double* T, double* W) {
@@ -117,73 +74,6 @@ void element_loads(const double* K0, int r, double* T, double* W) {
     }
 }
 
-}  // namespace
-
-struct shl_ctx {
-  int device = 0;
-  int num_sms = 148;
-  cudaStream_t stream = nullptr;
-  std::string err;
-  bool profiling = false;
-  int64_t launches = 0;
-  int64_t h2d = 0, d2h = 0;  // bytes across PCIe (counted at each copy)
-
-  // resident grid
-  int r = 0;
-  bool grid_ready = false, mesh_ready = false;
-  double norm = 0.0;
-  DevBuf tab, coeff, sl, sign8, centres, corners, csign, misc;
-  // mesh + topology
-  DevBuf occ0, occ1, beta64, beta32, elem_flag, node_flag, off, node_map, node_list, elem_list,
-      scan_tmp, beta_partials;
-  int64_t n_surface = 0, n_elem = 0;
-  int n_nodes = 0, full_fallback = 0, node0_active = 0;
-  double volume_ratio = 0.0, beta_sum = 0.0;
-  // solver
-  DevBuf vec, partials, state, cout;
-  Misc* hmisc = nullptr;
-  shl::PcgState* hstate = nullptr;
-  double* hC = nullptr;
-  cudaEvent_t ev[12] = {};
-  std::vector<cudaEvent_t> prof_ev;
-
-  void sync() { CK(cudaStreamSynchronize(stream)); }
-  float ms(int a, int b) {
-    float t = 0.f;
-    CK(cudaEventElapsedTime(&t, ev[a], ev[b]));
-    return t;
-  }
-};
-
-namespace {
-
-template <class Fn>
-int guarded(shl_ctx* ctx, Fn&& fn) {
-  try {
-    if (ctx) CK(cudaSetDevice(ctx->device));
-    fn();
-    if (ctx) ctx->err.clear();
-    return SHL_OK;
-  } catch (const ShlError& e) {
-    if (ctx) ctx->err = e.what();
-    g_thread_error = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    if (ctx) ctx->err = e.what();
-    g_thread_error = e.what();
-    return SHL_IO;
-  }
-}
-
-template <class Fn>
-auto tagged(const char* stage, Fn&& fn) {
-  try {
-    return fn();
-  } catch (const ShlError& e) {
-    if (e.code == SHL_CUDA || e.code == SHL_IO) throw;
-    throw ShlError(e.code, std::string(stage) + ": " + e.what());
-  }
-}
 
 void require_r(int r) {
   if (r < 4) throw ShlError(SHL_VALIDATION, "grid resolution must be >= 4");
@@ -202,12 +92,7 @@ void alloc_grid(shl_ctx* c, int r) {
 // ---- field (sample_grid, field.hpp:488-534) --------------------------------
 // Host half: reference arithmetic that must match glibc bit for bit
 // (expansion, coefficients, cosine tables).  Device half: K1.
-struct FieldInputs {
-  int r = 0, nc = 0, n = 0;
-  std::vector<double> coeff, tab;
-  std::vector<int8_t> sign;
-  size_t h2d_bytes() const { return (coeff.size() + tab.size()) * sizeof(double) + sign.size(); }
-};
+
 
 FieldInputs prepare_field(const shl::HostDesign& d, int r) {
   require_r(r);
@@ -404,9 +289,10 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   shl::PcgState* dst = c->state.as<shl::PcgState>();
   const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
                                          : reinterpret_cast<const TV*>(c->beta32.p);
-  shl::UpdateArgs<TX, TV> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1};
+  shl::UpdateArgs<TX, TV> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1,
+                            nullptr, 0};
   shl::ApplyArgs<TV> aa{c->node_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p, q,
-                        c->partials.as<double>(), dst, r, n, ld};
+                        c->partials.as<double>(), dst, r, n, ld, n, 0, r, nullptr, 0};
   // z0 = Dinv b, then w0 = A z0, p0 = z0, q0 = w0, alpha0
   shl::launch_update<TX, TV>(ua, grid_u, c->stream);
   shl::launch_apply<TV>(aa, grid_a, c->stream);
@@ -468,7 +354,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   }
   shl::ChomArgs<TX> ca{c->elem_list.as<int>(), c->node_map.as<int>(), c->beta64.as<double>(), x,
                        c->partials.as<double>(), c->cout.as<double>(), dst,
-                       static_cast<int>(c->n_elem), r, ld};
+                       static_cast<int>(c->n_elem), r, ld, 0, r, 0};
   shl::launch_chom<TX>(ca, grid_c, c->stream);
   launches += 1;
   CK(cudaGetLastError());
@@ -524,17 +410,24 @@ shl_solve_options default_opts(const shl_solve_options* o) {
   return d;
 }
 
-void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params* sp,
-                    const shl_material* mat, int r, const shl_solve_options* o, double* C_out,
-                    shl_stats* st) {
-  if (!design || !sp || !mat || !C_out) throw ShlError(SHL_VALIDATION, "null argument");
-  const shl_solve_options opt = default_opts(o);
-  double K0[576];
+// homogenize's own checks (pipeline.hpp:64-65: mat.validate, sp.validate) + K0
+void validate_inputs(const shl_design* design, const shl_shell_params* sp, const shl_material* mat,
+                     int r, double* K0) {
+  if (!design || !sp || !mat) throw ShlError(SHL_VALIDATION, "null argument");
   shl::element_stiffness(mat->youngs, mat->poisson, 1.0 / std::max(r, 1), K0);  // mat.validate
   if (!(sp->sharpness > 0.0)) throw ShlError(SHL_VALIDATION, "sharpness must be positive");
   if (!(sp->floor_ratio > 0.0 && sp->floor_ratio < 1.0))
     throw ShlError(SHL_VALIDATION, "floor must lie in (0, 1)");
   if (sp->expand_layers < 0) throw ShlError(SHL_VALIDATION, "expand_layers must be >= 0");
+}
+
+void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params* sp,
+                    const shl_material* mat, int r, const shl_solve_options* o, double* C_out,
+                    shl_stats* st) {
+  if (!C_out) throw ShlError(SHL_VALIDATION, "null argument");
+  const shl_solve_options opt = default_opts(o);
+  double K0[576];
+  validate_inputs(design, sp, mat, r, K0);
   const int64_t l0 = c->launches, h0 = c->h2d, d0 = c->d2h;
   FieldInputs fin = tagged("field", [&] { return prepare_field(shl::HostDesign::from_abi(*design), r); });
   CK(cudaEventRecord(c->ev[0], c->stream));
@@ -567,7 +460,11 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
   }
 }
 
-}  // namespace
+}  // namespace host
+}  // namespace shl
+
+using namespace shl::host;
+
 
 // =============================== C ABI =======================================
 extern "C" {
@@ -595,6 +492,7 @@ void shl_ctx_destroy(shl_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->nccl && c->nccl_deleter) c->nccl_deleter(c->nccl);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->prof_ev)

@@ -1,0 +1,468 @@
+// slab.cu -- z-slab domain decomposition of ONE design's solve (config C5).
+//
+// the torus is split into G slabs of whole z-planes; slab
+// s owns the active nodes of planes [z0, z1) and keeps one ghost plane on
+// each side (z0-1 and z1, periodic).  Field and mask are computed in full by
+// every rank (they cost ~0.5 ms at 256^3, less than the setup exchange they
+// would need), so the decomposition applies to the solver, where the time
+// goes.  Per PCG iteration:
+//   update (owned nodes)        -> 12 partial sums  -> cross-slab SUM -> scalars
+//   ghost exchange of z (2 planes of 18 components, one per neighbour)
+//   apply  (owned nodes, gathers owned + ghost z) -> 6 partial sums -> SUM
+// and once at the end an x ghost exchange + the C^H partial sums.
+//
+// Two transports share every kernel and index map:
+//   * emulated: G slabs in one context on one device; the exchange is a
+//     pack/unpack device copy and the cross-slab sum is a fixed-order finalize
+//     kernel.  Used by the parity tests (no second GPU needed, and no ranks
+//     waiting on each other on one device).
+//   * NCCL: one slab per rank; ncclSend/ncclRecv of packed ghost planes
+//     (periodic ring over NVLink/NVSwitch) and ncclAllReduce of the partial
+//     sums.  libnccl is dlopen'ed on first use so the single-GPU library
+//     never depends on it.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+#include <type_traits>
+#include <string>
+#include <vector>
+
+#include "context.h"
+
+namespace shl {
+namespace host {
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  void* handle = nullptr;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    // prefer an already-loaded NCCL (torch's), then the system one
+    a.handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!a.handle) a.handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!a.handle) return a;
+    auto sym = [&](const char* n) { return dlsym(a.handle, n); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    return a;
+  }();
+  if (!api.handle || !api.AllReduce || !api.Send)
+    throw ShlError(SHL_CUDA, "libnccl.so.2 could not be loaded for the z-slab transport");
+  return api;
+}
+
+#define NK(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      throw ShlError(SHL_CUDA, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+struct NcclComm {
+  ncclComm_t comm = nullptr;
+  unsigned char id[NCCL_UNIQUE_ID_BYTES] = {};
+  int rank = -1, nranks = 0;
+  ~NcclComm() {
+    if (comm) nccl().CommDestroy(comm);
+  }
+};
+
+// ---------------------------------------------------------------- slab plan
+struct SlabPlan {
+  int z0 = 0, z1 = 0;       // owned planes [z0, z1)
+  int zbase = 0, nzl = 0;   // node-map planes: zbase = z0-1 (mod r), nzl = z1-z0+2
+  int n_owned = 0, n_glo = 0, n_ghi = 0, n_local = 0;
+  int cnt_first = 0, cnt_last = 0;  // owned nodes on planes z0 and z1-1
+  int e_lo = 0, e_hi = 0;           // owned elements: range of the global element list
+  int noff_z0 = 0;                  // global node id of the first owned node
+};
+
+struct Slab {
+  SlabPlan P;
+  DevBuf map, list, vec, partials;
+  size_t ld = 0;
+};
+
+namespace {
+
+__global__ void plane_count_kernel(const int* __restrict__ flag, int r, int* __restrict__ out) {
+  const int z = blockIdx.x;
+  const size_t rr = static_cast<size_t>(r) * r;
+  int s = 0;
+  for (size_t t = threadIdx.x; t < rr; t += blockDim.x) s += flag[z * rr + t];
+  s = __reduce_add_sync(0xffffffffu, s);
+  __shared__ int w[32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int q = 0; q < (blockDim.x + 31) / 32; ++q) t += w[q];
+    out[z] = t;
+  }
+}
+
+// local node map over planes zbase .. zbase+nzl-1 and local -> grid id list
+__global__ void slab_map_kernel(const int* __restrict__ node_flag, const int* __restrict__ goff,
+                                int r, SlabPlan P, const int* __restrict__ plane_off,
+                                int* __restrict__ map, int* __restrict__ list) {
+  const size_t rr = static_cast<size_t>(r) * r;
+  const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (t >= rr * P.nzl) return;
+  const int lp = static_cast<int>(t / rr);
+  const int gz = (P.zbase + lp) % r;
+  const size_t g = gz * rr + t % rr;
+  int id = -1;
+  if (node_flag[g]) {
+    const int pid = goff[g] - plane_off[gz];  // index inside its plane
+    if (lp == 0)
+      id = P.n_owned + pid;
+    else if (lp == P.nzl - 1)
+      id = P.n_owned + P.n_glo + pid;
+    else
+      id = goff[g] - P.noff_z0;
+    list[id] = static_cast<int>(g);
+  }
+  map[t] = id;
+}
+
+}  // namespace
+
+// Build the G slab plans + device maps from the resident global mesh.
+void build_slabs(shl_ctx* c, int G, int first, int count, std::vector<Slab>& slabs) {
+  const int r = c->r;
+  if (G < 2 || G > r / 2) throw ShlError(SHL_VALIDATION, "z-slab count must lie in [2, r/2]");
+  DevBuf counts;
+  counts.ensure(sizeof(int) * (3 * r + 1));
+  int* ncnt = counts.as<int>();
+  int* ecnt = ncnt + r;
+  int* noff_dev = ecnt + r;
+  plane_count_kernel<<<r, 256, 0, c->stream>>>(c->node_flag.as<int>(), r, ncnt);
+  plane_count_kernel<<<r, 256, 0, c->stream>>>(c->elem_flag.as<int>(), r, ecnt);
+  CK(cudaGetLastError());
+  std::vector<int> h(2 * r);
+  CK(cudaMemcpyAsync(h.data(), ncnt, sizeof(int) * 2 * r, cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  std::vector<int> noff(r + 1, 0), eoff(r + 1, 0);
+  for (int z = 0; z < r; ++z) {
+    noff[z + 1] = noff[z] + h[z];
+    eoff[z + 1] = eoff[z] + h[r + z];
+  }
+  CK(cudaMemcpyAsync(noff_dev, noff.data(), sizeof(int) * r, cudaMemcpyHostToDevice, c->stream));
+  slabs.clear();
+  slabs.resize(count);
+  for (int q = 0; q < count; ++q) {
+    const int s = first + q;
+    SlabPlan& P = slabs[q].P;
+    P.z0 = static_cast<int>(static_cast<long long>(s) * r / G);
+    P.z1 = static_cast<int>(static_cast<long long>(s + 1) * r / G);
+    P.zbase = (P.z0 - 1 + r) % r;
+    P.nzl = P.z1 - P.z0 + 2;
+    P.n_owned = noff[P.z1] - noff[P.z0];
+    P.n_glo = h[(P.z0 - 1 + r) % r];
+    P.n_ghi = h[P.z1 % r];
+    P.n_local = P.n_owned + P.n_glo + P.n_ghi;
+    P.cnt_first = h[P.z0];
+    P.cnt_last = h[P.z1 - 1];
+    P.e_lo = eoff[P.z0];
+    P.e_hi = eoff[P.z1];
+    P.noff_z0 = noff[P.z0];
+    Slab& S = slabs[q];
+    const size_t cells = static_cast<size_t>(r) * r * P.nzl;
+    S.map.ensure(cells * sizeof(int));
+    S.list.ensure((static_cast<size_t>(P.n_local) + 1) * sizeof(int));
+    slab_map_kernel<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, c->stream>>>(
+        c->node_flag.as<int>(), c->off.as<int>(), r, P, noff_dev, S.map.as<int>(), S.list.as<int>());
+    CK(cudaGetLastError());
+  }
+  c->sync();  // `counts` dies here
+}
+
+// ---------------------------------------------------------------- solve
+template <typename TX, typename TV>
+void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
+                     shl_stats* st, int prec, int G, NcclComm* comm) {
+  const int r = c->r;
+  if (!c->node0_active)
+    throw ShlError(SHL_SOLVER, "mesh has no corner node group: cannot prescribe the strain gauge");
+  const bool dist = comm != nullptr;
+  const int first = dist ? comm->rank : 0;
+  const int nloc = dist ? 1 : G;  // slabs driven by this process
+  std::vector<Slab> slabs;
+  build_slabs(c, G, first, nloc, slabs);
+
+  int max_local = 0, max_plane = 0;
+  for (auto& S : slabs) {
+    const SlabPlan& P = S.P;
+    S.ld = round_up(P.n_local + 1, 32);
+    const size_t nX = 18 * S.ld;
+    S.vec.ensure(2 * nX * sizeof(TX) + (3 * nX + 6 * S.ld) * sizeof(TV));
+    S.partials.ensure(sizeof(double) * 21 * 2400);
+    max_local = std::max(max_local, P.n_local);
+    max_plane = std::max({max_plane, P.n_glo, P.n_ghi, P.cnt_first, P.cnt_last});
+  }
+  (void)max_local;
+  DevBuf tot, xfer;
+  tot.ensure(sizeof(double) * 21 * nloc);
+  xfer.ensure(4 * 18 * static_cast<size_t>(std::max(max_plane, 1)) * sizeof(double));
+  c->state.ensure(sizeof(PcgState));
+  c->cout.ensure(36 * sizeof(double));
+
+  auto X = [&](Slab& S) { return S.vec.as<TX>(); };
+  auto R = [&](Slab& S) { return S.vec.as<TX>() + 18 * S.ld; };
+  auto Z = [&](Slab& S) { return reinterpret_cast<TV*>(S.vec.as<TX>() + 36 * S.ld); };
+  auto Pv = [&](Slab& S) { return Z(S) + 18 * S.ld; };
+  auto Q = [&](Slab& S) { return Z(S) + 36 * S.ld; };
+  auto D = [&](Slab& S) { return Z(S) + 54 * S.ld; };
+
+  double T[144], W[144];
+  element_loads(K0, r, T, W);
+  const double ridge = c->n_nodes > 0 ? 1e-11 * std::fabs(K0[0]) * 8.0 * c->beta_sum / double(c->n_nodes) : 0.0;
+  CK(cudaEventRecord(c->ev[3], c->stream));
+  upload_element_constants(K0, W, T, c->stream);
+  for (auto& S : slabs) {
+    CK(cudaMemsetAsync(S.vec.p, 0, S.vec.cap, c->stream));
+    launch_setup<TX, TV>(S.list.as<int>(), S.P.n_owned, static_cast<int>(S.ld), r, c->beta64.as<double>(),
+                         ridge, R(S), D(S), c->stream);
+  }
+  PcgState hs{};
+  hs.tol = opt.tol;
+  hs.ridge = ridge;
+  hs.max_iter = opt.max_iter > 0 ? opt.max_iter : 20 * r + 2000;
+  std::memcpy(c->hstate, &hs, sizeof(hs));
+  CK(cudaMemcpyAsync(c->state.p, c->hstate, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaEventRecord(c->ev[4], c->stream));
+  PcgState* dst = c->state.as<PcgState>();
+  const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
+                                         : reinterpret_cast<const TV*>(c->beta32.p);
+  double* totals = tot.as<double>();
+
+  // cross-slab sum: in-process slabs are summed by the finalize kernel; ranks
+  // all-reduce their one total first
+  auto reduce = [&](int k) {
+    if (dist) NK(nccl().AllReduce(totals, totals, k, ncclFloat64, ncclSum, comm->comm, c->stream));
+  };
+  // ghost exchange of an 18-component vector (z each iteration, x for C^H)
+  auto exchange = [&](auto vec_of) {
+    using T = std::remove_pointer_t<decltype(vec_of(slabs[0]))>;
+    T* buf = xfer.as<T>();
+    if (!dist) {
+      for (int s = 0; s < nloc; ++s) {
+        Slab& me = slabs[s];
+        Slab& lo = slabs[(s - 1 + nloc) % nloc];
+        Slab& hi = slabs[(s + 1) % nloc];
+        launch_pack<T>(vec_of(lo), lo.P.n_owned - lo.P.cnt_last, lo.P.cnt_last, buf, c->stream);
+        launch_unpack<T>(vec_of(me), me.P.n_owned, me.P.n_glo, buf, c->stream);
+        launch_pack<T>(vec_of(hi), 0, hi.P.cnt_first, buf, c->stream);
+        launch_unpack<T>(vec_of(me), me.P.n_owned + me.P.n_glo, me.P.n_ghi, buf, c->stream);
+      }
+      return;
+    }
+    Slab& me = slabs[0];
+    const int lo = (comm->rank - 1 + comm->nranks) % comm->nranks, hi = (comm->rank + 1) % comm->nranks;
+    const size_t stride = 18 * static_cast<size_t>(std::max(max_plane, 1));
+    T *send_hi = buf, *send_lo = buf + stride, *recv_lo = buf + 2 * stride, *recv_hi = buf + 3 * stride;
+    const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+    launch_pack<T>(vec_of(me), me.P.n_owned - me.P.cnt_last, me.P.cnt_last, send_hi, c->stream);
+    launch_pack<T>(vec_of(me), 0, me.P.cnt_first, send_lo, c->stream);
+    NK(nccl().GroupStart());
+    NK(nccl().Send(send_hi, 18 * static_cast<size_t>(me.P.cnt_last), dt, hi, comm->comm, c->stream));
+    NK(nccl().Send(send_lo, 18 * static_cast<size_t>(me.P.cnt_first), dt, lo, comm->comm, c->stream));
+    NK(nccl().Recv(recv_lo, 18 * static_cast<size_t>(me.P.n_glo), dt, lo, comm->comm, c->stream));
+    NK(nccl().Recv(recv_hi, 18 * static_cast<size_t>(me.P.n_ghi), dt, hi, comm->comm, c->stream));
+    NK(nccl().GroupEnd());
+    launch_unpack<T>(vec_of(me), me.P.n_owned, me.P.n_glo, recv_lo, c->stream);
+    launch_unpack<T>(vec_of(me), me.P.n_owned + me.P.n_glo, me.P.n_ghi, recv_hi, c->stream);
+  };
+  auto grid_u = [&](const Slab& S) { return 6 * std::max(1, std::min((S.P.n_owned + 255) / 256, c->num_sms * 2)); };
+  auto grid_a = [&](const Slab& S) {
+    return std::max(1, std::min((S.P.n_owned + 255) / 256, c->num_sms * (sizeof(TV) == 4 ? 3 : 2)));
+  };
+  auto update_all = [&](int init) {
+    for (int s = 0; s < nloc; ++s) {
+      Slab& S = slabs[s];
+      UpdateArgs<TX, TV> ua{X(S), R(S), Pv(S), Q(S), Z(S), D(S), S.partials.as<double>(), dst,
+                            S.P.n_owned, static_cast<int>(S.ld), init, totals + 12 * s, 1};
+      launch_update<TX, TV>(ua, grid_u(S), c->stream);
+    }
+    reduce(12);
+    launch_finalize_update(dst, totals, nloc, init, c->stream);
+  };
+  auto apply_all = [&]() {
+    exchange([&](Slab& S) { return Z(S); });
+    for (int s = 0; s < nloc; ++s) {
+      Slab& S = slabs[s];
+      ApplyArgs<TV> aa{S.list.as<int>(), S.map.as<int>(), beta_apply, Z(S), Pv(S), Q(S),
+                       S.partials.as<double>(), dst, r, S.P.n_owned, static_cast<int>(S.ld),
+                       S.P.n_local, S.P.zbase, S.P.nzl, totals + 6 * s, 1};
+      launch_apply<TV>(aa, grid_a(S), c->stream);
+    }
+    reduce(6);
+    launch_finalize_apply(dst, totals, nloc, c->stream);
+  };
+
+  update_all(1);
+  apply_all();
+  const int check = opt.check_every > 0 ? opt.check_every : 16;
+  int64_t launches = 0;
+  for (;;) {
+    for (int it = 0; it < check; ++it) {
+      update_all(0);
+      apply_all();
+      launches += 2 * nloc + 2 + 8 * nloc;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->hstate, c->state.p, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (c->hstate->stop) break;
+  }
+  CK(cudaEventRecord(c->ev[5], c->stream));
+  const PcgState& fin = *c->hstate;
+  if (fin.error) throw ShlError(SHL_SOLVER, "grid CG: operator lost positive definiteness");
+  if (!fin.all_done) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "grid CG did not reach tolerance %g in %d iterations", opt.tol,
+                  fin.max_iter);
+    throw ShlError(SHL_SOLVER, buf);
+  }
+  // C^H: owned elements need x on the ghost-hi plane
+  exchange([&](Slab& S) { return X(S); });
+  for (int s = 0; s < nloc; ++s) {
+    Slab& S = slabs[s];
+    const int ne = S.P.e_hi - S.P.e_lo;
+    const int grid_c = std::max(1, std::min((ne + 31) / 32, c->num_sms * 16));
+    ChomArgs<TX> ca{c->elem_list.as<int>() + S.P.e_lo, S.map.as<int>(), c->beta64.as<double>(), X(S),
+                    S.partials.as<double>(), totals + 21 * s, dst, ne, r, static_cast<int>(S.ld),
+                    S.P.zbase, S.P.nzl, 1};
+    if (ne > 0)
+      launch_chom<TX>(ca, grid_c, c->stream);
+    else
+      CK(cudaMemsetAsync(totals + 21 * s, 0, 21 * sizeof(double), c->stream));
+  }
+  reduce(21);
+  launch_finalize_chom(totals, nloc, c->cout.as<double>(), c->stream);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->hC, c->cout.p, 36 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaEventRecord(c->ev[6], c->stream));
+  c->sync();
+  std::memcpy(C_out, c->hC, 36 * sizeof(double));
+  c->launches += launches;
+  if (st) {
+    st->t_AS = c->ms(3, 4);
+    st->t_solve = c->ms(4, 5);
+    st->t_C = c->ms(5, 6);
+    for (int s = 0; s < 6; ++s) st->iterations[s] = fin.iters[s];
+    st->converged = 1;
+    st->precision = prec;
+  }
+}
+
+void homogenize_slabs(shl_ctx* c, int G, NcclComm* comm, const shl_design* design,
+                      const shl_shell_params* sp, const shl_material* mat, int r,
+                      const shl_solve_options* o, double* C_out, shl_stats* st) {
+  if (!C_out) throw ShlError(SHL_VALIDATION, "null argument");
+  const shl_solve_options opt = default_opts(o);
+  double K0[576];
+  validate_inputs(design, sp, mat, r, K0);
+  FieldInputs fin = tagged("field", [&] { return prepare_field(HostDesign::from_abi(*design), r); });
+  CK(cudaEventRecord(c->ev[0], c->stream));
+  tagged("field", [&] {
+    run_field(c, fin);
+    return 0;
+  });
+  CK(cudaEventRecord(c->ev[1], c->stream));
+  read_norm(c);
+  if (c->norm == 0.0) throw ShlError(SHL_DEGENERATE, "field: design is degenerate (norm = 0)");
+  tagged("mesh", [&] {
+    run_mesh(c, *sp);
+    return 0;
+  });
+  CK(cudaEventRecord(c->ev[2], c->stream));
+  const int prec = resolve_precision(opt);
+  tagged("solve", [&] {
+    switch (prec) {
+      case SHL_PREC_FP64: run_solve_slabs<double, double>(c, K0, opt, C_out, st, prec, G, comm); break;
+      case SHL_PREC_MIXED: run_solve_slabs<double, float>(c, K0, opt, C_out, st, prec, G, comm); break;
+      default: run_solve_slabs<float, float>(c, K0, opt, C_out, st, prec, G, comm); break;
+    }
+    return 0;
+  });
+  if (st) {
+    st->t_field = c->ms(0, 1);
+    st->t_mesh = c->ms(1, 2);
+    st->t_fwd = c->ms(0, 6);
+    fill_mesh_stats(c, st);
+  }
+}
+
+}  // namespace host
+}  // namespace shl
+
+using namespace shl::host;
+
+extern "C" {
+
+int shl_homogenize_slabs(shl_ctx* c, int n_slabs, const shl_design* design,
+                         const shl_shell_params* sp, const shl_material* mat, int r,
+                         const shl_solve_options* opt, double* C_out, shl_stats* st) {
+  if (!c) return SHL_VALIDATION;
+  if (st) std::memset(st, 0, sizeof(*st));
+  return guarded(c, [&] { homogenize_slabs(c, n_slabs, nullptr, design, sp, mat, r, opt, C_out, st); });
+}
+
+int shl_nccl_unique_id(uint8_t* id_out) {
+  if (!id_out) return SHL_VALIDATION;
+  return guarded(nullptr, [&] {
+    ncclUniqueId id;
+    NK(nccl().GetUniqueId(&id));
+    std::memcpy(id_out, &id, NCCL_UNIQUE_ID_BYTES);
+  });
+}
+
+int shl_homogenize_zslab(shl_ctx* c, const uint8_t* nccl_id, int rank, int nranks,
+                         const shl_design* design, const shl_shell_params* sp,
+                         const shl_material* mat, int r, const shl_solve_options* opt,
+                         double* C_out, shl_stats* st) {
+  if (!c || !nccl_id || nranks < 2 || rank < 0 || rank >= nranks) return SHL_VALIDATION;
+  if (st) std::memset(st, 0, sizeof(*st));
+  return guarded(c, [&] {
+    auto* comm = static_cast<NcclComm*>(c->nccl);
+    if (!comm || comm->rank != rank || comm->nranks != nranks ||
+        std::memcmp(comm->id, nccl_id, NCCL_UNIQUE_ID_BYTES) != 0) {
+      delete comm;
+      c->nccl = nullptr;
+      comm = new NcclComm();
+      std::memcpy(comm->id, nccl_id, NCCL_UNIQUE_ID_BYTES);
+      comm->rank = rank;
+      comm->nranks = nranks;
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, NCCL_UNIQUE_ID_BYTES);
+      NK(nccl().CommInitRank(&comm->comm, nranks, id, rank));
+      c->nccl = comm;
+      c->nccl_deleter = [](void* p) { delete static_cast<NcclComm*>(p); };
+    }
+    homogenize_slabs(c, nranks, comm, design, sp, mat, r, opt, C_out, st);
+  });
+}
+
+}  // extern "C"

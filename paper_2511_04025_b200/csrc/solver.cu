@@ -120,6 +120,52 @@ __device__ __forceinline__ void reduce_partials(const double* partials, double (
   block_sum<NV>(out, scratch);
 }
 
+// ---- scalar updates (shared by the last block and the cross-slab finalize) --
+__device__ void finalize_apply_state(PcgState* st, const double (&tot)[6]) {
+  for (int s = 0; s < 6; ++s) {
+    st->delta[s] = tot[s];
+    if (st->done[s]) {
+      st->alpha[s] = 0.0;
+      continue;
+    }
+    // p.Ap = delta - beta * gamma / alpha_old  (= delta on the first step)
+    const double den = st->beta[s] == 0.0 ? tot[s] : tot[s] - st->beta[s] * st->gamma[s] / st->alpha[s];
+    if (!(den > 0.0)) st->error = 1;
+    st->pap[s] = den;
+    st->alpha[s] = st->gamma[s] / den;
+  }
+  if (st->error) st->stop = 1;
+}
+
+__device__ void finalize_update_state(PcgState* st, const double (&tot)[12], int init) {
+  bool all = true;
+  for (int t = 0; t < 6; ++t) {
+    st->rr[t] = tot[t];
+    const double rn = sqrt(tot[t]);
+    if (init) {
+      st->bnorm[t] = rn;
+      st->gamma[t] = tot[6 + t];
+      st->done[t] = rn == 0.0;
+      st->beta[t] = 0.0;
+      st->alpha[t] = 0.0;
+      st->iters[t] = 0;
+    } else if (!st->done[t]) {
+      st->iters[t] = st->it + 1;           // grid_solver.hpp:67
+      if (rn <= st->tol * st->bnorm[t]) {  // grid_solver.hpp:68-72
+        st->done[t] = 1;
+        st->beta[t] = 0.0;
+      } else {
+        st->beta[t] = tot[6 + t] / st->gamma[t];
+        st->gamma[t] = tot[6 + t];
+      }
+    }
+    all = all && st->done[t];
+  }
+  if (!init) st->it += 1;
+  st->all_done = all;
+  st->stop = all || st->error || st->it >= st->max_iter;
+}
+
 // ---- K3 + preconditioner setup -------------------------------------------
 // One thread per active node: block-Jacobi inverse (grid_solver.hpp:129-139)
 // and the strain right-hand sides (grid_solver.hpp:141-152), node 0 pinned.
@@ -272,7 +318,17 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
     const int i = g % r, j = (g / r) % r, k = g / rr;
     const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
     const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
-    const int zs[3] = {(k == 0 ? r - 1 : k - 1) * rr, k * rr, (k == r - 1 ? 0 : k + 1) * rr};
+    const int kz[3] = {k == 0 ? r - 1 : k - 1, k, k == r - 1 ? 0 : k + 1};
+    // beta is global (every rank holds the full mask); the node map covers
+    // local planes [zbase, zbase + nzl) (the whole torus when not slabbed)
+    const int zs[3] = {kz[0] * rr, kz[1] * rr, kz[2] * rr};
+    int zl[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      int lz = kz[d] - A.zbase;
+      lz += lz < 0 ? r : 0;
+      zl[d] = lz * rr;
+    }
     TV be[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -285,8 +341,8 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
 #pragma unroll
       for (int m = 0; m < 27; ++m) {
         const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-        int nb = (m == 13) ? idx : nmap[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
-        nb = nb < 0 ? A.n : nb;
+        int nb = (m == 13) ? idx : nmap[zl[dz + 1] + ys[dy + 1] + xs[dx + 1]];
+        nb = nb < 0 ? A.zero_slot : nb;
         TV S[9];
 #pragma unroll
         for (int q = 0; q < 9; ++q) S[q] = TV(0);
@@ -328,19 +384,11 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
     __syncthreads();
     reduce_partials<6>(A.partials, tot, scratch);
     if (threadIdx.x == 0) {
-      for (int s = 0; s < 6; ++s) {
-        st->delta[s] = tot[s];
-        if (st->done[s]) {
-          st->alpha[s] = 0.0;
-          continue;
-        }
-        // p.Ap = delta - beta * gamma / alpha_old  (= delta on the first step)
-        const double den = st->beta[s] == 0.0 ? tot[s] : tot[s] - st->beta[s] * st->gamma[s] / st->alpha[s];
-        if (!(den > 0.0)) st->error = 1;
-        st->pap[s] = den;
-        st->alpha[s] = st->gamma[s] / den;
+      if (A.defer) {
+        for (int s = 0; s < 6; ++s) A.totals[s] = tot[s];
+      } else {
+        finalize_apply_state(st, tot);
       }
-      if (st->error) st->stop = 1;
       st->counter_apply = 0;
     }
   }
@@ -426,32 +474,11 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
     __shared__ double scratch12[32 * 12];
     block_sum<12>(tot, scratch12);
     if (threadIdx.x == 0) {
-      bool all = true;
-      for (int t = 0; t < 6; ++t) {
-        st->rr[t] = tot[t];
-        const double rn = sqrt(tot[t]);
-        if (U.init) {
-          st->bnorm[t] = rn;
-          st->gamma[t] = tot[6 + t];
-          st->done[t] = rn == 0.0;
-          st->beta[t] = 0.0;
-          st->alpha[t] = 0.0;
-          st->iters[t] = 0;
-        } else if (!st->done[t]) {
-          st->iters[t] = st->it + 1;  // grid_solver.hpp:67
-          if (rn <= st->tol * st->bnorm[t]) {  // grid_solver.hpp:68-72
-            st->done[t] = 1;
-            st->beta[t] = 0.0;
-          } else {
-            st->beta[t] = tot[6 + t] / st->gamma[t];
-            st->gamma[t] = tot[6 + t];
-          }
-        }
-        all = all && st->done[t];
+      if (U.defer) {
+        for (int q = 0; q < 12; ++q) U.totals[q] = tot[q];
+      } else {
+        finalize_update_state(st, tot, U.init);
       }
-      if (!U.init) st->it += 1;
-      st->all_done = all;
-      st->stop = all || st->error || st->it >= st->max_iter;
       st->counter_update = 0;
     }
   }
@@ -478,8 +505,9 @@ __global__ void __launch_bounds__(32) chom_kernel(const ChomArgs<TX> Cg) {
     for (int n = 0; n < 8; ++n) {
       const int gx = (i + (n == 1 || n == 2 || n == 5 || n == 6)) % r;
       const int gy = (j + (n == 2 || n == 3 || n == 6 || n == 7)) % r;
-      const int gz = (k + (n >= 4)) % r;
-      const int idx = Cg.node_map[(static_cast<size_t>(gz) * r + gy) * r + gx];
+      int lz = (k + (n >= 4)) % r - Cg.zbase;
+      lz += lz < 0 ? r : 0;
+      const int idx = Cg.node_map[(static_cast<size_t>(lz) * r + gy) * r + gx];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -516,17 +544,92 @@ __global__ void __launch_bounds__(32) chom_kernel(const ChomArgs<TX> Cg) {
     __syncthreads();
     reduce_partials<21>(Cg.partials, tot, scratch);
     if (threadIdx.x == 0) {
-      for (int b = 0; b < 6; ++b)
-        for (int a = 0; a <= b; ++a) {
-          Cg.C_out[a * 6 + b] = tot[b * (b + 1) / 2 + a];
-          Cg.C_out[b * 6 + a] = tot[b * (b + 1) / 2 + a];
-        }
+      if (Cg.defer) {
+        for (int q = 0; q < 21; ++q) Cg.C_out[q] = tot[q];
+      } else {
+        for (int b = 0; b < 6; ++b)
+          for (int a = 0; a <= b; ++a) {
+            Cg.C_out[a * 6 + b] = tot[b * (b + 1) / 2 + a];
+            Cg.C_out[b * 6 + a] = tot[b * (b + 1) / 2 + a];
+          }
+      }
       st->counter_misc = 0;
     }
   }
 }
 
+// ---- cross-slab finalize + ghost-plane transport ---------------------------
+__global__ void finalize_update_kernel(PcgState* st, const double* totals, int nslab, int init) {
+  double tot[12];
+  for (int q = 0; q < 12; ++q) {
+    double s = 0.0;
+    for (int b = 0; b < nslab; ++b) s += totals[b * 12 + q];
+    tot[q] = s;
+  }
+  if (st->stop && !init) return;
+  finalize_update_state(st, tot, init);
+}
+
+__global__ void finalize_apply_kernel(PcgState* st, const double* totals, int nslab) {
+  if (st->stop) return;
+  double tot[6];
+  for (int q = 0; q < 6; ++q) {
+    double s = 0.0;
+    for (int b = 0; b < nslab; ++b) s += totals[b * 6 + q];
+    tot[q] = s;
+  }
+  finalize_apply_state(st, tot);
+}
+
+__global__ void finalize_chom_kernel(const double* totals, int nslab, double* C) {
+  for (int b = 0; b < 6; ++b)
+    for (int a = 0; a <= b; ++a) {
+      double s = 0.0;
+      for (int q = 0; q < nslab; ++q) s += totals[q * 21 + b * (b + 1) / 2 + a];
+      C[a * 6 + b] = s;
+      C[b * 6 + a] = s;
+    }
+}
+
+template <typename T>
+__global__ void pack_kernel(const T* __restrict__ vec, int first, int count, T* __restrict__ buf) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * 18) return;
+  const int q = t / count, i = t % count;
+  buf[t] = vec[vbase(first + i, 18) + q * 32];
+}
+
+template <typename T>
+__global__ void unpack_kernel(T* __restrict__ vec, int first, int count, const T* __restrict__ buf) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * 18) return;
+  const int q = t / count, i = t % count;
+  vec[vbase(first + i, 18) + q * 32] = buf[t];
+}
+
 }  // namespace
+
+void launch_finalize_update(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s) {
+  finalize_update_kernel<<<1, 1, 0, s>>>(st, totals, nslab, init);
+}
+void launch_finalize_apply(PcgState* st, const double* totals, int nslab, cudaStream_t s) {
+  finalize_apply_kernel<<<1, 1, 0, s>>>(st, totals, nslab);
+}
+void launch_finalize_chom(const double* totals, int nslab, double* C_out, cudaStream_t s) {
+  finalize_chom_kernel<<<1, 1, 0, s>>>(totals, nslab, C_out);
+}
+template <typename T>
+void launch_pack(const T* vec, int first, int count, T* buf, cudaStream_t s) {
+  if (count > 0) pack_kernel<T><<<(count * 18 + 255) / 256, 256, 0, s>>>(vec, first, count, buf);
+}
+template <typename T>
+void launch_unpack(T* vec, int first, int count, const T* buf, cudaStream_t s) {
+  if (count > 0) unpack_kernel<T><<<(count * 18 + 255) / 256, 256, 0, s>>>(vec, first, count, buf);
+}
+template void launch_pack<float>(const float*, int, int, float*, cudaStream_t);
+template void launch_pack<double>(const double*, int, int, double*, cudaStream_t);
+template void launch_unpack<float>(float*, int, int, const float*, cudaStream_t);
+template void launch_unpack<double>(double*, int, int, const double*, cudaStream_t);
 
 // ---- host-side launchers -----------------------------------------------------
 void upload_element_constants(const double* K0, const double* W, const double* T,

@@ -21,8 +21,13 @@ struct ApplyArgs {
   double* partials;
   PcgState* state;
   int r;
-  int n;
+  int n;          // nodes this launch owns (iterated)
   int ld;
+  int zero_slot;  // local id of the always-zero row (= owned + ghost nodes)
+  int zbase;      // global z of local node-map plane 0 (0 when not slabbed)
+  int nzl;        // node-map planes (r when not slabbed)
+  double* totals; // defer != 0: write the 6 reduced sums here, leave state alone
+  int defer;
 };
 
 template <typename TX, typename TV>
@@ -38,6 +43,8 @@ struct UpdateArgs {
   int n;
   int ld;
   int init;
+  double* totals;  // defer != 0: write the 12 reduced sums here, leave state alone
+  int defer;
 };
 
 template <typename TX>
@@ -47,12 +54,28 @@ struct ChomArgs {
   const double* beta64;
   const TX* x;
   double* partials;
-  double* C_out;
+  double* C_out;  // defer == 0: symmetric 6x6; defer != 0: 21 raw sums
   PcgState* state;
   int n_elem;
   int r;
   int ld;
+  int zbase;
+  int nzl;
+  int defer;
 };
+
+// Cross-slab reduction: sum `nslab` deferred totals in slab order and update
+// the PcgState (emulated slabs on one device, or after an NCCL all-reduce
+// with nslab = 1).
+void launch_finalize_update(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s);
+void launch_finalize_apply(PcgState* st, const double* totals, int nslab, cudaStream_t s);
+void launch_finalize_chom(const double* totals, int nslab, double* C_out, cudaStream_t s);
+// Ghost-plane transport: nodes [first, first+count) of an 18-component
+// blocked vector <-> dense [18][count] buffer.
+template <typename T>
+void launch_pack(const T* vec, int first, int count, T* buf, cudaStream_t s);
+template <typename T>
+void launch_unpack(T* vec, int first, int count, const T* buf, cudaStream_t s);
 
 void upload_element_constants(const double* K0, const double* W, const double* T, cudaStream_t s);
 template <typename TX, typename TV>

@@ -227,3 +227,23 @@ def test_batch_matches_single(S):
     for i, d in enumerate(designs):
         Cs = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), 16, opt).tensor
         assert np.array_equal(Cs, Cb[i])  # deterministic reductions
+
+
+@pytest.mark.parametrize("r,G,prec,tol", [(16, 2, "fp64", 1e-10), (32, 3, "mixed", 1e-6),
+                                          (32, 4, "fp32", 1e-5), (64, 8, "mixed", 1e-5)])
+def test_zslab_matches_single_device(S, r, G, prec, tol):
+    """Config C5 code path (emulated slabs): same C^H and iteration counts as the
+    undecomposed solve; only the cross-slab summation order differs."""
+    d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), 3)
+    opt = S.HomogenizeOptions(residual_tol=tol, precision=prec)
+    ref = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, opt)
+    got = S.homogenize_slabs(d, S.ShellParams(), S.BaseMaterial(), r, G, opt)
+    assert rel_fro(got.tensor, ref.tensor) < (1e-10 if prec == "fp64" else 1e-6)
+    assert np.abs(got.iterations - ref.iterations).max() <= 2
+    assert got.stats.n_nodes == ref.stats.n_nodes
+
+
+def test_zslab_validation(S):
+    d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), 3)
+    with pytest.raises(S.ValidationError):
+        S.homogenize_slabs(d, S.ShellParams(), S.BaseMaterial(), 16, 9)
