@@ -104,7 +104,8 @@ struct DeviceSolveOptions {
   double tol = 1e-9;
   int max_iter = 0;
   int precision = SHL_PREC_AUTO;
-  shl_solve_options abi() const { return {tol, max_iter, precision, 0, 0}; }
+  int preconditioner = SHL_PRECOND_JACOBI;
+  shl_solve_options abi() const { return {tol, max_iter, precision, 0, preconditioner}; }
 };
 
 // build_periodic_system + solve_test_strains + effective_tensor for `mesh`

@@ -32,8 +32,9 @@ class GridSolver {
   };
 
   // precision: SHL_PREC_AUTO (FP64 below tol 1e-7), _FP64, _MIXED or _FP32
-  Result solve(double tol = 1e-9, int max_iter = 0, int precision = SHL_PREC_AUTO) {
-    const shl_solve_options o{tol, max_iter, precision, 0, 0};
+  Result solve(double tol = 1e-9, int max_iter = 0, int precision = SHL_PREC_AUTO,
+               int preconditioner = SHL_PRECOND_JACOBI) {
+    const shl_solve_options o{tol, max_iter, precision, 0, preconditioner};
     double C[36];
     Result res;
     shl_ctx* ctx = detail::context();

@@ -24,6 +24,7 @@ struct HomogenizeOptions {
   int corner_gauge = 0;                 // any gauge gives the same tensor
   int precision = SHL_PREC_AUTO;        // device arithmetic (shellular_cuda.h)
   int max_iter = 0;
+  int preconditioner = SHL_PRECOND_JACOBI;  // or SHL_PRECOND_GMG (multigrid V-cycle)
   bool return_fields = false;           // copy the grid + element list back
 };
 
@@ -56,7 +57,7 @@ inline HomogenizationResult homogenize(const DesignParams& params, const ShellPa
   auto a = params.abi();
   const shl_shell_params spa = sp.abi();
   const shl_material ma = mat.abi();
-  const shl_solve_options o{opt.residual_tol, opt.max_iter, opt.precision, 0, 0};
+  const shl_solve_options o{opt.residual_tol, opt.max_iter, opt.precision, 0, opt.preconditioner};
   HomogenizationResult res;
   double C[36];
   shl_ctx* ctx = detail::context();

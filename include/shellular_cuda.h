@@ -80,12 +80,18 @@ typedef struct {
   double poisson; /* 0.3 */
 } shl_material;
 
+/* PCG preconditioner */
+enum {
+  SHL_PRECOND_JACOBI = 0, /* 3x3 block Jacobi (grid_solver.hpp:129-139) */
+  SHL_PRECOND_GMG = 1     /* Galerkin geometric multigrid V-cycle (new) */
+};
+
 typedef struct {
-  double tol;      /* per-column ||r|| <= tol*||b|| (grid_solver.hpp:68) */
-  int max_iter;    /* 0 = 20r+2000 (grid_solver.hpp:38) */
-  int precision;   /* SHL_PREC_* */
-  int check_every; /* host convergence poll period in iterations (0 = auto) */
-  int reserved;
+  double tol;         /* per-column ||r|| <= tol*||b|| (grid_solver.hpp:68) */
+  int max_iter;       /* 0 = 20r+2000 (grid_solver.hpp:38) */
+  int precision;      /* SHL_PREC_* */
+  int check_every;    /* host convergence poll period in iterations (0 = auto) */
+  int preconditioner; /* SHL_PRECOND_* */
 } shl_solve_options;
 
 /* StageTimings (common.hpp:145-160) + solver / mesh statistics */
@@ -102,12 +108,14 @@ typedef struct {
   int64_t n_tiles;    /* active apply tiles */
   double norm;        /* max |centre sample| */
   double volume_ratio;
-  double apply_ms; /* summed device time of the K.u apply launches (0 unless profiled) */
-  double update_ms;
+  double apply_ms;  /* summed device time of the K.u apply launches (0 unless profiled) */
+  double update_ms; /* update kernel + (GMG) V-cycle, same accounting */
   int64_t apply_launches;
   int64_t kernel_launches; /* kernels launched by this call */
   int64_t h2d_bytes;       /* host->device bytes moved by this call */
   int64_t d2h_bytes;       /* device->host bytes moved by this call */
+  int32_t gmg_levels;      /* multigrid levels incl. the fine one (0 = block Jacobi) */
+  int32_t reserved1;
 } shl_stats;
 
 int shl_ctx_create(int device, shl_ctx** out);

@@ -13,6 +13,7 @@ LIB_PATH = os.environ.get("SHL_LIB") or os.path.join(HERE, "libshellular_cuda.so
 
 SHL_OK, SHL_VALIDATION, SHL_DEGENERATE, SHL_SOLVER, SHL_IO, SHL_CUDA = range(6)
 PREC_AUTO, PREC_FP64, PREC_MIXED, PREC_FP32 = -1, 0, 1, 2
+PRECOND_JACOBI, PRECOND_GMG = 0, 1
 
 
 class shl_design(C.Structure):
@@ -32,7 +33,7 @@ class shl_material(C.Structure):
 
 class shl_solve_options(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("precision", C.c_int),
-                ("check_every", C.c_int), ("reserved", C.c_int)]
+                ("check_every", C.c_int), ("preconditioner", C.c_int)]
 
 
 class shl_stats(C.Structure):
@@ -45,7 +46,8 @@ class shl_stats(C.Structure):
                 ("n_tiles", C.c_int64), ("norm", C.c_double), ("volume_ratio", C.c_double),
                 ("apply_ms", C.c_double), ("update_ms", C.c_double),
                 ("apply_launches", C.c_int64), ("kernel_launches", C.c_int64),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("gmg_levels", C.c_int32), ("reserved1", C.c_int32)]
 
 
 # every symbol include/shellular_cuda.h declares (checked by tests/test_abi.py)

@@ -317,6 +317,7 @@ def isotropic_tensor(mat: BaseMaterial) -> np.ndarray:
 PRECISION = {"auto": L.PREC_AUTO, "fp64": L.PREC_FP64, "mixed": L.PREC_MIXED,
              "fp32": L.PREC_FP32}
 PRECISION_NAME = {v: k for k, v in PRECISION.items()}
+PRECONDITIONER = {"jacobi": L.PRECOND_JACOBI, "gmg": L.PRECOND_GMG}
 
 
 @dataclass
@@ -326,10 +327,12 @@ class HomogenizeOptions:
     max_iter: int = 0
     precision: str = "auto"
     check_every: int = 0
+    preconditioner: str = "jacobi"  # "jacobi" (grid_solver.hpp block Jacobi) | "gmg"
 
     def _abi(self):
         return L.shl_solve_options(float(self.residual_tol), int(self.max_iter),
-                                   PRECISION[self.precision], int(self.check_every), 0)
+                                   PRECISION[self.precision], int(self.check_every),
+                                   PRECONDITIONER[self.preconditioner])
 
 
 TIMING_KEYS = ("t_field", "t_mesh", "t_PBC", "t_AS", "t_RHS", "t_solve", "t_C", "t_fwd")
@@ -354,6 +357,7 @@ class SolveStats:
     kernel_launches: int
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    gmg_levels: int = 0
 
     @classmethod
     def from_abi(cls, s: L.shl_stats) -> "SolveStats":
@@ -361,7 +365,7 @@ class SolveStats:
                    bool(s.converged), PRECISION_NAME.get(s.precision, "?"), s.n_surface,
                    s.n_elements, s.n_nodes, s.n_tiles, s.norm, s.volume_ratio,
                    bool(s.full_fallback), s.apply_ms, s.update_ms, s.apply_launches,
-                   s.kernel_launches, s.h2d_bytes, s.d2h_bytes)
+                   s.kernel_launches, s.h2d_bytes, s.d2h_bytes, s.gmg_levels)
 
 
 class GridSolver:
@@ -377,7 +381,7 @@ class GridSolver:
         stats: SolveStats
 
     def __init__(self, beta: np.ndarray, r: int, K0: np.ndarray, ctx: Context | None = None,
-                 precision: str = "auto"):
+                 precision: str = "auto", preconditioner: str = "jacobi"):
         beta = np.ascontiguousarray(beta, np.float64).reshape(-1)
         if beta.size != r ** 3:
             raise ValidationError("beta array does not match resolution")
@@ -385,9 +389,10 @@ class GridSolver:
         self.K0 = np.ascontiguousarray(K0, np.float64).reshape(-1)
         self.ctx = ctx or default_context()
         self.precision = precision
+        self.preconditioner = preconditioner
 
     def solve(self, tol: float = 1e-9, max_iter: int = 0) -> "GridSolver.Result":
-        opt = HomogenizeOptions(tol, max_iter, self.precision)._abi()
+        opt = HomogenizeOptions(tol, max_iter, self.precision, 0, self.preconditioner)._abi()
         Cm = np.zeros(36)
         st = L.shl_stats()
         _check(L.lib().shl_grid_solve(self.ctx.handle, self.r, self.beta.ctypes.data,

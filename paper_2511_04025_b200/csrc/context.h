@@ -93,6 +93,13 @@ struct shl_ctx {
   double volume_ratio = 0.0, beta_sum = 0.0;
   // solver
   DevBuf vec, partials, state, cout;
+  // multigrid hierarchy (levels >= 1; level 0 aliases the solver's buffers)
+  struct GmgLevel {
+    int r = 0, n = 0, ld = 0;
+    DevBuf flag, off, map, list, stencil, dinv, vec, scan_tmp;
+  };
+  std::vector<GmgLevel> gmg;
+  DevBuf gmg0;  // level-0 V-cycle work vectors (xa, xb, res)
   Misc* hmisc = nullptr;
   shl::PcgState* hstate = nullptr;
   double* hC = nullptr;

@@ -1,0 +1,421 @@
+// gmg.cuh -- geometric multigrid preconditioner kernels (included by solver.cu,
+// which owns the __constant__ element matrices).
+//
+// Hierarchy on the periodic torus: level 0 is the matrix-free masked operator
+// (fine_gather); level l+1 has r/2^(l+1) nodes per axis and the Galerkin
+// operator A_{l+1} = P^T A_l P for trilinear interpolation P (weights 1, 1/2
+// per axis, periodic), restricted to coarse nodes whose support touches an
+// active fine node.  Coarse operators are stored as 27-point stencils of 3x3
+// blocks (243 values per node, 32-node blocked like every vector).  Galerkin
+// coarsening keeps the masked, 1e3-contrast shell operator faithful on every
+// level (no re-discretization of void/floor voxels).  The pinned node 0 is a
+// zero row/column on every level.  Smoother: damped 3x3 block Jacobi.
+//
+// All vectors carry the six load cases x three components (18 per node).
+
+namespace {
+
+constexpr int kStencil = 243;
+
+// ---------------------------------------------------------------- gathers
+template <typename TV>
+__device__ __forceinline__ void stencil_gather(GatherAcc<TV>& acc, int idx, int g,
+                                               const TV* __restrict__ xv,
+                                               const TV* __restrict__ stencil,
+                                               const int* __restrict__ nmap, int r, int zero_slot) {
+  acc.zero();
+  if (g == 0) return;
+  const int rr = r * r;
+  const int i = g % r, j = (g / r) % r, k = g / rr;
+  const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
+  const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
+  const int zs[3] = {(k == 0 ? r - 1 : k - 1) * rr, k * rr, (k == r - 1 ? 0 : k + 1) * rr};
+  const TV* sb = stencil + vbase(idx, kStencil);
+#pragma unroll 1
+  for (int m = 0; m < 27; ++m) {
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+    int nb = (m == 13) ? idx : nmap[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
+    nb = nb < 0 ? zero_slot : nb;
+    TV S[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) S[q] = sb[(m * 9 + q) * 32];
+    acc.add(S, xv + vbase(nb, 18));
+  }
+}
+
+template <typename TV>
+struct LevelArgs {
+  const int* node_list;
+  const int* node_map;
+  const TV* beta;     // level 0 only (dense r^3)
+  const TV* stencil;  // levels >= 1
+  const TV* dinv;     // 6 per node
+  int r, n, zero_slot;
+  TV ridge;           // level 0 only
+};
+
+// mode: 0 smooth   xout = xin + w Dinv (b - A xin)
+//       1 residual xout = b - A xin
+//       2 smooth + partial b.xout (the V-cycle output z = M r, gamma = r.z)
+template <typename TB, typename TV, bool kFine>
+__global__ void __launch_bounds__(256, 3)
+    level_sweep_kernel(const LevelArgs<TV> L, const TB* __restrict__ b, const TV* __restrict__ xin,
+                       TV* __restrict__ xout, TV omega, int mode, PcgState* st,
+                       double* partials, int init) {
+  __shared__ double scratch[32 * 6];
+  if (st->stop) return;
+  double gam[6] = {0, 0, 0, 0, 0, 0};
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < L.n; idx += gridDim.x * blockDim.x) {
+    const int g = L.node_list[idx];
+    GatherAcc<TV> acc;
+    if (kFine)
+      fine_gather<TV>(acc, idx, g, xin, L.beta, L.node_map, L.r, 0, L.zero_slot);
+    else
+      stencil_gather<TV>(acc, idx, g, xin, L.stencil, L.node_map, L.r, L.zero_slot);
+    const size_t ob = vbase(idx, 18);
+    TV D[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      TV res[3], xo[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const size_t o = ob + (c * 6 + s) * 32;
+        const TV xi = xin[o];
+        TV w = acc.get(c * 6 + s);
+        if (kFine && g != 0) w = fma_t(L.ridge, xi, w);
+        res[c] = static_cast<TV>(b[o]) - w;
+        xo[c] = xi;
+      }
+      if (mode == 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s) * 32] = g == 0 ? TV(0) : res[c];
+        continue;
+      }
+      const TV z0 = D[0] * res[0] + D[1] * res[1] + D[2] * res[2];
+      const TV z1 = D[1] * res[0] + D[3] * res[1] + D[4] * res[2];
+      const TV z2 = D[2] * res[0] + D[4] * res[1] + D[5] * res[2];
+      xo[0] = fma_t(omega, z0, xo[0]);
+      xo[1] = fma_t(omega, z1, xo[1]);
+      xo[2] = fma_t(omega, z2, xo[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xout[ob + (c * 6 + s) * 32] = xo[c];
+        if (mode == 2) gam[s] += static_cast<double>(b[ob + (c * 6 + s) * 32]) * static_cast<double>(xo[c]);
+      }
+    }
+  }
+  if (mode != 2) return;
+  block_sum<6>(gam, scratch);
+  if (publish_partial<6>(gam, partials, &st->counter_misc)) {
+    double tot[6];
+    __syncthreads();
+    reduce_partials<6>(partials, tot, scratch);
+    if (threadIdx.x == 0) {
+      finalize_gamma_state(st, tot, init);
+      st->counter_misc = 0;
+    }
+  }
+}
+
+// first sweep from x = 0: xout = w Dinv b (pointwise)
+template <typename TB, typename TV>
+__global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV* __restrict__ dinv,
+                                    int n, const TB* __restrict__ b, TV* __restrict__ xout, TV omega,
+                                    const PcgState* st) {
+  if (st->stop) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * 6) return;
+  const int idx = t / 6, s = t % 6;
+  const size_t ob = vbase(idx, 18) + s * 32;
+  TV D[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) D[q] = dinv[vbase(idx, 6) + q * 32];
+  const TV r0 = static_cast<TV>(b[ob]), r1 = static_cast<TV>(b[ob + 192]), r2 = static_cast<TV>(b[ob + 384]);
+  xout[ob] = omega * (D[0] * r0 + D[1] * r1 + D[2] * r2);
+  xout[ob + 192] = omega * (D[1] * r0 + D[3] * r1 + D[4] * r2);
+  xout[ob + 384] = omega * (D[2] * r0 + D[4] * r1 + D[5] * r2);
+  (void)node_list;
+}
+
+// ---------------------------------------------------------------- transfers
+// b_c(N) = sum_{n in supp(N)} w(n,N) res_f(n), w = prod over axes (1 | 1/2)
+template <typename TV>
+__global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c,
+                                const int* __restrict__ map_f, int r_f, const TV* __restrict__ res_f,
+                                TV* __restrict__ b_c, const PcgState* st) {
+  if (st->stop) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_c * 6) return;
+  const int idx = t / 6, s = t % 6;
+  const int G = list_c[idx];
+  const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
+  TV acc[3] = {TV(0), TV(0), TV(0)};
+  if (G != 0) {
+    for (int dk = -1; dk <= 1; ++dk)
+      for (int dj = -1; dj <= 1; ++dj)
+        for (int di = -1; di <= 1; ++di) {
+          const int fi = (2 * I + di + r_f) % r_f, fj = (2 * J + dj + r_f) % r_f,
+                    fk = (2 * K + dk + r_f) % r_f;
+          const int nf = map_f[(static_cast<size_t>(fk) * r_f + fj) * r_f + fi];
+          if (nf < 0) continue;
+          const TV w = TV((di ? 0.5 : 1.0) * (dj ? 0.5 : 1.0) * (dk ? 0.5 : 1.0));
+          const size_t o = vbase(nf, 18) + s * 32;
+          acc[0] = fma_t(w, res_f[o], acc[0]);
+          acc[1] = fma_t(w, res_f[o + 192], acc[1]);
+          acc[2] = fma_t(w, res_f[o + 384], acc[2]);
+        }
+  }
+  const size_t oc = vbase(idx, 18) + s * 32;
+  b_c[oc] = acc[0];
+  b_c[oc + 192] = acc[1];
+  b_c[oc + 384] = acc[2];
+}
+
+// x_f(n) += sum_N w(n,N) x_c(N) over the 1..8 coarse parents of n
+template <typename TV>
+__global__ void prolong_kernel(const int* __restrict__ list_f, int n_f, int r_f,
+                               const int* __restrict__ map_c, int r_c, const TV* __restrict__ x_c,
+                               TV* __restrict__ x_f, const PcgState* st) {
+  if (st->stop) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_f * 6) return;
+  const int idx = t / 6, s = t % 6;
+  const int g = list_f[idx];
+  if (g == 0) return;
+  const int i = g % r_f, j = (g / r_f) % r_f, k = g / (r_f * r_f);
+  const int pi[2] = {i >> 1, ((i + 1) >> 1) % r_c}, pj[2] = {j >> 1, ((j + 1) >> 1) % r_c},
+            pk[2] = {k >> 1, ((k + 1) >> 1) % r_c};
+  const int ni = (i & 1) ? 2 : 1, nj = (j & 1) ? 2 : 1, nk = (k & 1) ? 2 : 1;
+  const TV w = TV(1.0 / (ni * nj * nk));
+  TV acc[3] = {TV(0), TV(0), TV(0)};
+  for (int c = 0; c < nk; ++c)
+    for (int b = 0; b < nj; ++b)
+      for (int a = 0; a < ni; ++a) {
+        const int nc = map_c[(static_cast<size_t>(pk[c]) * r_c + pj[b]) * r_c + pi[a]];
+        if (nc < 0) continue;
+        const size_t o = vbase(nc, 18) + s * 32;
+        acc[0] += x_c[o];
+        acc[1] += x_c[o + 192];
+        acc[2] += x_c[o + 384];
+      }
+  const size_t of = vbase(idx, 18) + s * 32;
+  x_f[of] = fma_t(w, acc[0], x_f[of]);
+  x_f[of + 192] = fma_t(w, acc[1], x_f[of + 192]);
+  x_f[of + 384] = fma_t(w, acc[2], x_f[of + 384]);
+}
+
+// ---------------------------------------------------------------- setup
+// coarse node active iff a fine node of its support is active
+__global__ void coarse_flag_kernel(const int* __restrict__ map_f, int r_f, int r_c,
+                                   int* __restrict__ flag_c) {
+  const size_t n3 = static_cast<size_t>(r_c) * r_c * r_c;
+  const size_t G = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (G >= n3) return;
+  const int I = static_cast<int>(G % r_c), J = static_cast<int>((G / r_c) % r_c),
+            K = static_cast<int>(G / (static_cast<size_t>(r_c) * r_c));
+  int on = 0;
+  for (int dk = -1; dk <= 1 && !on; ++dk)
+    for (int dj = -1; dj <= 1 && !on; ++dj)
+      for (int di = -1; di <= 1 && !on; ++di) {
+        const int fi = (2 * I + di + r_f) % r_f, fj = (2 * J + dj + r_f) % r_f, fk = (2 * K + dk + r_f) % r_f;
+        on = map_f[(static_cast<size_t>(fk) * r_f + fj) * r_f + fi] >= 0;
+      }
+  flag_c[G] = on;
+}
+
+// S_{n,m} of level 0 (the masked element sum; pinned node 0 has no row/column)
+template <typename TV>
+__device__ __forceinline__ void fine_block(const TV* __restrict__ betav, int r, int fi, int fj,
+                                           int fk, int dx, int dy, int dz, TV ridge, TV (&S)[9]) {
+#pragma unroll
+  for (int q = 0; q < 9; ++q) S[q] = TV(0);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
+    const int bx = ox + dx, by = oy + dy, bz = oz + dz;
+    if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+    const int ei = (fi - ox + r) % r, ej = (fj - oy + r) % r, ek = (fk - oz + r) % r;
+    const TV be = betav[(static_cast<size_t>(ek) * r + ej) * r + ei];
+    if (be == TV(0)) continue;
+    const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) S[c * 3 + d] = fma_t(be, k0<TV>((3 * a + c) * 24 + 3 * b + d), S[c * 3 + d]);
+  }
+  if (dx == 0 && dy == 0 && dz == 0) {
+    S[0] += ridge;
+    S[4] += ridge;
+    S[8] += ridge;
+  }
+}
+
+// A_c(N, N+D) = sum_{n in supp N} sum_{m ~ n, m in supp(N+D)} w(n,N) A_f(n,m) w(m,N+D)
+// One thread per active coarse node; 243 accumulators in shared memory.
+template <typename TV, bool kFine>
+__global__ void __launch_bounds__(64) galerkin_kernel(const int* __restrict__ list_c, int n_c,
+                                                      int r_c, const int* __restrict__ map_f,
+                                                      int r_f, const TV* __restrict__ betav,
+                                                      const TV* __restrict__ stencil_f, TV ridge,
+                                                      TV* __restrict__ stencil_c) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  TV* acc = reinterpret_cast<TV*>(gsm) + threadIdx.x * kStencil;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_c) return;
+  for (int q = 0; q < kStencil; ++q) acc[q] = TV(0);
+  const int G = list_c[idx];
+  const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
+  if (G != 0) {
+    for (int nk = -1; nk <= 1; ++nk)
+      for (int nj = -1; nj <= 1; ++nj)
+        for (int ni = -1; ni <= 1; ++ni) {
+          // fine node n (unwrapped 2N + d) and its weight for N
+          const int ux = 2 * I + ni, uy = 2 * J + nj, uz = 2 * K + nk;
+          const int fi = (ux + r_f) % r_f, fj = (uy + r_f) % r_f, fk = (uz + r_f) % r_f;
+          const size_t gn = (static_cast<size_t>(fk) * r_f + fj) * r_f + fi;
+          const int nf = map_f[gn];
+          if (nf < 0 || gn == 0) continue;
+          const TV wn = TV((ni ? 0.5 : 1.0) * (nj ? 0.5 : 1.0) * (nk ? 0.5 : 1.0));
+          for (int m = 0; m < 27; ++m) {
+            const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+            const int vx = ux + dx, vy = uy + dy, vz = uz + dz;  // fine m, unwrapped
+            const int mi = (vx + r_f) % r_f, mj = (vy + r_f) % r_f, mk = (vz + r_f) % r_f;
+            const size_t gm = (static_cast<size_t>(mk) * r_f + mj) * r_f + mi;
+            if (gm == 0 || map_f[gm] < 0) continue;
+            TV S[9];
+            if (kFine) {
+              fine_block<TV>(betav, r_f, fi, fj, fk, dx, dy, dz, ridge, S);
+            } else {
+              const TV* sb = stencil_f + vbase(nf, kStencil);
+#pragma unroll
+              for (int q = 0; q < 9; ++q) S[q] = sb[(m * 9 + q) * 32];
+            }
+            // coarse parents of m (unwrapped): even -> v/2, odd -> (v-1)/2, (v+1)/2
+            const int ax0 = (vx - (vx & 1)) / 2, ay0 = (vy - (vy & 1)) / 2, az0 = (vz - (vz & 1)) / 2;
+            const int nx = (vx & 1) ? 2 : 1, ny = (vy & 1) ? 2 : 1, nz = (vz & 1) ? 2 : 1;
+            const TV wm = TV(1.0 / (nx * ny * nz));
+            for (int c = 0; c < nz; ++c)
+              for (int b = 0; b < ny; ++b)
+                for (int a = 0; a < nx; ++a) {
+                  // vx in [2I-2, 2I+2] so the parent offset lies in [-1, 1]
+                  const int Dx = ax0 + a - I, Dy = ay0 + b - J, Dz = az0 + c - K;
+                  const int slot = ((Dz + 1) * 3 + (Dy + 1)) * 3 + (Dx + 1);
+                  const TV w = wn * wm;
+#pragma unroll
+                  for (int q = 0; q < 9; ++q) acc[slot * 9 + q] = fma_t(w, S[q], acc[slot * 9 + q]);
+                }
+          }
+        }
+  }
+  TV* out = stencil_c + vbase(idx, kStencil);
+  for (int q = 0; q < kStencil; ++q) out[q * 32] = acc[q];
+}
+
+// Dinv of a stored level: inverse of the centre 3x3 block (0 for node 0 / singular)
+template <typename TV>
+__global__ void coarse_dinv_kernel(const int* __restrict__ list_c, int n_c,
+                                   const TV* __restrict__ stencil, TV* __restrict__ dinv) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_c) return;
+  const TV* sb = stencil + vbase(idx, kStencil) + 13 * 9 * 32;
+  double D[9];
+  for (int q = 0; q < 9; ++q) D[q] = static_cast<double>(sb[q * 32]);
+  double inv[6] = {0, 0, 0, 0, 0, 0};
+  const double c00 = D[4] * D[8] - D[5] * D[7], c01 = D[5] * D[6] - D[3] * D[8],
+               c02 = D[3] * D[7] - D[4] * D[6];
+  const double det = D[0] * c00 + D[1] * c01 + D[2] * c02;
+  if (list_c[idx] != 0 && det > 0.0) {
+    const double id = 1.0 / det;
+    inv[0] = c00 * id;
+    inv[1] = c01 * id;
+    inv[2] = c02 * id;
+    inv[3] = (D[0] * D[8] - D[2] * D[6]) * id;
+    inv[4] = (D[2] * D[3] - D[0] * D[5]) * id;
+    inv[5] = (D[0] * D[4] - D[1] * D[3]) * id;
+  }
+  for (int q = 0; q < 6; ++q) dinv[vbase(idx, 6) + q * 32] = static_cast<TV>(inv[q]);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+void launch_coarse_flags(const int* map_f, int r_f, int r_c, int* flag_c, cudaStream_t s) {
+  const size_t n3 = static_cast<size_t>(r_c) * r_c * r_c;
+  coarse_flag_kernel<<<static_cast<unsigned>((n3 + 255) / 256), 256, 0, s>>>(map_f, r_f, r_c, flag_c);
+}
+
+template <typename TV>
+void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int r_f,
+                     const TV* beta_f, const TV* stencil_f, TV ridge, TV* stencil_c, cudaStream_t s) {
+  if (n_c == 0) return;
+  const size_t smem = 64 * kStencil * sizeof(TV);
+  if (stencil_f == nullptr) {
+    cudaFuncSetAttribute(galerkin_kernel<TV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    galerkin_kernel<TV, true><<<(n_c + 63) / 64, 64, smem, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f,
+                                                                nullptr, ridge, stencil_c);
+  } else {
+    cudaFuncSetAttribute(galerkin_kernel<TV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    galerkin_kernel<TV, false><<<(n_c + 63) / 64, 64, smem, s>>>(list_c, n_c, r_c, map_f, r_f, nullptr,
+                                                                 stencil_f, ridge, stencil_c);
+  }
+}
+
+template <typename TV>
+void launch_coarse_dinv(const int* list_c, int n_c, const TV* stencil, TV* dinv, cudaStream_t s) {
+  if (n_c) coarse_dinv_kernel<TV><<<(n_c + 127) / 128, 128, 0, s>>>(list_c, n_c, stencil, dinv);
+}
+
+template <typename TB, typename TV>
+void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const TV* xin, TV* xout,
+                        TV omega, int mode, PcgState* st, double* partials, int init, int grid,
+                        cudaStream_t s) {
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
+  if (fine)
+    level_sweep_kernel<TB, TV, true><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+  else
+    level_sweep_kernel<TB, TV, false><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+}
+
+template <typename TB, typename TV>
+void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
+                         cudaStream_t s) {
+  if (L.n) jacobi_first_kernel<TB, TV><<<(L.n * 6 + 255) / 256, 256, 0, s>>>(L.node_list, L.dinv, L.n, b, xout, omega, st);
+}
+
+template <typename TV>
+void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
+                     const PcgState* st, cudaStream_t s) {
+  if (C.n) restrict_kernel<TV><<<(C.n * 6 + 255) / 256, 256, 0, s>>>(C.node_list, C.n, C.r, F.node_map, F.r, res_f, b_c, st);
+}
+
+template <typename TV>
+void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
+                    const PcgState* st, cudaStream_t s) {
+  if (F.n) prolong_kernel<TV><<<(F.n * 6 + 255) / 256, 256, 0, s>>>(F.node_list, F.n, F.r, C.node_map, C.r, x_c, x_f, st);
+}
+
+#define SHL_GMG_INST(TV)                                                                               \
+  template void launch_galerkin<TV>(const int*, int, int, const int*, int, const TV*, const TV*, TV, TV*, \
+                                    cudaStream_t);                                                     \
+  template void launch_coarse_dinv<TV>(const int*, int, const TV*, TV*, cudaStream_t);                 \
+  template void launch_restrict<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,  \
+                                    const PcgState*, cudaStream_t);                                   \
+  template void launch_prolong<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,   \
+                                   const PcgState*, cudaStream_t);
+SHL_GMG_INST(float)
+SHL_GMG_INST(double)
+template void launch_level_sweep<double, float>(const GmgLevelView<float>&, bool, const double*, const float*,
+                                                float*, float, int, PcgState*, double*, int, int, cudaStream_t);
+template void launch_level_sweep<float, float>(const GmgLevelView<float>&, bool, const float*, const float*,
+                                               float*, float, int, PcgState*, double*, int, int, cudaStream_t);
+template void launch_level_sweep<double, double>(const GmgLevelView<double>&, bool, const double*,
+                                                 const double*, double*, double, int, PcgState*, double*,
+                                                 int, int, cudaStream_t);
+template void launch_jacobi_first<double, float>(const GmgLevelView<float>&, const double*, float*, float,
+                                                 const PcgState*, cudaStream_t);
+template void launch_jacobi_first<float, float>(const GmgLevelView<float>&, const float*, float*, float,
+                                                const PcgState*, cudaStream_t);
+template void launch_jacobi_first<double, double>(const GmgLevelView<double>&, const double*, double*, double,
+                                                  const PcgState*, cudaStream_t);

@@ -237,6 +237,125 @@ int resolve_precision(const shl_solve_options& o) {
 }
 
 // ---- solve on the resident mesh ----------------------------------------------
+// ---- geometric multigrid hierarchy (gmg.cuh) ---------------------------------
+struct GmgParams {
+  int nu = 2;          // pre/post block-Jacobi sweeps
+  double omega = 0.6;  // Jacobi damping
+  int min_r = 8;       // coarsest grid (nodes per axis)
+  int coarse_sweeps = 20;
+  int max_levels = 8;
+};
+
+GmgParams gmg_params() {
+  GmgParams g;
+  if (const char* e = std::getenv("SHL_GMG_NU")) g.nu = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("SHL_GMG_OMEGA")) g.omega = std::atof(e);
+  if (const char* e = std::getenv("SHL_GMG_MIN_R")) g.min_r = std::max(4, std::atoi(e));
+  if (const char* e = std::getenv("SHL_GMG_COARSE")) g.coarse_sweeps = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("SHL_GMG_LEVELS")) g.max_levels = std::atoi(e);
+  return g;
+}
+
+// Coarse levels 1..L: active set, ordered ids, Galerkin stencils, Dinv.
+template <typename TV>
+int gmg_setup(shl_ctx* c, const GmgParams& gp, TV ridge) {
+  int rf = c->r;
+  const int* map_f = c->node_map.as<int>();
+  const TV* beta_f = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
+                                     : reinterpret_cast<const TV*>(c->beta32.p);
+  const TV* stencil_f = nullptr;
+  int L = 0;
+  while (L < gp.max_levels && rf % 2 == 0 && rf / 2 >= gp.min_r) {
+    const int rc = rf / 2;
+    const int n3 = rc * rc * rc;
+    if (static_cast<int>(c->gmg.size()) <= L) c->gmg.emplace_back();
+    auto& Lv = c->gmg[L];
+    Lv.flag.ensure(static_cast<size_t>(n3) * sizeof(int));
+    Lv.off.ensure(static_cast<size_t>(n3) * sizeof(int));
+    Lv.map.ensure(static_cast<size_t>(n3) * sizeof(int));
+    Lv.list.ensure(static_cast<size_t>(n3) * sizeof(int));
+    Lv.scan_tmp.ensure(shl::scan_temp_bytes(n3));
+    shl::launch_coarse_flags(map_f, rf, rc, Lv.flag.as<int>(), c->stream);
+    shl::launch_exclusive_scan(Lv.flag.as<int>(), Lv.off.as<int>(), n3, Lv.scan_tmp.p, Lv.scan_tmp.cap,
+                               c->stream);
+    shl::launch_scatter_compact(Lv.flag.as<int>(), Lv.off.as<int>(), n3, Lv.map.as<int>(),
+                                Lv.list.as<int>(), c->stream);
+    int last[2];
+    CK(cudaMemcpyAsync(&last[0], Lv.off.as<int>() + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&last[1], Lv.flag.as<int>() + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    Lv.r = rc;
+    Lv.n = last[0] + last[1];
+    Lv.ld = round_up(Lv.n + 1, 32);
+    Lv.stencil.ensure(static_cast<size_t>(243) * Lv.ld * sizeof(TV));
+    Lv.dinv.ensure(static_cast<size_t>(6) * Lv.ld * sizeof(TV));
+    Lv.vec.ensure(static_cast<size_t>(4) * 18 * Lv.ld * sizeof(TV));
+    CK(cudaMemsetAsync(Lv.vec.p, 0, static_cast<size_t>(4) * 18 * Lv.ld * sizeof(TV), c->stream));
+    shl::launch_galerkin<TV>(Lv.list.as<int>(), Lv.n, rc, map_f, rf, L == 0 ? beta_f : nullptr,
+                             stencil_f, L == 0 ? ridge : TV(0), Lv.stencil.as<TV>(), c->stream);
+    shl::launch_coarse_dinv<TV>(Lv.list.as<int>(), Lv.n, Lv.stencil.as<TV>(), Lv.dinv.as<TV>(), c->stream);
+    c->launches += 5;
+    CK(cudaGetLastError());
+    map_f = Lv.map.as<int>();
+    stencil_f = Lv.stencil.as<TV>();
+    rf = rc;
+    ++L;
+  }
+  return L;
+}
+
+// Symmetric V(nu, nu) cycle: z = M r on level 0; returns the buffer holding z.
+template <typename TX, typename TV>
+struct Vcycle {
+  shl_ctx* c;
+  GmgParams gp;
+  int L = 0;
+  std::vector<shl::GmgLevelView<TV>> view;  // 0..L
+  std::vector<TV*> b, xa, xb, res;          // per level (b[0] unused: level-0 rhs is r)
+  shl::PcgState* st;
+  double* partials;
+  int64_t launches = 0;
+
+  int grid(int n) const { return std::max(1, std::min((n + 255) / 256, c->num_sms * 3)); }
+
+  TV* level(int l, const TX* b0, int init) {
+    const auto& V = view[l];
+    const bool fine = l == 0;
+    const TV w = static_cast<TV>(gp.omega);
+    TV* cur = xa[l];
+    TV* oth = xb[l];
+    auto sweep = [&](TV* xin, TV* xout, int mode) {
+      if (fine)
+        shl::launch_level_sweep<TX, TV>(V, true, b0, xin, xout, w, mode, st, partials, init, grid(V.n), c->stream);
+      else
+        shl::launch_level_sweep<TV, TV>(V, false, b[l], xin, xout, w, mode, st, partials, init, grid(V.n),
+                                        c->stream);
+      ++launches;
+    };
+    if (fine)
+      shl::launch_jacobi_first<TX, TV>(V, b0, cur, w, st, c->stream);
+    else
+      shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, c->stream);
+    ++launches;
+    const int pre = (l == L) ? gp.coarse_sweeps : gp.nu;
+    for (int k = 1; k < pre; ++k) {
+      sweep(cur, oth, 0);
+      std::swap(cur, oth);
+    }
+    if (l == L) return cur;
+    sweep(cur, res[l], 1);
+    shl::launch_restrict<TV>(view[l + 1], V, res[l], b[l + 1], st, c->stream);
+    TV* xc = level(l + 1, b0, init);
+    shl::launch_prolong<TV>(V, view[l + 1], xc, cur, st, c->stream);
+    launches += 2;
+    for (int k = 1; k <= gp.nu; ++k) {
+      sweep(cur, oth, (fine && k == gp.nu) ? 2 : 0);
+      std::swap(cur, oth);
+    }
+    return cur;
+  }
+};
+
 template <typename TX, typename TV>
 void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
                shl_stats* st, int prec) {
@@ -277,6 +396,35 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   CK(cudaMemsetAsync(z, 0, 3 * nV * sizeof(TV), c->stream));
   shl::launch_setup<TX, TV>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), ridge, rv,
                             dinv, c->stream);
+  const bool use_gmg = opt.preconditioner == SHL_PRECOND_GMG;
+  Vcycle<TX, TV> vc{c, gmg_params()};
+  if (use_gmg) {
+    vc.L = gmg_setup<TV>(c, vc.gp, static_cast<TV>(ridge));
+    if (vc.L == 0) throw ShlError(SHL_VALIDATION, "multigrid needs r divisible by 2 with r/2 >= 8");
+    c->gmg0.ensure(static_cast<size_t>(3) * nV * sizeof(TV));
+    CK(cudaMemsetAsync(c->gmg0.p, 0, static_cast<size_t>(3) * nV * sizeof(TV), c->stream));
+    const TV* beta_v = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
+                                       : reinterpret_cast<const TV*>(c->beta32.p);
+    vc.view.push_back({c->node_list.as<int>(), c->node_map.as<int>(), beta_v, nullptr, dinv, r, n, n,
+                       static_cast<TV>(ridge)});
+    TV* g0 = c->gmg0.as<TV>();
+    vc.b.push_back(nullptr);
+    vc.xa.push_back(g0);
+    vc.xb.push_back(g0 + nV);
+    vc.res.push_back(g0 + 2 * nV);
+    for (int l = 0; l < vc.L; ++l) {
+      auto& Lv = c->gmg[l];
+      vc.view.push_back({Lv.list.as<int>(), Lv.map.as<int>(), nullptr, Lv.stencil.as<TV>(), Lv.dinv.as<TV>(),
+                         Lv.r, Lv.n, Lv.n, TV(0)});
+      TV* v = Lv.vec.as<TV>();
+      const size_t s18 = static_cast<size_t>(18) * Lv.ld;
+      vc.b.push_back(v);
+      vc.xa.push_back(v + s18);
+      vc.xb.push_back(v + 2 * s18);
+      vc.res.push_back(v + 3 * s18);
+    }
+    vc.partials = c->partials.as<double>();
+  }
   shl::PcgState hs{};
   hs.tol = opt.tol;
   hs.ridge = ridge;
@@ -290,11 +438,17 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
                                          : reinterpret_cast<const TV*>(c->beta32.p);
   shl::UpdateArgs<TX, TV> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1,
-                            nullptr, 0};
+                            nullptr, 0, use_gmg ? 1 : 0};
   shl::ApplyArgs<TV> aa{c->node_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p, q,
                         c->partials.as<double>(), dst, r, n, ld, n, 0, r, nullptr, 0};
-  // z0 = Dinv b, then w0 = A z0, p0 = z0, q0 = w0, alpha0
+  vc.st = dst;
+  // z = M r: block Jacobi inside the update kernel, or the V-cycle
+  auto precondition = [&](int init) {
+    if (use_gmg) aa.z = vc.level(0, rv, init);
+  };
+  // z0 = M b, then w0 = A z0, p0 = z0, q0 = w0, alpha0
   shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+  precondition(1);
   shl::launch_apply<TV>(aa, grid_a, c->stream);
   ua.init = 0;
   int64_t launches = 2 + 2;
@@ -313,11 +467,13 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
         }
         CK(cudaEventRecord(c->prof_ev[3 * issued], c->stream));
         shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+        precondition(0);
         CK(cudaEventRecord(c->prof_ev[3 * issued + 1], c->stream));
         shl::launch_apply<TV>(aa, grid_a, c->stream);
         CK(cudaEventRecord(c->prof_ev[3 * issued + 2], c->stream));
       } else {
         shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+        precondition(0);
         shl::launch_apply<TV>(aa, grid_a, c->stream);
       }
       ++issued;
@@ -342,6 +498,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
     }
     apply_launches = real;
   }
+  launches += vc.launches;
   CK(cudaEventRecord(c->ev[5], c->stream));
   const shl::PcgState& fin = *c->hstate;
   if (fin.error) throw ShlError(SHL_SOLVER, "grid CG: operator lost positive definiteness");
@@ -375,6 +532,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
     st->apply_ms = apply_ms;
     st->update_ms = update_ms;
     st->apply_launches = apply_launches;
+    st->gmg_levels = use_gmg ? vc.L + 1 : 0;
   }
 }
 

@@ -166,6 +166,45 @@ __device__ void finalize_update_state(PcgState* st, const double (&tot)[12], int
   st->stop = all || st->error || st->it >= st->max_iter;
 }
 
+// GMG mode: the update kernel only reduces r.r (convergence); beta comes
+// from gamma = r.z reduced by the V-cycle's last sweep.
+__device__ void finalize_update_gmg(PcgState* st, const double* rr, int init) {
+  bool all = true;
+  for (int t = 0; t < 6; ++t) {
+    st->rr[t] = rr[t];
+    const double rn = sqrt(rr[t]);
+    if (init) {
+      st->bnorm[t] = rn;
+      st->done[t] = rn == 0.0;
+      st->beta[t] = 0.0;
+      st->alpha[t] = 0.0;
+      st->iters[t] = 0;
+    } else if (!st->done[t]) {
+      st->iters[t] = st->it + 1;
+      if (rn <= st->tol * st->bnorm[t]) {
+        st->done[t] = 1;
+        st->beta[t] = 0.0;
+      }
+    }
+    all = all && st->done[t];
+  }
+  if (!init) st->it += 1;
+  st->all_done = all;
+  st->stop = all || st->error || st->it >= st->max_iter;
+}
+
+__device__ void finalize_gamma_state(PcgState* st, const double (&g)[6], int init) {
+  for (int t = 0; t < 6; ++t) {
+    if (init) {
+      st->gamma[t] = g[t];
+      st->beta[t] = 0.0;
+    } else if (!st->done[t]) {
+      st->beta[t] = g[t] / st->gamma[t];
+      st->gamma[t] = g[t];
+    }
+  }
+}
+
 // ---- K3 + preconditioner setup -------------------------------------------
 // One thread per active node: block-Jacobi inverse (grid_solver.hpp:129-139)
 // and the strain right-hand sides (grid_solver.hpp:141-152), node 0 pinned.
@@ -290,6 +329,60 @@ struct GatherAcc<double> {
   __device__ __forceinline__ double get(int q) const { return y[q]; }
 };
 
+// w = A x at active node idx (grid id g): the matrix-free level-0 operator.
+// beta is global (every rank holds the full mask); the node map covers local
+// planes [zbase, zbase + nzl) (the whole torus when not slabbed).
+template <typename TV>
+__device__ __forceinline__ void fine_gather(GatherAcc<TV>& acc, int idx, int g,
+                                            const TV* __restrict__ xv,
+                                            const TV* __restrict__ betav,
+                                            const int* __restrict__ nmap, int r, int zbase,
+                                            int zero_slot) {
+  acc.zero();
+  if (g == 0) return;  // pinned node (grid_solver.hpp:175)
+  const int rr = r * r;
+  const int i = g % r, j = (g / r) % r, k = g / rr;
+  const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
+  const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
+  const int kz[3] = {k == 0 ? r - 1 : k - 1, k, k == r - 1 ? 0 : k + 1};
+  const int zs[3] = {kz[0] * rr, kz[1] * rr, kz[2] * rr};
+  int zl[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    int lz = kz[d] - zbase;
+    lz += lz < 0 ? r : 0;
+    zl[d] = lz * rr;
+  }
+  TV be[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;  // node's corner in e
+    be[e] = betav[zs[1 - oz] + ys[1 - oy] + xs[1 - ox]];
+  }
+#pragma unroll
+  for (int m = 0; m < 27; ++m) {
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+    int nb = (m == 13) ? idx : nmap[zl[dz + 1] + ys[dy + 1] + xs[dx + 1]];
+    nb = nb < 0 ? zero_slot : nb;
+    TV S[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) S[q] = TV(0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
+      const int bx = ox + dx, by = oy + dy, bz = oz + dz;  // neighbour's corner in e
+      if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+      const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          S[c * 3 + d] = fma_t(be[e], k0<TV>((3 * a + c) * 24 + 3 * b + d), S[c * 3 + d]);
+    }
+    acc.add(S, xv + vbase(nb, 18));
+  }
+}
+
 template <typename TV>
 __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(const ApplyArgs<TV> A) {
   __shared__ double scratch[32 * 6];
@@ -311,56 +404,11 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
   }
   const TV ridge = static_cast<TV>(st->ridge);
   double dl[6] = {0, 0, 0, 0, 0, 0};
-  const int rr = r * r;
   (void)ld;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < A.n; idx += gridDim.x * blockDim.x) {
     const int g = A.node_list[idx];
-    const int i = g % r, j = (g / r) % r, k = g / rr;
-    const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
-    const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
-    const int kz[3] = {k == 0 ? r - 1 : k - 1, k, k == r - 1 ? 0 : k + 1};
-    // beta is global (every rank holds the full mask); the node map covers
-    // local planes [zbase, zbase + nzl) (the whole torus when not slabbed)
-    const int zs[3] = {kz[0] * rr, kz[1] * rr, kz[2] * rr};
-    int zl[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      int lz = kz[d] - A.zbase;
-      lz += lz < 0 ? r : 0;
-      zl[d] = lz * rr;
-    }
-    TV be[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;  // node's corner in e
-      be[e] = betav[zs[1 - oz] + ys[1 - oy] + xs[1 - ox]];
-    }
     GatherAcc<TV> acc;
-    acc.zero();
-    if (g != 0) {
-#pragma unroll
-      for (int m = 0; m < 27; ++m) {
-        const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-        int nb = (m == 13) ? idx : nmap[zl[dz + 1] + ys[dy + 1] + xs[dx + 1]];
-        nb = nb < 0 ? A.zero_slot : nb;
-        TV S[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) S[q] = TV(0);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
-          const int bx = ox + dx, by = oy + dy, bz = oz + dz;  // neighbour's corner in e
-          if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
-          const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-              S[c * 3 + d] = fma_t(be[e], k0<TV>((3 * a + c) * 24 + 3 * b + d), S[c * 3 + d]);
-        }
-        acc.add(S, zv + vbase(nb, 18));
-      }
-    }
+    fine_gather<TV>(acc, idx, g, zv, betav, nmap, r, A.zbase, A.zero_slot);
     const size_t ob = vbase(idx, 18);
 #pragma unroll
     for (int q = 0; q < 18; ++q) {
@@ -420,7 +468,7 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
     const size_t od = vbase(idx, 6);
     // all loads first (keeps ~15 independent requests in flight per thread)
     TX xc[3], rc[3];
-    TV pc[3], qc[3], D[6];
+    TV pc[3], qc[3], D[6] = {};
 #pragma unroll
     for (int c = 0; c < 3; ++c) rc[c] = rv[ob + c * 192];
     if (!U.init) {
@@ -431,14 +479,28 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
         qc[c] = qv[ob + c * 192];
       }
     }
+    if (!U.gmg) {
 #pragma unroll
-    for (int q = 0; q < 6; ++q) D[q] = dv[od + q * 32];
+      for (int q = 0; q < 6; ++q) D[q] = dv[od + q * 32];
+    }
     if (!U.init) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         xc[c] = fma_t(a, static_cast<TX>(pc[c]), xc[c]);
         rc[c] = fma_t(-a, static_cast<TX>(qc[c]), rc[c]);
       }
+    }
+    const double d0 = rc[0], d1 = rc[1], d2 = rc[2];
+    acc[0] += d0 * d0 + d1 * d1 + d2 * d2;
+    if (U.gmg) {
+      if (!U.init) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          xv[ob + c * 192] = xc[c];
+          rv[ob + c * 192] = rc[c];
+        }
+      }
+      continue;
     }
     const TV r0 = static_cast<TV>(rc[0]), r1 = static_cast<TV>(rc[1]), r2 = static_cast<TV>(rc[2]);
     const TV z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
@@ -454,8 +516,6 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
     zv[ob + 0 * 192] = z0;
     zv[ob + 1 * 192] = z1;
     zv[ob + 2 * 192] = z2;
-    const double d0 = rc[0], d1 = rc[1], d2 = rc[2];
-    acc[0] += d0 * d0 + d1 * d1 + d2 * d2;
     acc[1] += d0 * static_cast<double>(z0) + d1 * static_cast<double>(z1) + d2 * static_cast<double>(z2);
   }
   block_sum<2>(acc, scratch);
@@ -476,6 +536,8 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
     if (threadIdx.x == 0) {
       if (U.defer) {
         for (int q = 0; q < 12; ++q) U.totals[q] = tot[q];
+      } else if (U.gmg) {
+        finalize_update_gmg(st, tot, U.init);
       } else {
         finalize_update_state(st, tot, U.init);
       }
@@ -630,6 +692,8 @@ template void launch_pack<float>(const float*, int, int, float*, cudaStream_t);
 template void launch_pack<double>(const double*, int, int, double*, cudaStream_t);
 template void launch_unpack<float>(float*, int, int, const float*, cudaStream_t);
 template void launch_unpack<double>(double*, int, int, const double*, cudaStream_t);
+
+#include "gmg.cuh"
 
 // ---- host-side launchers -----------------------------------------------------
 void upload_element_constants(const double* K0, const double* W, const double* T,

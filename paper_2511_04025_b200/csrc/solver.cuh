@@ -45,6 +45,7 @@ struct UpdateArgs {
   int init;
   double* totals;  // defer != 0: write the 12 reduced sums here, leave state alone
   int defer;
+  int gmg;         // 1: z comes from the multigrid V-cycle (this kernel only reduces r.r)
 };
 
 template <typename TX>
@@ -76,6 +77,39 @@ template <typename T>
 void launch_pack(const T* vec, int first, int count, T* buf, cudaStream_t s);
 template <typename T>
 void launch_unpack(T* vec, int first, int count, const T* buf, cudaStream_t s);
+
+// One multigrid level as the kernels see it (gmg.cuh).
+template <typename TV>
+struct GmgLevelView {
+  const int* node_list;
+  const int* node_map;
+  const TV* beta;     // level 0: dense r^3 beta (matrix-free operator)
+  const TV* stencil;  // levels >= 1: Galerkin 27-point 3x3-block stencils
+  const TV* dinv;
+  int r, n, zero_slot;
+  TV ridge;
+};
+
+void launch_coarse_flags(const int* map_f, int r_f, int r_c, int* flag_c, cudaStream_t s);
+template <typename TV>
+void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int r_f, const TV* beta_f,
+                     const TV* stencil_f, TV ridge, TV* stencil_c, cudaStream_t s);
+template <typename TV>
+void launch_coarse_dinv(const int* list_c, int n_c, const TV* stencil, TV* dinv, cudaStream_t s);
+// mode 0 smooth, 1 residual, 2 final smooth + gamma = b.x reduction (updates beta)
+template <typename TB, typename TV>
+void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const TV* xin, TV* xout,
+                        TV omega, int mode, PcgState* st, double* partials, int init, int grid,
+                        cudaStream_t s);
+template <typename TB, typename TV>
+void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
+                         cudaStream_t s);
+template <typename TV>
+void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
+                     const PcgState* st, cudaStream_t s);
+template <typename TV>
+void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
+                    const PcgState* st, cudaStream_t s);
 
 void upload_element_constants(const double* K0, const double* W, const double* T, cudaStream_t s);
 template <typename TX, typename TV>
