@@ -30,9 +30,28 @@ namespace host {
 
 extern thread_local std::string g_thread_error;
 
+// Owning device allocation that only grows.  Move-only: a copied raw pointer
+// would be freed twice (e.g. when a std::vector of levels reallocates).
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) {
+    o.p = nullptr;
+    o.cap = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFree(p);
+      p = o.p;
+      cap = o.cap;
+      o.p = nullptr;
+      o.cap = 0;
+    }
+    return *this;
+  }
   void ensure(size_t bytes) {
     if (bytes <= cap) return;
     if (p) cudaFree(p);
