@@ -104,7 +104,7 @@ struct DeviceSolveOptions {
   double tol = 1e-9;
   int max_iter = 0;
   int precision = SHL_PREC_AUTO;
-  int preconditioner = SHL_PRECOND_JACOBI;
+  int preconditioner = SHL_PRECOND_AUTO;
   shl_solve_options abi() const { return {tol, max_iter, precision, 0, preconditioner}; }
 };
 

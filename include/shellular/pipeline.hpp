@@ -24,7 +24,7 @@ struct HomogenizeOptions {
   int corner_gauge = 0;                 // any gauge gives the same tensor
   int precision = SHL_PREC_AUTO;        // device arithmetic (shellular_cuda.h)
   int max_iter = 0;
-  int preconditioner = SHL_PRECOND_JACOBI;  // or SHL_PRECOND_GMG (multigrid V-cycle)
+  int preconditioner = SHL_PRECOND_AUTO;  // multigrid V-cycle when r allows (shellular_cuda.h)
   bool return_fields = false;           // copy the grid + element list back
 };
 

@@ -83,7 +83,8 @@ typedef struct {
 /* PCG preconditioner */
 enum {
   SHL_PRECOND_JACOBI = 0, /* 3x3 block Jacobi (grid_solver.hpp:129-139) */
-  SHL_PRECOND_GMG = 1     /* Galerkin geometric multigrid V-cycle (new) */
+  SHL_PRECOND_GMG = 1,    /* Galerkin geometric multigrid V-cycle (new) */
+  SHL_PRECOND_AUTO = 2    /* GMG when r is even and r/2 >= 8, else block Jacobi */
 };
 
 typedef struct {

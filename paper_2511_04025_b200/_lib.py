@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("SHL_LIB") or os.path.join(HERE, "libshellular_cuda.so
 
 SHL_OK, SHL_VALIDATION, SHL_DEGENERATE, SHL_SOLVER, SHL_IO, SHL_CUDA = range(6)
 PREC_AUTO, PREC_FP64, PREC_MIXED, PREC_FP32 = -1, 0, 1, 2
-PRECOND_JACOBI, PRECOND_GMG = 0, 1
+PRECOND_JACOBI, PRECOND_GMG, PRECOND_AUTO = 0, 1, 2
 
 
 class shl_design(C.Structure):

@@ -317,7 +317,7 @@ def isotropic_tensor(mat: BaseMaterial) -> np.ndarray:
 PRECISION = {"auto": L.PREC_AUTO, "fp64": L.PREC_FP64, "mixed": L.PREC_MIXED,
              "fp32": L.PREC_FP32}
 PRECISION_NAME = {v: k for k, v in PRECISION.items()}
-PRECONDITIONER = {"jacobi": L.PRECOND_JACOBI, "gmg": L.PRECOND_GMG}
+PRECONDITIONER = {"jacobi": L.PRECOND_JACOBI, "gmg": L.PRECOND_GMG, "auto": L.PRECOND_AUTO}
 
 
 @dataclass
@@ -327,7 +327,8 @@ class HomogenizeOptions:
     max_iter: int = 0
     precision: str = "auto"
     check_every: int = 0
-    preconditioner: str = "jacobi"  # "jacobi" (grid_solver.hpp block Jacobi) | "gmg"
+    # "auto" (multigrid when r is even and r/2 >= 8) | "gmg" | "jacobi" (grid_solver.hpp:129-139)
+    preconditioner: str = "auto"
 
     def _abi(self):
         return L.shl_solve_options(float(self.residual_tol), int(self.max_iter),

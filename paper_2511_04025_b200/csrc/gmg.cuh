@@ -31,7 +31,7 @@ __device__ __forceinline__ void stencil_gather(GatherAcc<TV>& acc, int idx, int 
   const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
   const int zs[3] = {(k == 0 ? r - 1 : k - 1) * rr, k * rr, (k == r - 1 ? 0 : k + 1) * rr};
   const TV* sb = stencil + vbase(idx, kStencil);
-#pragma unroll 1
+#pragma unroll 3
   for (int m = 0; m < 27; ++m) {
     const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
     int nb = (m == 13) ? idx : nmap[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
@@ -117,6 +117,51 @@ __global__ void __launch_bounds__(256, 3)
       st->counter_misc = 0;
     }
   }
+}
+
+// Coarsest level in ONE block: nsweep damped Jacobi sweeps from x = 0 with a
+// block barrier between sweeps (the level has <= r_min^3 nodes), instead of
+// nsweep launches that would be pure launch latency.
+template <typename TV>
+__global__ void __launch_bounds__(1024) coarsest_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
+                                                        TV* __restrict__ xa, TV* __restrict__ xb,
+                                                        TV omega, int nsweep, const PcgState* st,
+                                                        TV** result) {
+  if (st->stop) return;
+  TV* cur = xa;
+  TV* oth = xb;
+  for (int t = threadIdx.x; t < L.n * 6; t += blockDim.x) {  // x = w Dinv b
+    const int idx = t / 6, s = t % 6;
+    const size_t ob = vbase(idx, 18) + s * 32;
+    TV D[6];
+    for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
+    const TV r0 = b[ob], r1 = b[ob + 192], r2 = b[ob + 384];
+    cur[ob] = omega * (D[0] * r0 + D[1] * r1 + D[2] * r2);
+    cur[ob + 192] = omega * (D[1] * r0 + D[3] * r1 + D[4] * r2);
+    cur[ob + 384] = omega * (D[2] * r0 + D[4] * r1 + D[5] * r2);
+  }
+  for (int k = 1; k < nsweep; ++k) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < L.n; idx += blockDim.x) {
+      const int g = L.node_list[idx];
+      GatherAcc<TV> acc;
+      stencil_gather<TV>(acc, idx, g, cur, L.stencil, L.node_map, L.r, L.zero_slot);
+      const size_t ob = vbase(idx, 18);
+      TV D[6];
+      for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
+      for (int s = 0; s < 6; ++s) {
+        TV res[3];
+        for (int c = 0; c < 3; ++c) res[c] = b[ob + (c * 6 + s) * 32] - acc.get(c * 6 + s);
+        oth[ob + s * 32] = fma_t(omega, D[0] * res[0] + D[1] * res[1] + D[2] * res[2], cur[ob + s * 32]);
+        oth[ob + (6 + s) * 32] = fma_t(omega, D[1] * res[0] + D[3] * res[1] + D[4] * res[2], cur[ob + (6 + s) * 32]);
+        oth[ob + (12 + s) * 32] = fma_t(omega, D[2] * res[0] + D[4] * res[1] + D[5] * res[2], cur[ob + (12 + s) * 32]);
+      }
+    }
+    TV* t = cur;
+    cur = oth;
+    oth = t;
+  }
+  (void)result;
 }
 
 // first sweep from x = 0: xout = w Dinv b (pointwise)
@@ -378,6 +423,13 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
     level_sweep_kernel<TB, TV, false><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
 }
 
+template <typename TV>
+void launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xa, TV* xb, TV omega, int nsweep,
+                     const PcgState* st, cudaStream_t s) {
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
+  coarsest_kernel<TV><<<1, 1024, 0, s>>>(a, b, xa, xb, omega, nsweep, st, nullptr);
+}
+
 template <typename TB, typename TV>
 void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
                          cudaStream_t s) {
@@ -406,6 +458,10 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
                                    const PcgState*, cudaStream_t);
 SHL_GMG_INST(float)
 SHL_GMG_INST(double)
+template void launch_coarsest<float>(const GmgLevelView<float>&, const float*, float*, float*, float, int,
+                                     const PcgState*, cudaStream_t);
+template void launch_coarsest<double>(const GmgLevelView<double>&, const double*, double*, double*, double,
+                                      int, const PcgState*, cudaStream_t);
 template void launch_level_sweep<double, float>(const GmgLevelView<float>&, bool, const double*, const float*,
                                                 float*, float, int, PcgState*, double*, int, int, cudaStream_t);
 template void launch_level_sweep<float, float>(const GmgLevelView<float>&, bool, const float*, const float*,

@@ -239,8 +239,8 @@ int resolve_precision(const shl_solve_options& o) {
 // ---- solve on the resident mesh ----------------------------------------------
 // ---- geometric multigrid hierarchy (gmg.cuh) ---------------------------------
 struct GmgParams {
-  int nu = 2;          // pre/post block-Jacobi sweeps
-  double omega = 0.6;  // Jacobi damping
+  int nu = 1;          // pre/post block-Jacobi sweeps
+  double omega = 0.6;  // Jacobi damping (>= 0.7 loses smoother convergence: lambda_max(D^-1 A) ~ 2.9)
   int min_r = 8;       // coarsest grid (nodes per axis)
   int coarse_sweeps = 20;
   int max_levels = 8;
@@ -332,17 +332,22 @@ struct Vcycle {
                                         c->stream);
       ++launches;
     };
+    if (l == L && l > 0) {
+      // coarsest: all sweeps in one single-block kernel; result lands in
+      // xa (odd sweep count) or xb (even)
+      shl::launch_coarsest<TV>(V, b[l], cur, oth, w, gp.coarse_sweeps, st, c->stream);
+      ++launches;
+      return (gp.coarse_sweeps % 2) ? cur : oth;
+    }
     if (fine)
       shl::launch_jacobi_first<TX, TV>(V, b0, cur, w, st, c->stream);
     else
       shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, c->stream);
     ++launches;
-    const int pre = (l == L) ? gp.coarse_sweeps : gp.nu;
-    for (int k = 1; k < pre; ++k) {
+    for (int k = 1; k < gp.nu; ++k) {
       sweep(cur, oth, 0);
       std::swap(cur, oth);
     }
-    if (l == L) return cur;
     sweep(cur, res[l], 1);
     shl::launch_restrict<TV>(view[l + 1], V, res[l], b[l + 1], st, c->stream);
     TV* xc = level(l + 1, b0, init);
@@ -396,8 +401,9 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   CK(cudaMemsetAsync(z, 0, 3 * nV * sizeof(TV), c->stream));
   shl::launch_setup<TX, TV>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), ridge, rv,
                             dinv, c->stream);
-  const bool use_gmg = opt.preconditioner == SHL_PRECOND_GMG;
   Vcycle<TX, TV> vc{c, gmg_params()};
+  const bool use_gmg = opt.preconditioner == SHL_PRECOND_GMG ||
+                       (opt.preconditioner == SHL_PRECOND_AUTO && r % 2 == 0 && r / 2 >= vc.gp.min_r);
   if (use_gmg) {
     vc.L = gmg_setup<TV>(c, vc.gp, static_cast<TV>(ridge));
     if (vc.L == 0) throw ShlError(SHL_VALIDATION, "multigrid needs r divisible by 2 with r/2 >= 8");

@@ -108,7 +108,7 @@ def test_grid_solve_vs_oracle(S, O, seed, r, prec, tol, bar):
     om = O.build_reduced_mesh(O.sample_grid(od, r))
     K0 = O.element_stiffness(1.0, 0.3, 1.0 / r)
     ref = O.grid_solve(om.beta, K0, tol=1e-11)
-    res = S.GridSolver(om.beta, r, K0, precision=prec).solve(tol)
+    res = S.GridSolver(om.beta, r, K0, precision=prec, preconditioner="jacobi").solve(tol)
     assert rel_max(res.tensor, ref.C) < bar
     assert np.all(res.iterations > 0)
     if prec == "fp64":
@@ -235,7 +235,7 @@ def test_zslab_matches_single_device(S, r, G, prec, tol):
     """Config C5 code path (emulated slabs): same C^H and iteration counts as the
     undecomposed solve; only the cross-slab summation order differs."""
     d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), 3)
-    opt = S.HomogenizeOptions(residual_tol=tol, precision=prec)
+    opt = S.HomogenizeOptions(residual_tol=tol, precision=prec, preconditioner="jacobi")
     ref = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, opt)
     got = S.homogenize_slabs(d, S.ShellParams(), S.BaseMaterial(), r, G, opt)
     assert rel_fro(got.tensor, ref.tensor) < (1e-10 if prec == "fp64" else 1e-6)
@@ -247,3 +247,32 @@ def test_zslab_validation(S):
     d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), 3)
     with pytest.raises(S.ValidationError):
         S.homogenize_slabs(d, S.ShellParams(), S.BaseMaterial(), 16, 9)
+
+
+@pytest.mark.parametrize("r,prec,seed", [(32, "mixed", 1), (64, "mixed", 2), (64, "fp64", 3),
+                                         (128, "mixed", 1), (32, "fp32", 4)])
+def test_gmg_matches_block_jacobi(S, r, prec, seed):
+    """Multigrid-preconditioned CG reaches the same C^H as the reference's
+    block-Jacobi PCG, in an r-independent handful of iterations."""
+    d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), seed)
+    tol = 1e-5
+    ja = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r,
+                      S.HomogenizeOptions(residual_tol=tol, precision=prec, preconditioner="jacobi"))
+    mg = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r,
+                      S.HomogenizeOptions(residual_tol=tol, precision=prec, preconditioner="gmg"))
+    assert mg.stats.gmg_levels >= 2
+    assert rel_fro(mg.tensor, ja.tensor) < 1e-6
+    assert max(mg.iterations) < 60 < max(ja.iterations)
+
+
+def test_gmg_vs_oracle_and_direct(S, O):
+    """GMG on a seeded r=16 reduced mesh against the oracle's masked PCG (which is
+    pinned to the reference's master-slave direct solve)."""
+    r = 16
+    od = O.seeded_design(12)
+    om = O.build_reduced_mesh(O.sample_grid(od, r))
+    K0 = O.element_stiffness(1.0, 0.3, 1.0 / r)
+    ref = O.grid_solve(om.beta, K0, tol=1e-11)
+    res = S.GridSolver(om.beta, r, K0, precision="fp64", preconditioner="gmg").solve(1e-11)
+    assert res.stats.gmg_levels == 2
+    assert rel_max(res.tensor, ref.C) < 1e-8
