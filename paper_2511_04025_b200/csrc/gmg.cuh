@@ -31,7 +31,7 @@ __device__ __forceinline__ void stencil_gather(GatherAcc<TV>& acc, int idx, int 
   const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
   const int zs[3] = {(k == 0 ? r - 1 : k - 1) * rr, k * rr, (k == r - 1 ? 0 : k + 1) * rr};
   const TV* sb = stencil + vbase(idx, kStencil);
-#pragma unroll 3
+#pragma unroll
   for (int m = 0; m < 27; ++m) {
     const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
     int nb = (m == 13) ? idx : nmap[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
@@ -162,6 +162,99 @@ __global__ void __launch_bounds__(1024) coarsest_kernel(const LevelArgs<TV> L, c
     oth = t;
   }
   (void)result;
+}
+
+// ---------------------------------------------------------------- coarsest: dense direct
+// The coarsest level (r = 4: <= 64 nodes, <= 192 unknowns) is solved exactly:
+// its Galerkin matrix is assembled densely (periodic offsets that wrap onto
+// the same node add up), ridged by 1e-8 mean|diag| for floating parts, and
+// inverted once per design by Gauss-Jordan in FP64; each V-cycle then applies
+// the inverse to the six load cases in one small kernel.
+template <typename TV>
+__global__ void dense_assemble_kernel(const int* __restrict__ list, int n, const int* __restrict__ map,
+                                      int r, const TV* __restrict__ stencil, double* __restrict__ A) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * 27) return;
+  const int i = t / 27, m = t % 27;
+  const int g = list[i];
+  if (g == 0) return;
+  const int x = g % r, y = (g / r) % r, z = g / (r * r);
+  const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+  const int nx = (x + dx + r) % r, ny = (y + dy + r) % r, nz = (z + dz + r) % r;
+  const int gj = (nz * r + ny) * r + nx;
+  const int j = map[gj];
+  if (j < 0 || gj == 0) return;
+  const int N = 3 * n;
+  const TV* sb = stencil + vbase(i, kStencil) + m * 9 * 32;
+  for (int c = 0; c < 3; ++c)
+    for (int d = 0; d < 3; ++d)
+      atomicAdd(&A[static_cast<size_t>(3 * i + c) * N + 3 * j + d], static_cast<double>(sb[(c * 3 + d) * 32]));
+}
+
+// [A | I] -> [I | A^-1] in one block (SPD after the ridge: no pivoting)
+template <typename TV>
+__global__ void __launch_bounds__(1024) dense_invert_kernel(double* __restrict__ A, double* __restrict__ W,
+                                                            int n, const int* __restrict__ list,
+                                                            TV* __restrict__ Ainv) {
+  const int N = 3 * n, N2 = 2 * N;
+  __shared__ double ridge;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    int cnt = 0;
+    for (int q = 0; q < N; ++q)
+      if (A[static_cast<size_t>(q) * N + q] != 0.0) {
+        s += fabs(A[static_cast<size_t>(q) * N + q]);
+        ++cnt;
+      }
+    ridge = cnt ? 1e-8 * s / cnt : 1.0;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < N * N2; t += blockDim.x) {
+    const int row = t / N2, col = t % N2;
+    double v;
+    if (col < N) {
+      v = A[static_cast<size_t>(row) * N + col];
+      if (row == col) v = (list[row / 3] == 0) ? 1.0 : v + ridge;  // pinned node: identity
+    } else {
+      v = (col - N == row) ? 1.0 : 0.0;
+    }
+    W[t] = v;
+  }
+  __syncthreads();
+  // N <= 768 (coarsest <= 256 nodes): pivot row and pivot column staged in smem
+  __shared__ double pivrow[1536];
+  __shared__ double pivcol[768];
+  for (int k = 0; k < N; ++k) {
+    const double piv = W[static_cast<size_t>(k) * N2 + k];
+    for (int col = threadIdx.x; col < N2; col += blockDim.x) pivrow[col] = W[static_cast<size_t>(k) * N2 + col] / piv;
+    for (int row = threadIdx.x; row < N; row += blockDim.x) pivcol[row] = W[static_cast<size_t>(row) * N2 + k];
+    __syncthreads();
+    for (int t = threadIdx.x; t < N * N2; t += blockDim.x) {
+      const int row = t / N2, col = t % N2;
+      W[t] = (row == k) ? pivrow[col] : W[t] - pivcol[row] * pivrow[col];
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
+    const int row = t / N, col = t % N;
+    const bool pinned = list[row / 3] == 0 || list[col / 3] == 0;
+    Ainv[t] = pinned ? TV(0) : static_cast<TV>(W[static_cast<size_t>(row) * N2 + N + col]);
+  }
+}
+
+template <typename TV>
+__global__ void dense_apply_kernel(const TV* __restrict__ Ainv, int n, const TV* __restrict__ b,
+                                   TV* __restrict__ x, const PcgState* st) {
+  if (st->stop) return;
+  const int N = 3 * n;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N * 6; t += gridDim.x * blockDim.x) {
+    const int row = t / 6, s = t % 6;
+    double acc = 0.0;
+    for (int j = 0; j < N; ++j)
+      acc += static_cast<double>(Ainv[static_cast<size_t>(row) * N + j]) *
+             static_cast<double>(b[vbase(j / 3, 18) + ((j % 3) * 6 + s) * 32]);
+    x[vbase(row / 3, 18) + ((row % 3) * 6 + s) * 32] = static_cast<TV>(acc);
+  }
 }
 
 // first sweep from x = 0: xout = w Dinv b (pointwise)
@@ -430,6 +523,19 @@ void launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xa, TV* xb, TV 
   coarsest_kernel<TV><<<1, 1024, 0, s>>>(a, b, xa, xb, omega, nsweep, st, nullptr);
 }
 
+template <typename TV>
+void launch_dense_setup(const GmgLevelView<TV>& L, double* A, double* W, TV* Ainv, cudaStream_t s) {
+  const int N = 3 * L.n;
+  cudaMemsetAsync(A, 0, sizeof(double) * N * N, s);
+  dense_assemble_kernel<TV><<<(L.n * 27 + 127) / 128, 128, 0, s>>>(L.node_list, L.n, L.node_map, L.r, L.stencil, A);
+  dense_invert_kernel<TV><<<1, 1024, 0, s>>>(A, W, L.n, L.node_list, Ainv);
+}
+
+template <typename TV>
+void launch_dense_apply(const TV* Ainv, int n, const TV* b, TV* x, const PcgState* st, cudaStream_t s) {
+  dense_apply_kernel<TV><<<(3 * n * 6 + 127) / 128, 128, 0, s>>>(Ainv, n, b, x, st);
+}
+
 template <typename TB, typename TV>
 void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
                          cudaStream_t s) {
@@ -458,6 +564,11 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
                                    const PcgState*, cudaStream_t);
 SHL_GMG_INST(float)
 SHL_GMG_INST(double)
+template void launch_dense_setup<float>(const GmgLevelView<float>&, double*, double*, float*, cudaStream_t);
+template void launch_dense_setup<double>(const GmgLevelView<double>&, double*, double*, double*, cudaStream_t);
+template void launch_dense_apply<float>(const float*, int, const float*, float*, const PcgState*, cudaStream_t);
+template void launch_dense_apply<double>(const double*, int, const double*, double*, const PcgState*,
+                                         cudaStream_t);
 template void launch_coarsest<float>(const GmgLevelView<float>&, const float*, float*, float*, float, int,
                                      const PcgState*, cudaStream_t);
 template void launch_coarsest<double>(const GmgLevelView<double>&, const double*, double*, double*, double,

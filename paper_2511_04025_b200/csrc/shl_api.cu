@@ -241,9 +241,10 @@ int resolve_precision(const shl_solve_options& o) {
 struct GmgParams {
   int nu = 1;          // pre/post block-Jacobi sweeps
   double omega = 0.6;  // Jacobi damping (>= 0.7 loses smoother convergence: lambda_max(D^-1 A) ~ 2.9)
-  int min_r = 8;       // coarsest grid (nodes per axis)
-  int coarse_sweeps = 20;
+  int min_r = 4;       // coarsest grid (nodes per axis), solved densely when <= 256 nodes
+  int coarse_sweeps = 20;  // only when the coarsest level is too large to invert
   int max_levels = 8;
+  bool dense = true;
 };
 
 GmgParams gmg_params() {
@@ -253,6 +254,7 @@ GmgParams gmg_params() {
   if (const char* e = std::getenv("SHL_GMG_MIN_R")) g.min_r = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("SHL_GMG_COARSE")) g.coarse_sweeps = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SHL_GMG_LEVELS")) g.max_levels = std::atoi(e);
+  if (const char* e = std::getenv("SHL_GMG_DENSE")) g.dense = std::atoi(e) != 0;
   return g;
 }
 
@@ -315,6 +317,7 @@ struct Vcycle {
   shl::PcgState* st;
   double* partials;
   int64_t launches = 0;
+  const TV* dense_inv = nullptr;  // coarsest-level inverse (nullptr: Jacobi sweeps)
 
   int grid(int n) const { return std::max(1, std::min((n + 255) / 256, c->num_sms * 3)); }
 
@@ -332,6 +335,11 @@ struct Vcycle {
                                         c->stream);
       ++launches;
     };
+    if (l == L && l > 0 && dense_inv) {
+      shl::launch_dense_apply<TV>(dense_inv, V.n, b[l], cur, st, c->stream);
+      ++launches;
+      return cur;
+    }
     if (l == L && l > 0) {
       // coarsest: all sweeps in one single-block kernel; result lands in
       // xa (odd sweep count) or xb (even)
@@ -339,11 +347,10 @@ struct Vcycle {
       ++launches;
       return (gp.coarse_sweeps % 2) ? cur : oth;
     }
-    if (fine)
-      shl::launch_jacobi_first<TX, TV>(V, b0, cur, w, st, c->stream);
-    else
+    if (!fine) {
       shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, c->stream);
-    ++launches;
+      ++launches;
+    }  // level 0: the update kernel already wrote w Dinv r into xa[0]
     for (int k = 1; k < gp.nu; ++k) {
       sweep(cur, oth, 0);
       std::swap(cur, oth);
@@ -430,6 +437,17 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
       vc.res.push_back(v + 3 * s18);
     }
     vc.partials = c->partials.as<double>();
+    const auto& Vc = vc.view.back();
+    if (vc.gp.dense && Vc.n <= shl::kDenseCoarsestMaxNodes) {
+      const size_t N = 3 * static_cast<size_t>(Vc.n);
+      c->gmg_dense.ensure(N * N * sizeof(double) * 3 + N * N * sizeof(TV));
+      double* A = c->gmg_dense.as<double>();
+      double* Wk = A + N * N;
+      TV* Ainv = reinterpret_cast<TV*>(Wk + 2 * N * N);
+      shl::launch_dense_setup<TV>(Vc, A, Wk, Ainv, c->stream);
+      CK(cudaGetLastError());
+      vc.dense_inv = Ainv;
+    }
   }
   shl::PcgState hs{};
   hs.tol = opt.tol;
@@ -444,7 +462,8 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
                                          : reinterpret_cast<const TV*>(c->beta32.p);
   shl::UpdateArgs<TX, TV> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1,
-                            nullptr, 0, use_gmg ? 1 : 0};
+                            nullptr, 0, use_gmg ? 1 : 0, use_gmg ? vc.xa[0] : nullptr,
+                            static_cast<TV>(vc.gp.omega)};
   shl::ApplyArgs<TV> aa{c->node_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p, q,
                         c->partials.as<double>(), dst, r, n, ld, n, 0, r, nullptr, 0};
   vc.st = dst;

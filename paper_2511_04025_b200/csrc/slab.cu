@@ -302,7 +302,8 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     for (int s = 0; s < nloc; ++s) {
       Slab& S = slabs[s];
       UpdateArgs<TX, TV> ua{X(S), R(S), Pv(S), Q(S), Z(S), D(S), S.partials.as<double>(), dst,
-                            S.P.n_owned, static_cast<int>(S.ld), init, totals + 12 * s, 1};
+                            S.P.n_owned, static_cast<int>(S.ld), init, totals + 12 * s, 1, 0,
+                            nullptr, TV(0)};
       launch_update<TX, TV>(ua, grid_u(S), c->stream);
     }
     reduce(12);

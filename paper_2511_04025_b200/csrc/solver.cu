@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
         qc[c] = qv[ob + c * 192];
       }
     }
-    if (!U.gmg) {
+    if (!U.gmg || U.gmg_x0) {
 #pragma unroll
       for (int q = 0; q < 6; ++q) D[q] = dv[od + q * 32];
     }
@@ -499,6 +499,13 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
           xv[ob + c * 192] = xc[c];
           rv[ob + c * 192] = rc[c];
         }
+      }
+      if (U.gmg_x0) {  // fused first smoothing sweep of the V-cycle (x = w Dinv r)
+        const TV r0 = static_cast<TV>(rc[0]), r1 = static_cast<TV>(rc[1]), r2 = static_cast<TV>(rc[2]);
+        const TV w = U.gmg_omega;
+        U.gmg_x0[ob + 0 * 192] = w * (D[0] * r0 + D[1] * r1 + D[2] * r2);
+        U.gmg_x0[ob + 1 * 192] = w * (D[1] * r0 + D[3] * r1 + D[4] * r2);
+        U.gmg_x0[ob + 2 * 192] = w * (D[2] * r0 + D[4] * r1 + D[5] * r2);
       }
       continue;
     }
