@@ -197,24 +197,33 @@ __global__ void __launch_bounds__(1024) dense_invert_kernel(double* __restrict__
                                                             int n, const int* __restrict__ list,
                                                             TV* __restrict__ Ainv) {
   const int N = 3 * n, N2 = 2 * N;
-  __shared__ double ridge;
+  // Rows whose diagonal is (numerically) empty -- coarse nodes whose support
+  // barely touches the shell -- are dropped like pinned node 0 (the Jacobi
+  // path zeroes them through det <= 0); the rest get a 1e-4 mean|diag| ridge
+  // so that coarse null modes of floating parts stay bounded.
+  __shared__ double ridge, mean_diag;
   if (threadIdx.x == 0) {
     double s = 0.0;
     int cnt = 0;
     for (int q = 0; q < N; ++q)
-      if (A[static_cast<size_t>(q) * N + q] != 0.0) {
-        s += fabs(A[static_cast<size_t>(q) * N + q]);
+      if (A[static_cast<size_t>(q) * N + q] > 0.0) {
+        s += A[static_cast<size_t>(q) * N + q];
         ++cnt;
       }
-    ridge = cnt ? 1e-8 * s / cnt : 1.0;
+    mean_diag = cnt ? s / cnt : 1.0;
+    ridge = 1e-4 * mean_diag;
   }
   __syncthreads();
+  auto dropped = [&](int q) {
+    return list[q / 3] == 0 || !(A[static_cast<size_t>(q) * N + q] > 1e-6 * mean_diag);
+  };
   for (int t = threadIdx.x; t < N * N2; t += blockDim.x) {
     const int row = t / N2, col = t % N2;
     double v;
     if (col < N) {
       v = A[static_cast<size_t>(row) * N + col];
-      if (row == col) v = (list[row / 3] == 0) ? 1.0 : v + ridge;  // pinned node: identity
+      if (dropped(row) || dropped(col)) v = 0.0;
+      if (row == col) v = dropped(row) ? 1.0 : v + ridge;
     } else {
       v = (col - N == row) ? 1.0 : 0.0;
     }
@@ -237,8 +246,9 @@ __global__ void __launch_bounds__(1024) dense_invert_kernel(double* __restrict__
   }
   for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
     const int row = t / N, col = t % N;
-    const bool pinned = list[row / 3] == 0 || list[col / 3] == 0;
-    Ainv[t] = pinned ? TV(0) : static_cast<TV>(W[static_cast<size_t>(row) * N2 + N + col]);
+    const bool zero = dropped(row) || dropped(col);
+    const double sym = 0.5 * (W[static_cast<size_t>(row) * N2 + N + col] + W[static_cast<size_t>(col) * N2 + N + row]);
+    Ainv[t] = zero ? TV(0) : static_cast<TV>(sym);
   }
 }
 
@@ -451,15 +461,30 @@ __global__ void __launch_bounds__(64) galerkin_kernel(const int* __restrict__ li
   for (int q = 0; q < kStencil; ++q) out[q * 32] = acc[q];
 }
 
-// Dinv of a stored level: inverse of the centre 3x3 block (0 for node 0 / singular)
+// Dinv of a stored level: inverse of the centre 3x3 block (0 for node 0 /
+// singular).  l1 != 0: l1-block-Jacobi -- each diagonal entry also gets the
+// row's off-block absolute sum, which makes the smoother convergent for any
+// SPD matrix (no damping to tune on Galerkin levels, whose lambda_max(D^-1 A)
+// exceeds the fine level's).
 template <typename TV>
 __global__ void coarse_dinv_kernel(const int* __restrict__ list_c, int n_c,
-                                   const TV* __restrict__ stencil, TV* __restrict__ dinv) {
+                                   const TV* __restrict__ stencil, TV* __restrict__ dinv, int l1) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_c) return;
   const TV* sb = stencil + vbase(idx, kStencil) + 13 * 9 * 32;
   double D[9];
   for (int q = 0; q < 9; ++q) D[q] = static_cast<double>(sb[q * 32]);
+  if (l1) {
+    const TV* s0 = stencil + vbase(idx, kStencil);
+    for (int c = 0; c < 3; ++c) {
+      double extra = 0.0;
+      for (int m = 0; m < 27; ++m) {
+        if (m == 13) continue;
+        for (int d = 0; d < 3; ++d) extra += fabs(static_cast<double>(s0[(m * 9 + c * 3 + d) * 32]));
+      }
+      D[c * 3 + c] += extra;
+    }
+  }
   double inv[6] = {0, 0, 0, 0, 0, 0};
   const double c00 = D[4] * D[8] - D[5] * D[7], c01 = D[5] * D[6] - D[3] * D[8],
                c02 = D[3] * D[7] - D[4] * D[6];
@@ -501,8 +526,8 @@ void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int 
 }
 
 template <typename TV>
-void launch_coarse_dinv(const int* list_c, int n_c, const TV* stencil, TV* dinv, cudaStream_t s) {
-  if (n_c) coarse_dinv_kernel<TV><<<(n_c + 127) / 128, 128, 0, s>>>(list_c, n_c, stencil, dinv);
+void launch_coarse_dinv(const int* list_c, int n_c, const TV* stencil, TV* dinv, int l1, cudaStream_t s) {
+  if (n_c) coarse_dinv_kernel<TV><<<(n_c + 127) / 128, 128, 0, s>>>(list_c, n_c, stencil, dinv, l1);
 }
 
 template <typename TB, typename TV>
@@ -557,7 +582,7 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
 #define SHL_GMG_INST(TV)                                                                               \
   template void launch_galerkin<TV>(const int*, int, int, const int*, int, const TV*, const TV*, TV, TV*, \
                                     cudaStream_t);                                                     \
-  template void launch_coarse_dinv<TV>(const int*, int, const TV*, TV*, cudaStream_t);                 \
+  template void launch_coarse_dinv<TV>(const int*, int, const TV*, TV*, int, cudaStream_t);            \
   template void launch_restrict<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,  \
                                     const PcgState*, cudaStream_t);                                   \
   template void launch_prolong<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,   \

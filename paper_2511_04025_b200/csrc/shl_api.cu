@@ -245,6 +245,8 @@ struct GmgParams {
   int coarse_sweeps = 20;  // only when the coarsest level is too large to invert
   int max_levels = 8;
   bool dense = true;
+  double omega_c = 0.6;    // damping on the stored (Galerkin) levels
+  int l1 = 0;              // l1-block-Jacobi on the stored levels
 };
 
 GmgParams gmg_params() {
@@ -255,6 +257,8 @@ GmgParams gmg_params() {
   if (const char* e = std::getenv("SHL_GMG_COARSE")) g.coarse_sweeps = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SHL_GMG_LEVELS")) g.max_levels = std::atoi(e);
   if (const char* e = std::getenv("SHL_GMG_DENSE")) g.dense = std::atoi(e) != 0;
+  if (const char* e = std::getenv("SHL_GMG_OMEGA_C")) g.omega_c = std::atof(e);
+  if (const char* e = std::getenv("SHL_GMG_L1")) g.l1 = std::atoi(e);
   return g;
 }
 
@@ -295,7 +299,8 @@ int gmg_setup(shl_ctx* c, const GmgParams& gp, TV ridge) {
     CK(cudaMemsetAsync(Lv.vec.p, 0, static_cast<size_t>(4) * 18 * Lv.ld * sizeof(TV), c->stream));
     shl::launch_galerkin<TV>(Lv.list.as<int>(), Lv.n, rc, map_f, rf, L == 0 ? beta_f : nullptr,
                              stencil_f, L == 0 ? ridge : TV(0), Lv.stencil.as<TV>(), c->stream);
-    shl::launch_coarse_dinv<TV>(Lv.list.as<int>(), Lv.n, Lv.stencil.as<TV>(), Lv.dinv.as<TV>(), c->stream);
+    shl::launch_coarse_dinv<TV>(Lv.list.as<int>(), Lv.n, Lv.stencil.as<TV>(), Lv.dinv.as<TV>(), gp.l1,
+                                c->stream);
     c->launches += 5;
     CK(cudaGetLastError());
     map_f = Lv.map.as<int>();
@@ -324,7 +329,7 @@ struct Vcycle {
   TV* level(int l, const TX* b0, int init) {
     const auto& V = view[l];
     const bool fine = l == 0;
-    const TV w = static_cast<TV>(gp.omega);
+    const TV w = static_cast<TV>(fine ? gp.omega : gp.omega_c);
     TV* cur = xa[l];
     TV* oth = xb[l];
     auto sweep = [&](TV* xin, TV* xout, int mode) {

@@ -97,7 +97,7 @@ template <typename TV>
 void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int r_f, const TV* beta_f,
                      const TV* stencil_f, TV ridge, TV* stencil_c, cudaStream_t s);
 template <typename TV>
-void launch_coarse_dinv(const int* list_c, int n_c, const TV* stencil, TV* dinv, cudaStream_t s);
+void launch_coarse_dinv(const int* list_c, int n_c, const TV* stencil, TV* dinv, int l1, cudaStream_t s);
 // mode 0 smooth, 1 residual, 2 final smooth + gamma = b.x reduction (updates beta)
 template <typename TB, typename TV>
 void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const TV* xin, TV* xout,
