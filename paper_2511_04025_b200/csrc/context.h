@@ -119,7 +119,6 @@ struct shl_ctx {
   };
   std::vector<GmgLevel> gmg;
   DevBuf gmg0;  // level-0 V-cycle work vectors (xa, xb, res)
-  DevBuf gmg_dense;  // coarsest-level dense matrix, Gauss-Jordan workspace, inverse
   Misc* hmisc = nullptr;
   shl::PcgState* hstate = nullptr;
   double* hC = nullptr;

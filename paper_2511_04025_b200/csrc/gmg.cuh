@@ -119,151 +119,89 @@ __global__ void __launch_bounds__(256, 3)
   }
 }
 
-// Coarsest level in ONE block: nsweep damped Jacobi sweeps from x = 0 with a
-// block barrier between sweeps (the level has <= r_min^3 nodes), instead of
-// nsweep launches that would be pure launch latency.
+// Stored (Galerkin) levels are small and latency-bound, so they run one
+// thread per (node, load case): 27 stencil blocks (L1-shared by the six
+// load-case threads of a node) against the neighbour's 3 components.
+template <typename TV>
+__device__ __forceinline__ void coarse_point(const LevelArgs<TV>& L, const TV* __restrict__ b,
+                                             const TV* __restrict__ xin, TV* __restrict__ xout,
+                                             TV omega, int mode, int idx, int s) {
+  const int g = L.node_list[idx];
+  const size_t ob = vbase(idx, 18) + s * 32;
+  if (g == 0) {
+    xout[ob] = xout[ob + 192] = xout[ob + 384] = TV(0);
+    return;
+  }
+  const int r = L.r, rr = r * r;
+  const int i = g % r, j = (g / r) % r, k = g / rr;
+  const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
+  const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
+  const int zs[3] = {(k == 0 ? r - 1 : k - 1) * rr, k * rr, (k == r - 1 ? 0 : k + 1) * rr};
+  const TV* sb = L.stencil + vbase(idx, kStencil);
+  TV y0 = TV(0), y1 = TV(0), y2 = TV(0);
+#pragma unroll
+  for (int m = 0; m < 27; ++m) {
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+    int nb = (m == 13) ? idx : L.node_map[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
+    nb = nb < 0 ? L.zero_slot : nb;
+    const TV* xm = xin + vbase(nb, 18) + s * 32;
+    const TV x0 = xm[0], x1 = xm[192], x2 = xm[384];
+    const TV* S = sb + m * 9 * 32;
+    y0 = fma_t(S[0 * 32], x0, fma_t(S[1 * 32], x1, fma_t(S[2 * 32], x2, y0)));
+    y1 = fma_t(S[3 * 32], x0, fma_t(S[4 * 32], x1, fma_t(S[5 * 32], x2, y1)));
+    y2 = fma_t(S[6 * 32], x0, fma_t(S[7 * 32], x1, fma_t(S[8 * 32], x2, y2)));
+  }
+  const TV r0 = b[ob] - y0, r1 = b[ob + 192] - y1, r2 = b[ob + 384] - y2;
+  if (mode == 1) {
+    xout[ob] = r0;
+    xout[ob + 192] = r1;
+    xout[ob + 384] = r2;
+    return;
+  }
+  TV D[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
+  xout[ob] = fma_t(omega, D[0] * r0 + D[1] * r1 + D[2] * r2, xin[ob]);
+  xout[ob + 192] = fma_t(omega, D[1] * r0 + D[3] * r1 + D[4] * r2, xin[ob + 192]);
+  xout[ob + 384] = fma_t(omega, D[2] * r0 + D[4] * r1 + D[5] * r2, xin[ob + 384]);
+}
+
+template <typename TV>
+__global__ void __launch_bounds__(256) coarse_sweep_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
+                                                           const TV* __restrict__ xin, TV* __restrict__ xout,
+                                                           TV omega, int mode, const PcgState* st) {
+  if (st->stop) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= L.n * 6) return;
+  coarse_point<TV>(L, b, xin, xout, omega, mode, t / 6, t % 6);
+}
+
+// Coarsest level in ONE block: x = w Dinv b, then nsweep-1 damped Jacobi
+// sweeps with a block barrier between them (the level has <= min_r^3 nodes),
+// instead of nsweep launches that would be pure launch latency.
 template <typename TV>
 __global__ void __launch_bounds__(1024) coarsest_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
-                                                        TV* __restrict__ xa, TV* __restrict__ xb,
-                                                        TV omega, int nsweep, const PcgState* st,
-                                                        TV** result) {
+                                                        TV* xa, TV* xb, TV omega, int nsweep,
+                                                        const PcgState* st) {
   if (st->stop) return;
-  TV* cur = xa;
-  TV* oth = xb;
-  for (int t = threadIdx.x; t < L.n * 6; t += blockDim.x) {  // x = w Dinv b
+  for (int t = threadIdx.x; t < L.n * 6; t += blockDim.x) {
     const int idx = t / 6, s = t % 6;
     const size_t ob = vbase(idx, 18) + s * 32;
     TV D[6];
     for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
     const TV r0 = b[ob], r1 = b[ob + 192], r2 = b[ob + 384];
-    cur[ob] = omega * (D[0] * r0 + D[1] * r1 + D[2] * r2);
-    cur[ob + 192] = omega * (D[1] * r0 + D[3] * r1 + D[4] * r2);
-    cur[ob + 384] = omega * (D[2] * r0 + D[4] * r1 + D[5] * r2);
+    xa[ob] = omega * (D[0] * r0 + D[1] * r1 + D[2] * r2);
+    xa[ob + 192] = omega * (D[1] * r0 + D[3] * r1 + D[4] * r2);
+    xa[ob + 384] = omega * (D[2] * r0 + D[4] * r1 + D[5] * r2);
   }
+  TV* cur = xa;
+  TV* oth = xb;
   for (int k = 1; k < nsweep; ++k) {
     __syncthreads();
-    for (int idx = threadIdx.x; idx < L.n; idx += blockDim.x) {
-      const int g = L.node_list[idx];
-      GatherAcc<TV> acc;
-      stencil_gather<TV>(acc, idx, g, cur, L.stencil, L.node_map, L.r, L.zero_slot);
-      const size_t ob = vbase(idx, 18);
-      TV D[6];
-      for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
-      for (int s = 0; s < 6; ++s) {
-        TV res[3];
-        for (int c = 0; c < 3; ++c) res[c] = b[ob + (c * 6 + s) * 32] - acc.get(c * 6 + s);
-        oth[ob + s * 32] = fma_t(omega, D[0] * res[0] + D[1] * res[1] + D[2] * res[2], cur[ob + s * 32]);
-        oth[ob + (6 + s) * 32] = fma_t(omega, D[1] * res[0] + D[3] * res[1] + D[4] * res[2], cur[ob + (6 + s) * 32]);
-        oth[ob + (12 + s) * 32] = fma_t(omega, D[2] * res[0] + D[4] * res[1] + D[5] * res[2], cur[ob + (12 + s) * 32]);
-      }
-    }
-    TV* t = cur;
+    for (int t = threadIdx.x; t < L.n * 6; t += blockDim.x) coarse_point<TV>(L, b, cur, oth, omega, 0, t / 6, t % 6);
+    TV* tmp = cur;
     cur = oth;
-    oth = t;
-  }
-  (void)result;
-}
-
-// ---------------------------------------------------------------- coarsest: dense direct
-// The coarsest level (r = 4: <= 64 nodes, <= 192 unknowns) is solved exactly:
-// its Galerkin matrix is assembled densely (periodic offsets that wrap onto
-// the same node add up), ridged by 1e-8 mean|diag| for floating parts, and
-// inverted once per design by Gauss-Jordan in FP64; each V-cycle then applies
-// the inverse to the six load cases in one small kernel.
-template <typename TV>
-__global__ void dense_assemble_kernel(const int* __restrict__ list, int n, const int* __restrict__ map,
-                                      int r, const TV* __restrict__ stencil, double* __restrict__ A) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * 27) return;
-  const int i = t / 27, m = t % 27;
-  const int g = list[i];
-  if (g == 0) return;
-  const int x = g % r, y = (g / r) % r, z = g / (r * r);
-  const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-  const int nx = (x + dx + r) % r, ny = (y + dy + r) % r, nz = (z + dz + r) % r;
-  const int gj = (nz * r + ny) * r + nx;
-  const int j = map[gj];
-  if (j < 0 || gj == 0) return;
-  const int N = 3 * n;
-  const TV* sb = stencil + vbase(i, kStencil) + m * 9 * 32;
-  for (int c = 0; c < 3; ++c)
-    for (int d = 0; d < 3; ++d)
-      atomicAdd(&A[static_cast<size_t>(3 * i + c) * N + 3 * j + d], static_cast<double>(sb[(c * 3 + d) * 32]));
-}
-
-// [A | I] -> [I | A^-1] in one block (SPD after the ridge: no pivoting)
-template <typename TV>
-__global__ void __launch_bounds__(1024) dense_invert_kernel(double* __restrict__ A, double* __restrict__ W,
-                                                            int n, const int* __restrict__ list,
-                                                            TV* __restrict__ Ainv) {
-  const int N = 3 * n, N2 = 2 * N;
-  // Rows whose diagonal is (numerically) empty -- coarse nodes whose support
-  // barely touches the shell -- are dropped like pinned node 0 (the Jacobi
-  // path zeroes them through det <= 0); the rest get a 1e-4 mean|diag| ridge
-  // so that coarse null modes of floating parts stay bounded.
-  __shared__ double ridge, mean_diag;
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    int cnt = 0;
-    for (int q = 0; q < N; ++q)
-      if (A[static_cast<size_t>(q) * N + q] > 0.0) {
-        s += A[static_cast<size_t>(q) * N + q];
-        ++cnt;
-      }
-    mean_diag = cnt ? s / cnt : 1.0;
-    ridge = 1e-4 * mean_diag;
-  }
-  __syncthreads();
-  auto dropped = [&](int q) {
-    return list[q / 3] == 0 || !(A[static_cast<size_t>(q) * N + q] > 1e-6 * mean_diag);
-  };
-  for (int t = threadIdx.x; t < N * N2; t += blockDim.x) {
-    const int row = t / N2, col = t % N2;
-    double v;
-    if (col < N) {
-      v = A[static_cast<size_t>(row) * N + col];
-      if (dropped(row) || dropped(col)) v = 0.0;
-      if (row == col) v = dropped(row) ? 1.0 : v + ridge;
-    } else {
-      v = (col - N == row) ? 1.0 : 0.0;
-    }
-    W[t] = v;
-  }
-  __syncthreads();
-  // N <= 768 (coarsest <= 256 nodes): pivot row and pivot column staged in smem
-  __shared__ double pivrow[1536];
-  __shared__ double pivcol[768];
-  for (int k = 0; k < N; ++k) {
-    const double piv = W[static_cast<size_t>(k) * N2 + k];
-    for (int col = threadIdx.x; col < N2; col += blockDim.x) pivrow[col] = W[static_cast<size_t>(k) * N2 + col] / piv;
-    for (int row = threadIdx.x; row < N; row += blockDim.x) pivcol[row] = W[static_cast<size_t>(row) * N2 + k];
-    __syncthreads();
-    for (int t = threadIdx.x; t < N * N2; t += blockDim.x) {
-      const int row = t / N2, col = t % N2;
-      W[t] = (row == k) ? pivrow[col] : W[t] - pivcol[row] * pivrow[col];
-    }
-    __syncthreads();
-  }
-  for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
-    const int row = t / N, col = t % N;
-    const bool zero = dropped(row) || dropped(col);
-    const double sym = 0.5 * (W[static_cast<size_t>(row) * N2 + N + col] + W[static_cast<size_t>(col) * N2 + N + row]);
-    Ainv[t] = zero ? TV(0) : static_cast<TV>(sym);
-  }
-}
-
-template <typename TV>
-__global__ void dense_apply_kernel(const TV* __restrict__ Ainv, int n, const TV* __restrict__ b,
-                                   TV* __restrict__ x, const PcgState* st) {
-  if (st->stop) return;
-  const int N = 3 * n;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N * 6; t += gridDim.x * blockDim.x) {
-    const int row = t / 6, s = t % 6;
-    double acc = 0.0;
-    for (int j = 0; j < N; ++j)
-      acc += static_cast<double>(Ainv[static_cast<size_t>(row) * N + j]) *
-             static_cast<double>(b[vbase(j / 3, 18) + ((j % 3) * 6 + s) * 32]);
-    x[vbase(row / 3, 18) + ((row % 3) * 6 + s) * 32] = static_cast<TV>(acc);
+    oth = tmp;
   }
 }
 
@@ -535,30 +473,20 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s) {
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
-  if (fine)
+  if (fine) {
     level_sweep_kernel<TB, TV, true><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
-  else
-    level_sweep_kernel<TB, TV, false><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+  } else {
+    (void)grid;
+    coarse_sweep_kernel<TV><<<(L.n * 6 + 255) / 256, 256, 0, s>>>(a, reinterpret_cast<const TV*>(b), xin,
+                                                                  xout, omega, mode, st);
+  }
 }
 
 template <typename TV>
 void launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xa, TV* xb, TV omega, int nsweep,
                      const PcgState* st, cudaStream_t s) {
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
-  coarsest_kernel<TV><<<1, 1024, 0, s>>>(a, b, xa, xb, omega, nsweep, st, nullptr);
-}
-
-template <typename TV>
-void launch_dense_setup(const GmgLevelView<TV>& L, double* A, double* W, TV* Ainv, cudaStream_t s) {
-  const int N = 3 * L.n;
-  cudaMemsetAsync(A, 0, sizeof(double) * N * N, s);
-  dense_assemble_kernel<TV><<<(L.n * 27 + 127) / 128, 128, 0, s>>>(L.node_list, L.n, L.node_map, L.r, L.stencil, A);
-  dense_invert_kernel<TV><<<1, 1024, 0, s>>>(A, W, L.n, L.node_list, Ainv);
-}
-
-template <typename TV>
-void launch_dense_apply(const TV* Ainv, int n, const TV* b, TV* x, const PcgState* st, cudaStream_t s) {
-  dense_apply_kernel<TV><<<(3 * n * 6 + 127) / 128, 128, 0, s>>>(Ainv, n, b, x, st);
+  coarsest_kernel<TV><<<1, 1024, 0, s>>>(a, b, xa, xb, omega, nsweep, st);
 }
 
 template <typename TB, typename TV>
@@ -589,11 +517,6 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
                                    const PcgState*, cudaStream_t);
 SHL_GMG_INST(float)
 SHL_GMG_INST(double)
-template void launch_dense_setup<float>(const GmgLevelView<float>&, double*, double*, float*, cudaStream_t);
-template void launch_dense_setup<double>(const GmgLevelView<double>&, double*, double*, double*, cudaStream_t);
-template void launch_dense_apply<float>(const float*, int, const float*, float*, const PcgState*, cudaStream_t);
-template void launch_dense_apply<double>(const double*, int, const double*, double*, const PcgState*,
-                                         cudaStream_t);
 template void launch_coarsest<float>(const GmgLevelView<float>&, const float*, float*, float*, float, int,
                                      const PcgState*, cudaStream_t);
 template void launch_coarsest<double>(const GmgLevelView<double>&, const double*, double*, double*, double,

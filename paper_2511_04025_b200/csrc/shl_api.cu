@@ -241,10 +241,10 @@ int resolve_precision(const shl_solve_options& o) {
 struct GmgParams {
   int nu = 1;          // pre/post block-Jacobi sweeps
   double omega = 0.6;  // Jacobi damping (>= 0.7 loses smoother convergence: lambda_max(D^-1 A) ~ 2.9)
-  int min_r = 4;       // coarsest grid (nodes per axis), solved densely when <= 256 nodes
-  int coarse_sweeps = 20;  // only when the coarsest level is too large to invert
+  int min_r = 8;       // coarsest grid (nodes per axis); r = 4 Galerkin levels of a thin shell
+                       // made the V-cycle indefinite on half the designs tested
+  int coarse_sweeps = 20;  // damped Jacobi sweeps on the coarsest level (one kernel)
   int max_levels = 8;
-  bool dense = true;
   double omega_c = 0.6;    // damping on the stored (Galerkin) levels
   int l1 = 0;              // l1-block-Jacobi on the stored levels
 };
@@ -256,7 +256,6 @@ GmgParams gmg_params() {
   if (const char* e = std::getenv("SHL_GMG_MIN_R")) g.min_r = std::max(4, std::atoi(e));
   if (const char* e = std::getenv("SHL_GMG_COARSE")) g.coarse_sweeps = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SHL_GMG_LEVELS")) g.max_levels = std::atoi(e);
-  if (const char* e = std::getenv("SHL_GMG_DENSE")) g.dense = std::atoi(e) != 0;
   if (const char* e = std::getenv("SHL_GMG_OMEGA_C")) g.omega_c = std::atof(e);
   if (const char* e = std::getenv("SHL_GMG_L1")) g.l1 = std::atoi(e);
   return g;
@@ -322,7 +321,6 @@ struct Vcycle {
   shl::PcgState* st;
   double* partials;
   int64_t launches = 0;
-  const TV* dense_inv = nullptr;  // coarsest-level inverse (nullptr: Jacobi sweeps)
 
   int grid(int n) const { return std::max(1, std::min((n + 255) / 256, c->num_sms * 3)); }
 
@@ -340,11 +338,6 @@ struct Vcycle {
                                         c->stream);
       ++launches;
     };
-    if (l == L && l > 0 && dense_inv) {
-      shl::launch_dense_apply<TV>(dense_inv, V.n, b[l], cur, st, c->stream);
-      ++launches;
-      return cur;
-    }
     if (l == L && l > 0) {
       // coarsest: all sweeps in one single-block kernel; result lands in
       // xa (odd sweep count) or xb (even)
@@ -442,17 +435,6 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
       vc.res.push_back(v + 3 * s18);
     }
     vc.partials = c->partials.as<double>();
-    const auto& Vc = vc.view.back();
-    if (vc.gp.dense && Vc.n <= shl::kDenseCoarsestMaxNodes) {
-      const size_t N = 3 * static_cast<size_t>(Vc.n);
-      c->gmg_dense.ensure(N * N * sizeof(double) * 3 + N * N * sizeof(TV));
-      double* A = c->gmg_dense.as<double>();
-      double* Wk = A + N * N;
-      TV* Ainv = reinterpret_cast<TV*>(Wk + 2 * N * N);
-      shl::launch_dense_setup<TV>(Vc, A, Wk, Ainv, c->stream);
-      CK(cudaGetLastError());
-      vc.dense_inv = Ainv;
-    }
   }
   shl::PcgState hs{};
   hs.tol = opt.tol;

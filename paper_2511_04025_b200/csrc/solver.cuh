@@ -103,11 +103,6 @@ template <typename TB, typename TV>
 void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const TV* xin, TV* xout,
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s);
-constexpr int kDenseCoarsestMaxNodes = 256;
-template <typename TV>
-void launch_dense_setup(const GmgLevelView<TV>& L, double* A, double* W, TV* Ainv, cudaStream_t s);
-template <typename TV>
-void launch_dense_apply(const TV* Ainv, int n, const TV* b, TV* x, const PcgState* st, cudaStream_t s);
 template <typename TV>
 void launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xa, TV* xb, TV omega, int nsweep,
                      const PcgState* st, cudaStream_t s);
