@@ -119,92 +119,6 @@ __global__ void __launch_bounds__(256, 3)
   }
 }
 
-// Stored (Galerkin) levels are small and latency-bound, so they run one
-// thread per (node, load case): 27 stencil blocks (L1-shared by the six
-// load-case threads of a node) against the neighbour's 3 components.
-template <typename TV>
-__device__ __forceinline__ void coarse_point(const LevelArgs<TV>& L, const TV* __restrict__ b,
-                                             const TV* __restrict__ xin, TV* __restrict__ xout,
-                                             TV omega, int mode, int idx, int s) {
-  const int g = L.node_list[idx];
-  const size_t ob = vbase(idx, 18) + s * 32;
-  if (g == 0) {
-    xout[ob] = xout[ob + 192] = xout[ob + 384] = TV(0);
-    return;
-  }
-  const int r = L.r, rr = r * r;
-  const int i = g % r, j = (g / r) % r, k = g / rr;
-  const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
-  const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
-  const int zs[3] = {(k == 0 ? r - 1 : k - 1) * rr, k * rr, (k == r - 1 ? 0 : k + 1) * rr};
-  const TV* sb = L.stencil + vbase(idx, kStencil);
-  TV y0 = TV(0), y1 = TV(0), y2 = TV(0);
-#pragma unroll
-  for (int m = 0; m < 27; ++m) {
-    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-    int nb = (m == 13) ? idx : L.node_map[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
-    nb = nb < 0 ? L.zero_slot : nb;
-    const TV* xm = xin + vbase(nb, 18) + s * 32;
-    const TV x0 = xm[0], x1 = xm[192], x2 = xm[384];
-    const TV* S = sb + m * 9 * 32;
-    y0 = fma_t(S[0 * 32], x0, fma_t(S[1 * 32], x1, fma_t(S[2 * 32], x2, y0)));
-    y1 = fma_t(S[3 * 32], x0, fma_t(S[4 * 32], x1, fma_t(S[5 * 32], x2, y1)));
-    y2 = fma_t(S[6 * 32], x0, fma_t(S[7 * 32], x1, fma_t(S[8 * 32], x2, y2)));
-  }
-  const TV r0 = b[ob] - y0, r1 = b[ob + 192] - y1, r2 = b[ob + 384] - y2;
-  if (mode == 1) {
-    xout[ob] = r0;
-    xout[ob + 192] = r1;
-    xout[ob + 384] = r2;
-    return;
-  }
-  TV D[6];
-#pragma unroll
-  for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
-  xout[ob] = fma_t(omega, D[0] * r0 + D[1] * r1 + D[2] * r2, xin[ob]);
-  xout[ob + 192] = fma_t(omega, D[1] * r0 + D[3] * r1 + D[4] * r2, xin[ob + 192]);
-  xout[ob + 384] = fma_t(omega, D[2] * r0 + D[4] * r1 + D[5] * r2, xin[ob + 384]);
-}
-
-template <typename TV>
-__global__ void __launch_bounds__(256) coarse_sweep_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
-                                                           const TV* __restrict__ xin, TV* __restrict__ xout,
-                                                           TV omega, int mode, const PcgState* st) {
-  if (st->stop) return;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= L.n * 6) return;
-  coarse_point<TV>(L, b, xin, xout, omega, mode, t / 6, t % 6);
-}
-
-// Coarsest level in ONE block: x = w Dinv b, then nsweep-1 damped Jacobi
-// sweeps with a block barrier between them (the level has <= min_r^3 nodes),
-// instead of nsweep launches that would be pure launch latency.
-template <typename TV>
-__global__ void __launch_bounds__(1024) coarsest_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
-                                                        TV* xa, TV* xb, TV omega, int nsweep,
-                                                        const PcgState* st) {
-  if (st->stop) return;
-  for (int t = threadIdx.x; t < L.n * 6; t += blockDim.x) {
-    const int idx = t / 6, s = t % 6;
-    const size_t ob = vbase(idx, 18) + s * 32;
-    TV D[6];
-    for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
-    const TV r0 = b[ob], r1 = b[ob + 192], r2 = b[ob + 384];
-    xa[ob] = omega * (D[0] * r0 + D[1] * r1 + D[2] * r2);
-    xa[ob + 192] = omega * (D[1] * r0 + D[3] * r1 + D[4] * r2);
-    xa[ob + 384] = omega * (D[2] * r0 + D[4] * r1 + D[5] * r2);
-  }
-  TV* cur = xa;
-  TV* oth = xb;
-  for (int k = 1; k < nsweep; ++k) {
-    __syncthreads();
-    for (int t = threadIdx.x; t < L.n * 6; t += blockDim.x) coarse_point<TV>(L, b, cur, oth, omega, 0, t / 6, t % 6);
-    TV* tmp = cur;
-    cur = oth;
-    oth = tmp;
-  }
-}
-
 // first sweep from x = 0: xout = w Dinv b (pointwise)
 template <typename TB, typename TV>
 __global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV* __restrict__ dinv,
@@ -473,20 +387,10 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s) {
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
-  if (fine) {
+  if (fine)
     level_sweep_kernel<TB, TV, true><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
-  } else {
-    (void)grid;
-    coarse_sweep_kernel<TV><<<(L.n * 6 + 255) / 256, 256, 0, s>>>(a, reinterpret_cast<const TV*>(b), xin,
-                                                                  xout, omega, mode, st);
-  }
-}
-
-template <typename TV>
-void launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xa, TV* xb, TV omega, int nsweep,
-                     const PcgState* st, cudaStream_t s) {
-  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
-  coarsest_kernel<TV><<<1, 1024, 0, s>>>(a, b, xa, xb, omega, nsweep, st);
+  else
+    level_sweep_kernel<TB, TV, false><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
 }
 
 template <typename TB, typename TV>
@@ -517,10 +421,6 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
                                    const PcgState*, cudaStream_t);
 SHL_GMG_INST(float)
 SHL_GMG_INST(double)
-template void launch_coarsest<float>(const GmgLevelView<float>&, const float*, float*, float*, float, int,
-                                     const PcgState*, cudaStream_t);
-template void launch_coarsest<double>(const GmgLevelView<double>&, const double*, double*, double*, double,
-                                      int, const PcgState*, cudaStream_t);
 template void launch_level_sweep<double, float>(const GmgLevelView<float>&, bool, const double*, const float*,
                                                 float*, float, int, PcgState*, double*, int, int, cudaStream_t);
 template void launch_level_sweep<float, float>(const GmgLevelView<float>&, bool, const float*, const float*,

@@ -243,7 +243,7 @@ struct GmgParams {
   double omega = 0.6;  // Jacobi damping (>= 0.7 loses smoother convergence: lambda_max(D^-1 A) ~ 2.9)
   int min_r = 8;       // coarsest grid (nodes per axis); r = 4 Galerkin levels of a thin shell
                        // made the V-cycle indefinite on half the designs tested
-  int coarse_sweeps = 20;  // damped Jacobi sweeps on the coarsest level (one kernel)
+  int coarse_sweeps = 10;  // damped Jacobi sweeps on the coarsest level
   int max_levels = 8;
   double omega_c = 0.6;    // damping on the stored (Galerkin) levels
   int l1 = 0;              // l1-block-Jacobi on the stored levels
@@ -338,21 +338,16 @@ struct Vcycle {
                                         c->stream);
       ++launches;
     };
-    if (l == L && l > 0) {
-      // coarsest: all sweeps in one single-block kernel; result lands in
-      // xa (odd sweep count) or xb (even)
-      shl::launch_coarsest<TV>(V, b[l], cur, oth, w, gp.coarse_sweeps, st, c->stream);
-      ++launches;
-      return (gp.coarse_sweeps % 2) ? cur : oth;
-    }
     if (!fine) {
       shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, c->stream);
       ++launches;
     }  // level 0: the update kernel already wrote w Dinv r into xa[0]
-    for (int k = 1; k < gp.nu; ++k) {
+    const int pre = (l == L) ? gp.coarse_sweeps : gp.nu;  // coarsest: damped Jacobi solve
+    for (int k = 1; k < pre; ++k) {
       sweep(cur, oth, 0);
       std::swap(cur, oth);
     }
+    if (l == L) return cur;
     sweep(cur, res[l], 1);
     shl::launch_restrict<TV>(view[l + 1], V, res[l], b[l + 1], st, c->stream);
     TV* xc = level(l + 1, b0, init);

@@ -103,9 +103,6 @@ template <typename TB, typename TV>
 void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const TV* xin, TV* xout,
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s);
-template <typename TV>
-void launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xa, TV* xb, TV omega, int nsweep,
-                     const PcgState* st, cudaStream_t s);
 template <typename TB, typename TV>
 void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
                          cudaStream_t s);
