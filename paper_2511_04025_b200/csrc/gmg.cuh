@@ -119,6 +119,79 @@ __global__ void __launch_bounds__(256, 3)
   }
 }
 
+// Stored (Galerkin) levels are small, so a per-node loop over 27 neighbours is
+// a pure dependent-load chain (~30 us per sweep regardless of size).  Here one
+// WARP owns a node and lane m < 27 owns stencil neighbour m: each lane does one
+// node-map lookup and one block-times-vector (9 x 6 FMA), a butterfly shuffle
+// sums the 18 outputs, and lanes 0..5 finish load case s = lane.
+template <typename TV>
+__global__ void __launch_bounds__(256) coarse_warp_sweep_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
+                                                                const TV* __restrict__ xin, TV* __restrict__ xout,
+                                                                TV omega, int mode, const PcgState* st) {
+  if (st->stop) return;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= L.n) return;  // whole warps exit together
+  const int idx = warp;
+  const int g = L.node_list[idx];
+  TV y[18];
+#pragma unroll
+  for (int q = 0; q < 18; ++q) y[q] = TV(0);
+  if (g != 0 && lane < 27) {
+    const int r = L.r, rr = r * r;
+    const int i = g % r, j = (g / r) % r, k = g / rr;
+    const int dx = lane % 3 - 1, dy = (lane / 3) % 3 - 1, dz = lane / 9 - 1;
+    const int xi = (i + dx + r) % r, yj = (j + dy + r) % r, zk = (k + dz + r) % r;
+    int nb = (lane == 13) ? idx : L.node_map[(zk * r + yj) * r + xi];
+    if (nb >= 0) {
+      const TV* S = L.stencil + vbase(idx, kStencil) + lane * 9 * 32;
+      const TV* xm = xin + vbase(nb, 18);
+      TV Sv[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) Sv[q] = S[q * 32];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const TV x0 = xm[s * 32], x1 = xm[(6 + s) * 32], x2 = xm[(12 + s) * 32];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          y[c * 6 + s] = fma_t(Sv[c * 3 + 0], x0, fma_t(Sv[c * 3 + 1], x1, Sv[c * 3 + 2] * x2));
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 18; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) y[q] += __shfl_xor_sync(0xffffffffu, y[q], o);
+  if (lane >= 6) return;
+  const int sl = lane;
+  const size_t ob = vbase(idx, 18) + sl * 32;
+  if (g == 0) {
+    xout[ob] = xout[ob + 192] = xout[ob + 384] = TV(0);
+    return;
+  }
+  // select this lane's load case without dynamic register indexing
+  TV y0 = y[sl], y1 = y[6 + sl], y2 = y[12 + sl];
+#pragma unroll
+  for (int s = 0; s < 6; ++s)
+    if (s == sl) {
+      y0 = y[s];
+      y1 = y[6 + s];
+      y2 = y[12 + s];
+    }
+  const TV r0 = b[ob] - y0, r1 = b[ob + 192] - y1, r2 = b[ob + 384] - y2;
+  if (mode == 1) {
+    xout[ob] = r0;
+    xout[ob + 192] = r1;
+    xout[ob + 384] = r2;
+    return;
+  }
+  TV D[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
+  xout[ob] = fma_t(omega, D[0] * r0 + D[1] * r1 + D[2] * r2, xin[ob]);
+  xout[ob + 192] = fma_t(omega, D[1] * r0 + D[3] * r1 + D[4] * r2, xin[ob + 192]);
+  xout[ob + 384] = fma_t(omega, D[2] * r0 + D[4] * r1 + D[5] * r2, xin[ob + 384]);
+}
+
 // first sweep from x = 0: xout = w Dinv b (pointwise)
 template <typename TB, typename TV>
 __global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV* __restrict__ dinv,
@@ -387,10 +460,13 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s) {
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
-  if (fine)
+  if (fine) {
     level_sweep_kernel<TB, TV, true><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
-  else
-    level_sweep_kernel<TB, TV, false><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+  } else {
+    (void)grid;  // one warp per node (mode 2 is level-0 only)
+    coarse_warp_sweep_kernel<TV><<<(L.n + 7) / 8, 256, 0, s>>>(a, reinterpret_cast<const TV*>(b), xin, xout,
+                                                               omega, mode, st);
+  }
 }
 
 template <typename TB, typename TV>
