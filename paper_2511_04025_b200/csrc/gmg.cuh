@@ -462,8 +462,9 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
   if (fine) {
     level_sweep_kernel<TB, TV, true><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
-  } else {
-    (void)grid;  // one warp per node (mode 2 is level-0 only)
+  } else if (L.n > 32768) {  // large stored level: thread per node is throughput-bound
+    level_sweep_kernel<TB, TV, false><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+  } else {  // small stored level: latency-bound, one warp per node (mode 2 is level-0 only)
     coarse_warp_sweep_kernel<TV><<<(L.n + 7) / 8, 256, 0, s>>>(a, reinterpret_cast<const TV*>(b), xin, xout,
                                                                omega, mode, st);
   }
