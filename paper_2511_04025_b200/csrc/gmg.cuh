@@ -326,60 +326,64 @@ __device__ __forceinline__ void fine_block(const TV* __restrict__ betav, int r, 
 }
 
 // A_c(N, N+D) = sum_{n in supp N} sum_{m ~ n, m in supp(N+D)} w(n,N) A_f(n,m) w(m,N+D)
-// Same product, one WARP per coarse node N and lane d < 27 per coarse offset
-// D: the lane visits every fine pair (n in supp N, m in supp(N+D), |m-n| <= 1)
-// and keeps its 9 accumulators in registers -- no shared-memory accumulators,
-// 27-way parallel per coarse node.
+// One thread per active coarse node; 243 accumulators in shared memory.
 template <typename TV, bool kFine>
-__global__ void __launch_bounds__(256) galerkin_warp_kernel(const int* __restrict__ list_c, int n_c, int r_c,
-                                                            const int* __restrict__ map_f, int r_f,
-                                                            const TV* __restrict__ betav,
-                                                            const TV* __restrict__ stencil_f, TV ridge,
-                                                            TV* __restrict__ stencil_c) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= n_c || lane >= 27) return;
-  const int idx = warp;
+__global__ void __launch_bounds__(64) galerkin_kernel(const int* __restrict__ list_c, int n_c,
+                                                      int r_c, const int* __restrict__ map_f,
+                                                      int r_f, const TV* __restrict__ betav,
+                                                      const TV* __restrict__ stencil_f, TV ridge,
+                                                      TV* __restrict__ stencil_c) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  TV* acc = reinterpret_cast<TV*>(gsm) + threadIdx.x * kStencil;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_c) return;
+  for (int q = 0; q < kStencil; ++q) acc[q] = TV(0);
   const int G = list_c[idx];
   const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
-  const int Dx = lane % 3 - 1, Dy = (lane / 3) % 3 - 1, Dz = lane / 9 - 1;
-  TV acc[9];
-#pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] = TV(0);
   if (G != 0) {
-    for (int nn = 0; nn < 27; ++nn) {
-      const int ni = nn % 3 - 1, nj = (nn / 3) % 3 - 1, nk = nn / 9 - 1;
-      const int ux = 2 * I + ni, uy = 2 * J + nj, uz = 2 * K + nk;
-      const int fi = (ux + r_f) % r_f, fj = (uy + r_f) % r_f, fk = (uz + r_f) % r_f;
-      const size_t gn = (static_cast<size_t>(fk) * r_f + fj) * r_f + fi;
-      const int nf = map_f[gn];
-      if (nf < 0 || gn == 0) continue;
-      const TV wn = TV((ni ? 0.5 : 1.0) * (nj ? 0.5 : 1.0) * (nk ? 0.5 : 1.0));
-      for (int ee = 0; ee < 27; ++ee) {
-        const int ex = ee % 3 - 1, ey = (ee / 3) % 3 - 1, ez = ee / 9 - 1;
-        // m = 2(N+D) + e (unwrapped); its offset from n must lie in [-1,1]^3
-        const int dx = 2 * Dx + ex - ni, dy = 2 * Dy + ey - nj, dz = 2 * Dz + ez - nk;
-        if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) continue;
-        const int mi = (ux + dx + r_f) % r_f, mj = (uy + dy + r_f) % r_f, mk = (uz + dz + r_f) % r_f;
-        const size_t gm = (static_cast<size_t>(mk) * r_f + mj) * r_f + mi;
-        if (gm == 0 || map_f[gm] < 0) continue;
-        TV S[9];
-        if (kFine) {
-          fine_block<TV>(betav, r_f, fi, fj, fk, dx, dy, dz, ridge, S);
-        } else {
-          const int m = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
-          const TV* sb = stencil_f + vbase(nf, kStencil) + m * 9 * 32;
+    for (int nk = -1; nk <= 1; ++nk)
+      for (int nj = -1; nj <= 1; ++nj)
+        for (int ni = -1; ni <= 1; ++ni) {
+          // fine node n (unwrapped 2N + d) and its weight for N
+          const int ux = 2 * I + ni, uy = 2 * J + nj, uz = 2 * K + nk;
+          const int fi = (ux + r_f) % r_f, fj = (uy + r_f) % r_f, fk = (uz + r_f) % r_f;
+          const size_t gn = (static_cast<size_t>(fk) * r_f + fj) * r_f + fi;
+          const int nf = map_f[gn];
+          if (nf < 0 || gn == 0) continue;
+          const TV wn = TV((ni ? 0.5 : 1.0) * (nj ? 0.5 : 1.0) * (nk ? 0.5 : 1.0));
+          for (int m = 0; m < 27; ++m) {
+            const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+            const int vx = ux + dx, vy = uy + dy, vz = uz + dz;  // fine m, unwrapped
+            const int mi = (vx + r_f) % r_f, mj = (vy + r_f) % r_f, mk = (vz + r_f) % r_f;
+            const size_t gm = (static_cast<size_t>(mk) * r_f + mj) * r_f + mi;
+            if (gm == 0 || map_f[gm] < 0) continue;
+            TV S[9];
+            if (kFine) {
+              fine_block<TV>(betav, r_f, fi, fj, fk, dx, dy, dz, ridge, S);
+            } else {
+              const TV* sb = stencil_f + vbase(nf, kStencil);
 #pragma unroll
-          for (int q = 0; q < 9; ++q) S[q] = sb[q * 32];
+              for (int q = 0; q < 9; ++q) S[q] = sb[(m * 9 + q) * 32];
+            }
+            // coarse parents of m (unwrapped): even -> v/2, odd -> (v-1)/2, (v+1)/2
+            const int ax0 = (vx - (vx & 1)) / 2, ay0 = (vy - (vy & 1)) / 2, az0 = (vz - (vz & 1)) / 2;
+            const int nx = (vx & 1) ? 2 : 1, ny = (vy & 1) ? 2 : 1, nz = (vz & 1) ? 2 : 1;
+            const TV wm = TV(1.0 / (nx * ny * nz));
+            for (int c = 0; c < nz; ++c)
+              for (int b = 0; b < ny; ++b)
+                for (int a = 0; a < nx; ++a) {
+                  // vx in [2I-2, 2I+2] so the parent offset lies in [-1, 1]
+                  const int Dx = ax0 + a - I, Dy = ay0 + b - J, Dz = az0 + c - K;
+                  const int slot = ((Dz + 1) * 3 + (Dy + 1)) * 3 + (Dx + 1);
+                  const TV w = wn * wm;
+#pragma unroll
+                  for (int q = 0; q < 9; ++q) acc[slot * 9 + q] = fma_t(w, S[q], acc[slot * 9 + q]);
+                }
+          }
         }
-        const TV w = wn * TV((ex ? 0.5 : 1.0) * (ey ? 0.5 : 1.0) * (ez ? 0.5 : 1.0));
-#pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q] = fma_t(w, S[q], acc[q]);
-      }
-    }
   }
-  TV* out = stencil_c + vbase(idx, kStencil) + lane * 9 * 32;
-#pragma unroll
-  for (int q = 0; q < 9; ++q) out[q * 32] = acc[q];
+  TV* out = stencil_c + vbase(idx, kStencil);
+  for (int q = 0; q < kStencil; ++q) out[q * 32] = acc[q];
 }
 
 // Dinv of a stored level: inverse of the centre 3x3 block (0 for node 0 /
@@ -434,13 +438,16 @@ template <typename TV>
 void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int r_f,
                      const TV* beta_f, const TV* stencil_f, TV ridge, TV* stencil_c, cudaStream_t s) {
   if (n_c == 0) return;
-  const unsigned blocks = static_cast<unsigned>((n_c + 7) / 8);  // 8 coarse nodes (warps) per block
-  if (stencil_f == nullptr)
-    galerkin_warp_kernel<TV, true><<<blocks, 256, 0, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f, nullptr, ridge,
-                                                          stencil_c);
-  else
-    galerkin_warp_kernel<TV, false><<<blocks, 256, 0, s>>>(list_c, n_c, r_c, map_f, r_f, nullptr, stencil_f,
-                                                           ridge, stencil_c);
+  const size_t smem = 64 * kStencil * sizeof(TV);
+  if (stencil_f == nullptr) {
+    cudaFuncSetAttribute(galerkin_kernel<TV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    galerkin_kernel<TV, true><<<(n_c + 63) / 64, 64, smem, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f,
+                                                                nullptr, ridge, stencil_c);
+  } else {
+    cudaFuncSetAttribute(galerkin_kernel<TV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    galerkin_kernel<TV, false><<<(n_c + 63) / 64, 64, smem, s>>>(list_c, n_c, r_c, map_f, r_f, nullptr,
+                                                                 stencil_f, ridge, stencil_c);
+  }
 }
 
 template <typename TV>
