@@ -13,7 +13,8 @@
 //   K3 rhs_kernel      b_n = -sum_e beta_e (K0 T)_{a(e,n)}      grid_solver.hpp:141-152
 //   K4 apply_kernel    w = A z by node-centric gather (no atomics, one thread
 //                      per active node), p = z + beta p, q = w + beta q in
-//                      place (Chronopoulos-Gear PCG), partial z.w
+//                      place (single-SpMV PCG: A is applied to z, q = A p by
+//                      recurrence), partial p.q
 //   K5 update_kernel   x += alpha p, r -= alpha q, z = Dinv r, partial r.z, r.r
 //   K6 chom_kernel     C_ab = sum_e beta_e (x_e+T)_a^T K0 (x_e+T)_b        :183-197
 //
@@ -123,13 +124,12 @@ __device__ __forceinline__ void reduce_partials(const double* partials, double (
 // ---- scalar updates (shared by the last block and the cross-slab finalize) --
 __device__ void finalize_apply_state(PcgState* st, const double (&tot)[6]) {
   for (int s = 0; s < 6; ++s) {
-    st->delta[s] = tot[s];
+    st->delta[s] = tot[s];  // p.q
     if (st->done[s]) {
       st->alpha[s] = 0.0;
       continue;
     }
-    // p.Ap = delta - beta * gamma / alpha_old  (= delta on the first step)
-    const double den = st->beta[s] == 0.0 ? tot[s] : tot[s] - st->beta[s] * st->gamma[s] / st->alpha[s];
+    const double den = tot[s];  // p^T A p (grid_solver.hpp:62-63)
     if (!(den > 0.0)) st->error = 1;
     st->pap[s] = den;
     st->alpha[s] = st->gamma[s] / den;
@@ -416,7 +416,6 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
       const size_t o = ob + q * 32;
       const TV zq = zv[o];
       const TV w = g != 0 ? fma_t(ridge, zq, acc.get(q)) : TV(0);
-      dl[s] += static_cast<double>(zq) * static_cast<double>(w);
       TV pn = TV(0), qn = TV(0);
       if (!dn[s]) {
         pn = fma_t(bcoef[s], pv[o], zq);
@@ -424,6 +423,9 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
       }
       pv[o] = pn;
       qv[o] = qn;
+      // p.Ap from the updated p and q (q = A p by recurrence); more robust than
+      // the delta - beta*gamma/alpha recurrence under a strong FP32 preconditioner
+      dl[s] += static_cast<double>(pn) * static_cast<double>(qn);
     }
   }
   block_sum<6>(dl, scratch);
