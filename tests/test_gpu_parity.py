@@ -276,3 +276,18 @@ def test_gmg_vs_oracle_and_direct(S, O):
     res = S.GridSolver(om.beta, r, K0, precision="fp64", preconditioner="gmg").solve(1e-11)
     assert res.stats.gmg_levels == 2
     assert rel_max(res.tensor, ref.C) < 1e-8
+
+
+@pytest.mark.parametrize("seed", [4, 44])
+def test_fp32_ridge_keeps_ch(S, seed):
+    """Designs whose floating components stalled the FP32 multigrid iteration at
+    the FP64 ridge: the FP32-mode ridge (1e-8 mean|diag|) converges without
+    falling back, and C^H matches the FP64 solve far inside the 1e-4 bar."""
+    r = 128 if seed == 4 else 64
+    d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), seed)
+    mixed = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r,
+                         S.HomogenizeOptions(residual_tol=1e-5, precision="mixed", preconditioner="gmg"))
+    fp64 = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r,
+                        S.HomogenizeOptions(residual_tol=1e-8, precision="fp64", preconditioner="gmg"))
+    assert max(mixed.iterations) < 60
+    assert rel_fro(mixed.tensor, fp64.tensor) < 1e-6
