@@ -119,6 +119,131 @@ __global__ void __launch_bounds__(256, 3)
   }
 }
 
+// stencil_gather restricted to neighbour plane dz = PLANE-1.
+template <typename TV, int PLANE>
+__device__ __forceinline__ void stencil_gather_plane(GatherAcc<TV>& acc, int idx, int g,
+                                                     const TV* __restrict__ xv,
+                                                     const TV* __restrict__ stencil,
+                                                     const int* __restrict__ nmap, int r, int zero_slot) {
+  acc.zero();
+  if (g == 0) return;
+  const int rr = r * r;
+  const int i = g % r, j = (g / r) % r, k = g / rr;
+  const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
+  const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
+  constexpr int dz = PLANE - 1;
+  const int zl = (dz < 0 ? (k == 0 ? r - 1 : k - 1) : (dz > 0 ? (k == r - 1 ? 0 : k + 1) : k)) * rr;
+  const TV* sb = stencil + vbase(idx, kStencil);
+#pragma unroll
+  for (int mm = 0; mm < 9; ++mm) {
+    const int m = PLANE * 9 + mm;
+    const int dx = mm % 3 - 1, dy = mm / 3 - 1;
+    int nb = (m == 13) ? idx : nmap[zl + ys[dy + 1] + xs[dx + 1]];
+    nb = nb < 0 ? zero_slot : nb;
+    TV S[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) S[q] = sb[(m * 9 + q) * 32];
+    acc.add(S, xv + vbase(nb, 18));
+  }
+}
+
+// level_sweep_kernel latency-split three ways: three warps per 32 nodes, warp p
+// gathers plane dz=p-1, warp p then finishes load-case pair p (gather3_tile).
+template <typename TB, typename TV, bool kFine>
+__global__ void __launch_bounds__(192)
+    level_sweep3_kernel(const LevelArgs<TV> L, const TB* __restrict__ b, const TV* __restrict__ xin,
+                        TV* __restrict__ xout, TV omega, int mode, PcgState* st, double* partials,
+                        int init) {
+  __shared__ __align__(16) TV part_s[2][3 * 18 * 32];
+  __shared__ double scratch[32 * 6];
+  if (st->stop) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = w / 3, part = w % 3;
+  double gam2[2] = {0, 0};
+  for (int tile = blockIdx.x; tile * 64 < L.n; tile += gridDim.x) {
+    const int idx = tile * 64 + grp * 32 + lane;
+    const bool valid = idx < L.n;
+    const int g = valid ? L.node_list[idx] : -1;
+    {
+      GatherAcc<TV> acc;
+      if (!valid) {
+        acc.zero();
+      } else if (kFine) {
+        if (part == 0)
+          fine_gather_plane<TV, 0>(acc, idx, g, xin, L.beta, L.node_map, L.r, 0, L.zero_slot);
+        else if (part == 1)
+          fine_gather_plane<TV, 1>(acc, idx, g, xin, L.beta, L.node_map, L.r, 0, L.zero_slot);
+        else
+          fine_gather_plane<TV, 2>(acc, idx, g, xin, L.beta, L.node_map, L.r, 0, L.zero_slot);
+      } else {
+        if (part == 0)
+          stencil_gather_plane<TV, 0>(acc, idx, g, xin, L.stencil, L.node_map, L.r, L.zero_slot);
+        else if (part == 1)
+          stencil_gather_plane<TV, 1>(acc, idx, g, xin, L.stencil, L.node_map, L.r, L.zero_slot);
+        else
+          stencil_gather_plane<TV, 2>(acc, idx, g, xin, L.stencil, L.node_map, L.r, L.zero_slot);
+      }
+#pragma unroll
+      for (int q = 0; q < 18; ++q) part_s[grp][(part * 18 + q) * 32 + lane] = acc.get(q);
+    }
+    __syncthreads();
+    if (valid) {
+      const size_t ob = vbase(idx, 18);
+      TV D[6];
+      if (mode != 1) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int s_ = 2 * part + k;
+        TV res[3], xo[3], bb[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const size_t o = ob + (c * 6 + s_) * 32;
+          const TV xi = xin[o];
+          TV wv = gather3_sum<TV>(part_s[grp], c * 6 + s_, lane);
+          if (kFine && g != 0) wv = fma_t(L.ridge, xi, wv);
+          bb[c] = static_cast<TV>(b[o]);
+          res[c] = bb[c] - wv;
+          xo[c] = xi;
+        }
+        if (mode == 1) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s_) * 32] = g == 0 ? TV(0) : res[c];
+          continue;
+        }
+        const TV z0 = D[0] * res[0] + D[1] * res[1] + D[2] * res[2];
+        const TV z1 = D[1] * res[0] + D[3] * res[1] + D[4] * res[2];
+        const TV z2 = D[2] * res[0] + D[4] * res[1] + D[5] * res[2];
+        xo[0] = fma_t(omega, z0, xo[0]);
+        xo[1] = fma_t(omega, z1, xo[1]);
+        xo[2] = fma_t(omega, z2, xo[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          xout[ob + (c * 6 + s_) * 32] = xo[c];
+          if (mode == 2) gam2[k] += static_cast<double>(b[ob + (c * 6 + s_) * 32]) * static_cast<double>(xo[c]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (mode != 2) return;
+  double gam[6];
+#pragma unroll
+  for (int s_ = 0; s_ < 6; ++s_) gam[s_] = (s_ >> 1) == part ? gam2[s_ & 1] : 0.0;
+  block_sum<6>(gam, scratch);
+  if (publish_partial<6>(gam, partials, &st->counter_misc)) {
+    double tot[6];
+    __syncthreads();
+    reduce_partials<6>(partials, tot, scratch);
+    if (threadIdx.x == 0) {
+      finalize_gamma_state(st, tot, init);
+      st->counter_misc = 0;
+    }
+  }
+}
+
 // Stored (Galerkin) levels are small, so a per-node loop over 27 neighbours is
 // a pure dependent-load chain (~30 us per sweep regardless of size).  Here one
 // WARP owns a node and lane m < 27 owns stencil neighbour m: each lane does one
@@ -386,6 +511,121 @@ __global__ void __launch_bounds__(64) galerkin_kernel(const int* __restrict__ li
   for (int q = 0; q < kStencil; ++q) out[q * 32] = acc[q];
 }
 
+// ---- level-1 Galerkin from elements -------------------------------------
+// Inside one coarse cell the trilinear P maps the cell's 8 coarse corners onto
+// the 27 fine nodes of its 8 fine elements, so P^T A_f P restricted to the cell
+// is sum_j beta_j M_j with M_j = P_j^T K0 P_j (24x24, coarse corners in bit
+// order x + 2y + 4z).  A_1(N, N+D) is then plain element assembly over the (up
+// to 8) cells holding both N and N+D: 8 fine elements x 9 FMA per cell.  Rows
+// and columns through fine node 0 only reach coarse node 0, whose row is zero
+// and whose value is held at zero, so the operator equals the node-wise form.
+__device__ double g_cellMd[8 * 576];
+__device__ float g_cellMf[8 * 576];
+
+__device__ __forceinline__ double tri_w(int t, int cc) {  // fine offset t in {0,1,2} from corner cc
+  return t == 1 ? 0.5 : ((t == 0) == (cc == 0) ? 1.0 : 0.0);
+}
+
+__global__ void cell_matrices_kernel() {
+  const int j = blockIdx.x, e = threadIdx.x;
+  const int row = e / 24, col = e % 24;
+  const int C = row / 3, c = row % 3, C2 = col / 3, c2 = col % 3;
+  const int jx = j & 1, jy = (j >> 1) & 1, jz = (j >> 2) & 1;
+  double acc = 0.0;
+  for (int a = 0; a < 8; ++a) {
+    const int ax = a & 1, ay = (a >> 1) & 1, az = (a >> 2) & 1;
+    const double wa = tri_w(jx + ax, C & 1) * tri_w(jy + ay, (C >> 1) & 1) * tri_w(jz + az, C >> 2);
+    if (wa == 0.0) continue;
+    for (int b = 0; b < 8; ++b) {
+      const int bx = b & 1, by = (b >> 1) & 1, bz = (b >> 2) & 1;
+      const double wb = tri_w(jx + bx, C2 & 1) * tri_w(jy + by, (C2 >> 1) & 1) * tri_w(jz + bz, C2 >> 2);
+      if (wb == 0.0) continue;
+      acc += wa * wb * c_K0d[(3 * corner_id(ax, ay, az) + c) * 24 + 3 * corner_id(bx, by, bz) + c2];
+    }
+  }
+  g_cellMd[j * 576 + e] = acc;
+  g_cellMf[j * 576 + e] = static_cast<float>(acc);
+}
+
+template <typename TV>
+__device__ __forceinline__ const TV* cell_matrices();
+template <>
+__device__ __forceinline__ const double* cell_matrices<double>() { return g_cellMd; }
+template <>
+__device__ __forceinline__ const float* cell_matrices<float>() { return g_cellMf; }
+
+// block (32 coarse nodes, 27 stencil slots): thread (x, m) owns block m of node x,
+// so each stencil store is one coalesced 32-node line.
+template <typename TV>
+__global__ void __launch_bounds__(864) galerkin_fine_kernel(const int* __restrict__ list_c, int n_c, int r_c,
+                                                            const int* __restrict__ map_f, int r_f,
+                                                            const TV* __restrict__ betav, TV ridge,
+                                                            TV* __restrict__ stencil_c) {
+  __shared__ TV M[8 * 576];
+  const TV* Mg = cell_matrices<TV>();
+  for (int t = threadIdx.y * 32 + threadIdx.x; t < 8 * 576; t += 864) M[t] = Mg[t];
+  __syncthreads();
+  const int idx = blockIdx.x * 32 + threadIdx.x;
+  if (idx >= n_c) return;
+  const int m = threadIdx.y;
+  const int Dx = m % 3 - 1, Dy = (m / 3) % 3 - 1, Dz = m / 9 - 1;
+  const int G = list_c[idx];
+  TV S[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) S[q] = TV(0);
+  if (G != 0) {
+    const int rc2 = r_c * r_c;
+    const int I = G % r_c, J = (G / r_c) % r_c, K = G / rc2;
+    for (int az = 0; az < 2; ++az) {
+      const int bz = az + Dz;
+      if (bz < 0 || bz > 1) continue;
+      const int cz = 2 * ((K - az + r_c) % r_c);
+      for (int ay = 0; ay < 2; ++ay) {
+        const int by = ay + Dy;
+        if (by < 0 || by > 1) continue;
+        const int cy = 2 * ((J - ay + r_c) % r_c);
+        for (int ax = 0; ax < 2; ++ax) {
+          const int bx = ax + Dx;
+          if (bx < 0 || bx > 1) continue;
+          const int cx = 2 * ((I - ax + r_c) % r_c);
+          const int A = ax + 2 * ay + 4 * az, B = bx + 2 * by + 4 * bz;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const TV be = betav[(static_cast<size_t>(cz + (j >> 2)) * r_f + cy + ((j >> 1) & 1)) * r_f + cx + (j & 1)];
+            const TV* Mj = M + j * 576 + (3 * A) * 24 + 3 * B;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int d = 0; d < 3; ++d) S[c * 3 + d] = fma_t(be, Mj[c * 24 + d], S[c * 3 + d]);
+          }
+        }
+      }
+    }
+    if (ridge != TV(0)) {  // ridge * sum_n w(n,N) w(n,N+D) over active fine n != 0
+      TV wsum = TV(0);
+      for (int nz = -1; nz <= 1; ++nz) {
+        if (Dz != 0 && nz != Dz) continue;
+        for (int ny = -1; ny <= 1; ++ny) {
+          if (Dy != 0 && ny != Dy) continue;
+          for (int nx = -1; nx <= 1; ++nx) {
+            if (Dx != 0 && nx != Dx) continue;
+            const int fi = (2 * I + nx + r_f) % r_f, fj = (2 * J + ny + r_f) % r_f, fk = (2 * K + nz + r_f) % r_f;
+            const size_t gn = (static_cast<size_t>(fk) * r_f + fj) * r_f + fi;
+            if (gn == 0 || map_f[gn] < 0) continue;
+            wsum += TV((nx ? 0.25 : 1.0) * (ny ? 0.25 : 1.0) * (nz ? 0.25 : 1.0));
+          }
+        }
+      }
+      S[0] = fma_t(ridge, wsum, S[0]);
+      S[4] = fma_t(ridge, wsum, S[4]);
+      S[8] = fma_t(ridge, wsum, S[8]);
+    }
+  }
+  TV* out = stencil_c + vbase(idx, kStencil) + m * 9 * 32;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) out[q * 32] = S[q];
+}
+
 // Dinv of a stored level: inverse of the centre 3x3 block (0 for node 0 /
 // singular).  l1 != 0: l1-block-Jacobi -- each diagonal entry also gets the
 // row's off-block absolute sum, which makes the smoother convergent for any
@@ -439,7 +679,12 @@ void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int 
                      const TV* beta_f, const TV* stencil_f, TV ridge, TV* stencil_c, cudaStream_t s) {
   if (n_c == 0) return;
   const size_t smem = 64 * kStencil * sizeof(TV);
-  if (stencil_f == nullptr) {
+  static const bool nodewise = std::getenv("SHL_GALERKIN_NODEWISE") != nullptr;  // A/B check
+  if (stencil_f == nullptr && !nodewise) {
+    cell_matrices_kernel<<<8, 576, 0, s>>>();
+    galerkin_fine_kernel<TV><<<(n_c + 31) / 32, dim3(32, 27), 0, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f, ridge,
+                                                                      stencil_c);
+  } else if (stencil_f == nullptr) {
     cudaFuncSetAttribute(galerkin_kernel<TV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     galerkin_kernel<TV, true><<<(n_c + 63) / 64, 64, smem, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f,
                                                                 nullptr, ridge, stencil_c);
@@ -460,10 +705,13 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s) {
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
-  if (fine) {
+  static const bool one = std::getenv("SHL_APPLY1") != nullptr;  // A/B: thread-per-node kernels
+  if (fine && one) {
     level_sweep_kernel<TB, TV, true><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+  } else if (fine) {
+    level_sweep3_kernel<TB, TV, true><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
   } else if (L.n > 32768) {  // large stored level: thread per node is throughput-bound
-    level_sweep_kernel<TB, TV, false><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+    level_sweep3_kernel<TB, TV, false><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
   } else {  // small stored level: latency-bound, one warp per node (mode 2 is level-0 only)
     coarse_warp_sweep_kernel<TV><<<(L.n + 7) / 8, 256, 0, s>>>(a, reinterpret_cast<const TV*>(b), xin, xout,
                                                                omega, mode, st);

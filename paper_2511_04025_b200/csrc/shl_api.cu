@@ -301,7 +301,7 @@ int gmg_setup(shl_ctx* c, const GmgParams& gp, TV ridge) {
                              stencil_f, L == 0 ? ridge : TV(0), Lv.stencil.as<TV>(), c->stream);
     shl::launch_coarse_dinv<TV>(Lv.list.as<int>(), Lv.n, Lv.stencil.as<TV>(), Lv.dinv.as<TV>(), gp.l1,
                                 c->stream);
-    c->launches += 5;
+    c->launches += L == 0 ? 6 : 5;  // level 1 adds the cell-matrix kernel
     CK(cudaGetLastError());
     map_f = Lv.map.as<int>();
     stencil_f = Lv.stencil.as<TV>();
@@ -323,7 +323,7 @@ struct Vcycle {
   double* partials;
   int64_t launches = 0;
 
-  int grid(int n) const { return std::max(1, std::min((n + 255) / 256, c->num_sms * 3)); }
+  int grid(int n) const { return shl::apply_grid(n, c->num_sms); }
 
   TV* level(int l, const TX* b0, int init) {
     const auto& V = view[l];
@@ -382,7 +382,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   TV* dinv = q + nV;
   // update: (node block, load case) blocks; apply: grid-stride over active nodes
   const int grid_u = 6 * std::max(1, std::min((n + 255) / 256, c->num_sms * 2));
-  const int grid_a = std::max(1, std::min((n + 255) / 256, c->num_sms * (sizeof(TV) == 4 ? 3 : 2)));
+  const int grid_a = shl::apply_grid(n, c->num_sms);
   const int grid_c = std::max(1, std::min(static_cast<int>((c->n_elem + 31) / 32), c->num_sms * 16));
   c->partials.ensure(sizeof(double) *
                      std::max<size_t>({static_cast<size_t>(grid_a) * 6,

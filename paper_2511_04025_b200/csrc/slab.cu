@@ -296,7 +296,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
   };
   auto grid_u = [&](const Slab& S) { return 6 * std::max(1, std::min((S.P.n_owned + 255) / 256, c->num_sms * 2)); };
   auto grid_a = [&](const Slab& S) {
-    return std::max(1, std::min((S.P.n_owned + 255) / 256, c->num_sms * (sizeof(TV) == 4 ? 3 : 2)));
+    return apply_grid(S.P.n_owned, c->num_sms);
   };
   auto update_all = [&](int init) {
     for (int s = 0; s < nloc; ++s) {

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "solver.cuh"
@@ -383,6 +384,89 @@ __device__ __forceinline__ void fine_gather(GatherAcc<TV>& acc, int idx, int g,
   }
 }
 
+// Partial w = A x over the nine neighbours in plane dz = PLANE-1 (PLANE is a
+// compile-time constant so the K0 indices stay immediates).
+template <typename TV, int PLANE>
+__device__ __forceinline__ void fine_gather_plane(GatherAcc<TV>& acc, int idx, int g,
+                                                  const TV* __restrict__ xv,
+                                                  const TV* __restrict__ betav,
+                                                  const int* __restrict__ nmap, int r, int zbase,
+                                                  int zero_slot) {
+  acc.zero();
+  if (g == 0) return;
+  const int rr = r * r;
+  const int i = g % r, j = (g / r) % r, k = g / rr;
+  const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
+  const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
+  constexpr int dz = PLANE - 1;
+  const int kn = dz < 0 ? (k == 0 ? r - 1 : k - 1) : (dz > 0 ? (k == r - 1 ? 0 : k + 1) : k);
+  int lz = kn - zbase;
+  lz += lz < 0 ? r : 0;
+  const int zl = lz * rr;
+  // the elements shared with this plane: node corner oz with oz + dz in {0,1}
+  TV be[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
+    if (oz + dz < 0 || oz + dz > 1) {
+      be[e] = TV(0);
+      continue;
+    }
+    const int ek = oz ? (k == 0 ? r - 1 : k - 1) : k;
+    be[e] = betav[ek * rr + ys[1 - oy] + xs[1 - ox]];
+  }
+#pragma unroll
+  for (int mm = 0; mm < 9; ++mm) {
+    const int dx = mm % 3 - 1, dy = mm / 3 - 1;
+    int nb = (dx == 0 && dy == 0 && dz == 0) ? idx : nmap[zl + ys[dy + 1] + xs[dx + 1]];
+    nb = nb < 0 ? zero_slot : nb;
+    TV S[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) S[q] = TV(0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
+      const int bx = ox + dx, by = oy + dy, bz = oz + dz;
+      if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+      const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          S[c * 3 + d] = fma_t(be[e], k0<TV>((3 * a + c) * 24 + 3 * b + d), S[c * 3 + d]);
+    }
+    acc.add(S, xv + vbase(nb, 18));
+  }
+}
+
+// Three warps cooperate on 32 consecutive nodes: warp p gathers plane dz=p-1,
+// the partial sums meet in shared memory, and the caller's epilogue runs on
+// warp p for load-case pair p (s = 2p, 2p+1).  part_s: [3][18][32].
+template <typename TV>
+__device__ __forceinline__ void gather3_tile(TV* part_s, int part, int lane, int idx, bool valid,
+                                             int g, const TV* __restrict__ xv,
+                                             const TV* __restrict__ betav,
+                                             const int* __restrict__ nmap, int r, int zbase,
+                                             int zero_slot) {
+  GatherAcc<TV> acc;
+  if (!valid) {
+    acc.zero();
+  } else if (part == 0) {
+    fine_gather_plane<TV, 0>(acc, idx, g, xv, betav, nmap, r, zbase, zero_slot);
+  } else if (part == 1) {
+    fine_gather_plane<TV, 1>(acc, idx, g, xv, betav, nmap, r, zbase, zero_slot);
+  } else {
+    fine_gather_plane<TV, 2>(acc, idx, g, xv, betav, nmap, r, zbase, zero_slot);
+  }
+#pragma unroll
+  for (int q = 0; q < 18; ++q) part_s[(part * 18 + q) * 32 + lane] = acc.get(q);
+}
+
+template <typename TV>
+__device__ __forceinline__ TV gather3_sum(const TV* part_s, int q, int lane) {
+  return part_s[(0 * 18 + q) * 32 + lane] + part_s[(1 * 18 + q) * 32 + lane] + part_s[(2 * 18 + q) * 32 + lane];
+}
+
 template <typename TV>
 __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(const ApplyArgs<TV> A) {
   __shared__ double scratch[32 * 6];
@@ -436,6 +520,75 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
     if (threadIdx.x == 0) {
       if (A.defer) {
         for (int s = 0; s < 6; ++s) A.totals[s] = tot[s];
+      } else {
+        finalize_apply_state(st, tot);
+      }
+      st->counter_apply = 0;
+    }
+  }
+}
+
+// Same contract as apply_kernel, latency-split three ways (gather3_tile).
+template <typename TV>
+__global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV> A) {
+  __shared__ __align__(16) TV part_s[2][3 * 18 * 32];
+  __shared__ double scratch[32 * 6];
+  PcgState* st = A.state;
+  if (st->stop) return;
+  const TV* __restrict__ zv = A.z;
+  TV* __restrict__ pv = A.p;
+  TV* __restrict__ qv = A.q;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = w / 3, part = w % 3;
+  const TV ridge = static_cast<TV>(st->ridge);
+  bool dn[2];
+  TV bcoef[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    dn[k] = st->done[2 * part + k] != 0;
+    bcoef[k] = static_cast<TV>(st->beta[2 * part + k]);
+  }
+  double pq2[2] = {0, 0};
+  for (int tile = blockIdx.x; tile * 64 < A.n; tile += gridDim.x) {
+    const int idx = tile * 64 + grp * 32 + lane;
+    const bool valid = idx < A.n;
+    const int g = valid ? A.node_list[idx] : -1;
+    gather3_tile<TV>(part_s[grp], part, lane, idx, valid, g, zv, A.beta, A.node_map, A.r, A.zbase,
+                     A.zero_slot);
+    __syncthreads();
+    if (valid) {
+      const size_t ob = vbase(idx, 18);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int s_ = 2 * part + k, q = c * 6 + s_;
+          const size_t o = ob + q * 32;
+          const TV zq = zv[o];
+          const TV wv = g != 0 ? fma_t(ridge, zq, gather3_sum<TV>(part_s[grp], q, lane)) : TV(0);
+          TV pn = TV(0), qn = TV(0);
+          if (!dn[k]) {
+            pn = fma_t(bcoef[k], pv[o], zq);
+            qn = fma_t(bcoef[k], qv[o], wv);
+          }
+          pv[o] = pn;
+          qv[o] = qn;
+          pq2[k] += static_cast<double>(pn) * static_cast<double>(qn);
+        }
+    }
+    __syncthreads();
+  }
+  double pq[6];
+#pragma unroll
+  for (int s_ = 0; s_ < 6; ++s_) pq[s_] = (s_ >> 1) == part ? pq2[s_ & 1] : 0.0;
+  block_sum<6>(pq, scratch);
+  if (publish_partial<6>(pq, A.partials, &st->counter_apply)) {
+    double tot[6];
+    __syncthreads();
+    reduce_partials<6>(A.partials, tot, scratch);
+    if (threadIdx.x == 0) {
+      if (A.defer) {
+        for (int s_ = 0; s_ < 6; ++s_) A.totals[s_] = tot[s_];
       } else {
         finalize_apply_state(st, tot);
       }
@@ -727,8 +880,14 @@ void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double
 
 template <typename TV>
 void launch_apply(const ApplyArgs<TV>& a, int grid, cudaStream_t s) {
-  apply_kernel<TV><<<grid, 256, 0, s>>>(a);
+  if (std::getenv("SHL_APPLY1")) {  // single-warp-per-node variant (A/B checks)
+    apply_kernel<TV><<<grid, 256, 0, s>>>(a);
+    return;
+  }
+  apply3_kernel<TV><<<grid, 192, 0, s>>>(a);
 }
+
+int apply_grid(int n, int num_sms) { return std::max(1, std::min((n + 63) / 64, num_sms * 4)); }
 
 template <typename TX, typename TV>
 void launch_update(const UpdateArgs<TX, TV>& u, int grid, cudaStream_t s) {

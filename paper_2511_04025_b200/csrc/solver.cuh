@@ -119,6 +119,9 @@ void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double
                   double ridge, TX* rvec, TV* dinv, cudaStream_t s);
 template <typename TV>
 void launch_apply(const ApplyArgs<TV>& a, int grid, cudaStream_t s);
+// Grid (block count) launch_apply / launch_level_sweep use for n nodes; the
+// caller sizes its partials buffer as 6 doubles per block.
+int apply_grid(int n, int num_sms);
 template <typename TX, typename TV>
 void launch_update(const UpdateArgs<TX, TV>& u, int grid, cudaStream_t s);
 template <typename TX>
