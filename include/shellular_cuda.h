@@ -116,7 +116,8 @@ typedef struct {
   int64_t h2d_bytes;       /* host->device bytes moved by this call */
   int64_t d2h_bytes;       /* device->host bytes moved by this call */
   int32_t gmg_levels;      /* multigrid levels incl. the fine one (0 = block Jacobi) */
-  int32_t precond_fallback; /* 1: AUTO multigrid broke down, solved with block Jacobi */
+  int32_t precond_fallback; /* 1: AUTO multigrid broke down, solved with block Jacobi;
+                               2: mixed multigrid redone with the FP64-accumulated operator */
 } shl_stats;
 
 int shl_ctx_create(int device, shl_ctx** out);

@@ -359,6 +359,7 @@ class SolveStats:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     gmg_levels: int = 0
+    precond_fallback: int = 0  # 1: block-Jacobi redo, 2: FP64-operator redo (shellular_cuda.h)
 
     @classmethod
     def from_abi(cls, s: L.shl_stats) -> "SolveStats":
@@ -366,7 +367,7 @@ class SolveStats:
                    bool(s.converged), PRECISION_NAME.get(s.precision, "?"), s.n_surface,
                    s.n_elements, s.n_nodes, s.n_tiles, s.norm, s.volume_ratio,
                    bool(s.full_fallback), s.apply_ms, s.update_ms, s.apply_launches,
-                   s.kernel_launches, s.h2d_bytes, s.d2h_bytes, s.gmg_levels)
+                   s.kernel_launches, s.h2d_bytes, s.d2h_bytes, s.gmg_levels, s.precond_fallback)
 
 
 class GridSolver:

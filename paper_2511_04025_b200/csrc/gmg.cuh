@@ -626,6 +626,60 @@ __global__ void __launch_bounds__(864) galerkin_fine_kernel(const int* __restric
   for (int q = 0; q < 9; ++q) out[q * 32] = S[q];
 }
 
+// ---- Galerkin from a stored level ----------------------------------------
+// One warp per (coarse node N, stencil slot D); lane t < 27 owns fine node
+// n = 2N + off(t) of N's support and sums w(n,N) A_f(n,m) w(m,N+D) over the
+// fine stencil neighbours m of n inside supp(N+D); a butterfly sums the lanes.
+template <typename TV>
+__global__ void __launch_bounds__(256) galerkin_stored_kernel(const int* __restrict__ list_c, int n_c, int r_c,
+                                                              const int* __restrict__ map_f, int r_f,
+                                                              const TV* __restrict__ stencil_f,
+                                                              TV* __restrict__ stencil_c) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n_c * 27) return;  // whole warps exit together
+  const int idx = warp / 27, slot = warp % 27;
+  const int Dx = slot % 3 - 1, Dy = (slot / 3) % 3 - 1, Dz = slot / 9 - 1;
+  const int G = list_c[idx];
+  TV S[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) S[q] = TV(0);
+  if (G != 0 && lane < 27) {
+    const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
+    const int nx = lane % 3 - 1, ny = (lane / 3) % 3 - 1, nz = lane / 9 - 1;
+    const int fi = (2 * I + nx + r_f) % r_f, fj = (2 * J + ny + r_f) % r_f, fk = (2 * K + nz + r_f) % r_f;
+    const size_t gn = (static_cast<size_t>(fk) * r_f + fj) * r_f + fi;
+    const int nf = map_f[gn];
+    if (nf >= 0 && gn != 0) {
+      const TV wn = TV((nx ? 0.5 : 1.0) * (ny ? 0.5 : 1.0) * (nz ? 0.5 : 1.0));
+      const TV* sb = stencil_f + vbase(nf, kStencil);
+#pragma unroll 1
+      for (int m = 0; m < 27; ++m) {
+        const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+        // m relative to 2(N+D): must lie in [-1, 1] on every axis
+        const int ex = nx + dx - 2 * Dx, ey = ny + dy - 2 * Dy, ez = nz + dz - 2 * Dz;
+        if (ex < -1 || ex > 1 || ey < -1 || ey > 1 || ez < -1 || ez > 1) continue;
+        const int mi = (fi + dx + r_f) % r_f, mj = (fj + dy + r_f) % r_f, mk = (fk + dz + r_f) % r_f;
+        const size_t gm = (static_cast<size_t>(mk) * r_f + mj) * r_f + mi;
+        if (gm == 0 || map_f[gm] < 0) continue;
+        const TV w = wn * TV((ex ? 0.5 : 1.0) * (ey ? 0.5 : 1.0) * (ez ? 0.5 : 1.0));
+#pragma unroll
+        for (int q = 0; q < 9; ++q) S[q] = fma_t(w, sb[(m * 9 + q) * 32], S[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) S[q] += __shfl_xor_sync(0xffffffffu, S[q], o);
+  if (lane < 9) {
+    TV v = S[0];
+#pragma unroll
+    for (int q = 1; q < 9; ++q)
+      if (lane == q) v = S[q];
+    stencil_c[vbase(idx, kStencil) + (slot * 9 + lane) * 32] = v;
+  }
+}
+
 // Dinv of a stored level: inverse of the centre 3x3 block (0 for node 0 /
 // singular).  l1 != 0: l1-block-Jacobi -- each diagonal entry also gets the
 // row's off-block absolute sum, which makes the smoother convergent for any
@@ -684,6 +738,10 @@ void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int 
     cell_matrices_kernel<<<8, 576, 0, s>>>();
     galerkin_fine_kernel<TV><<<(n_c + 31) / 32, dim3(32, 27), 0, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f, ridge,
                                                                       stencil_c);
+  } else if (!nodewise) {
+    const long long threads = static_cast<long long>(n_c) * 27 * 32;
+    galerkin_stored_kernel<TV><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(list_c, n_c, r_c, map_f,
+                                                                                            r_f, stencil_f, stencil_c);
   } else if (stencil_f == nullptr) {
     cudaFuncSetAttribute(galerkin_kernel<TV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     galerkin_kernel<TV, true><<<(n_c + 63) / 64, 64, smem, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f,

@@ -248,6 +248,8 @@ struct GmgParams {
   int max_levels = 8;
   double omega_c = 0.6;    // damping on the stored (Galerkin) levels
   int l1 = 0;              // l1-block-Jacobi on the stored levels
+  int nu0 = 0;             // level-0 sweeps when > 0 (else nu)
+  int nu_at(int l) const { return (l == 0 && nu0 > 0) ? nu0 : nu; }
 };
 
 GmgParams gmg_params() {
@@ -259,6 +261,7 @@ GmgParams gmg_params() {
   if (const char* e = std::getenv("SHL_GMG_LEVELS")) g.max_levels = std::atoi(e);
   if (const char* e = std::getenv("SHL_GMG_OMEGA_C")) g.omega_c = std::atof(e);
   if (const char* e = std::getenv("SHL_GMG_L1")) g.l1 = std::atoi(e);
+  if (const char* e = std::getenv("SHL_GMG_NU0")) g.nu0 = std::max(1, std::atoi(e));
   return g;
 }
 
@@ -343,7 +346,8 @@ struct Vcycle {
       shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, c->stream);
       ++launches;
     }  // level 0: the update kernel already wrote w Dinv r into xa[0]
-    const int pre = (l == L) ? gp.coarse_sweeps : gp.nu;  // coarsest: damped Jacobi solve
+    const int nu = gp.nu_at(l);
+    const int pre = (l == L) ? gp.coarse_sweeps : nu;  // coarsest: damped Jacobi solve
     for (int k = 1; k < pre; ++k) {
       sweep(cur, oth, 0);
       std::swap(cur, oth);
@@ -354,17 +358,18 @@ struct Vcycle {
     TV* xc = level(l + 1, b0, init);
     shl::launch_prolong<TV>(V, view[l + 1], xc, cur, st, c->stream);
     launches += 2;
-    for (int k = 1; k <= gp.nu; ++k) {
-      sweep(cur, oth, (fine && k == gp.nu) ? 2 : 0);
+    for (int k = 1; k <= nu; ++k) {
+      sweep(cur, oth, (fine && k == nu) ? 2 : 0);
       std::swap(cur, oth);
     }
     return cur;
   }
 };
 
-template <typename TX, typename TV>
+// TX: x, r; TV: p, q and the operator; TZ: z and the V-cycle (solver.cuh).
+template <typename TX, typename TV, typename TZ>
 void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
-               shl_stats* st, int prec) {
+               shl_stats* st, int prec, bool use_gmg) {
   const int r = c->r;
   if (!c->node0_active)
     throw ShlError(SHL_SOLVER,
@@ -373,13 +378,13 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   // 32-node blocked vectors (solver.cu vbase); node n is an always-zero row
   const int ld = round_up(n + 1, 32);
   const size_t nX = static_cast<size_t>(18) * ld, nV = nX;
-  c->vec.ensure(2 * nX * sizeof(TX) + (3 * nV + 6 * static_cast<size_t>(ld)) * sizeof(TV));
+  c->vec.ensure(2 * nX * sizeof(TX) + 2 * nV * sizeof(TV) + (nV + 6 * static_cast<size_t>(ld)) * sizeof(TZ));
   TX* x = c->vec.as<TX>();
   TX* rv = x + nX;
-  TV* z = reinterpret_cast<TV*>(rv + nX);
-  TV* p = z + nV;
+  TV* p = reinterpret_cast<TV*>(rv + nX);
   TV* q = p + nV;
-  TV* dinv = q + nV;
+  TZ* z = reinterpret_cast<TZ*>(q + nV);
+  TZ* dinv = z + nV;
   // update: (node block, load case) blocks; apply: grid-stride over active nodes
   const int grid_u = 6 * std::max(1, std::min((n + 255) / 256, c->num_sms * 2));
   const int grid_a = shl::apply_grid(n, c->num_sms);
@@ -402,36 +407,39 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   // still FP32-resolution-small: C^H moves by < 1e-7 relative (tests compare
   // against FP64).  Every K0 diagonal entry is equal, so
   // mean diag = K0[0] * (8 sum beta) / n_nodes.
-  const double ridge_rel = sizeof(TV) == 8 ? 1e-11 : 1e-8;
-  const double ridge = n > 0 ? ridge_rel * std::fabs(K0[0]) * 8.0 * c->beta_sum / double(n) : 0.0;
+  static const char* ridge_env = std::getenv("SHL_RIDGE_REL");  // dev aid
+  // the operator PCG solves uses the Krylov type's ridge; the preconditioner
+  // (block Jacobi / V-cycle) the ridge of its own storage type
+  const double diag_mean = n > 0 ? std::fabs(K0[0]) * 8.0 * c->beta_sum / double(n) : 0.0;
+  const double ridge_op = diag_mean * (ridge_env ? std::atof(ridge_env) : (sizeof(TV) == 8 ? 1e-11 : 1e-8));
+  const double ridge = diag_mean * (ridge_env ? std::atof(ridge_env) : (sizeof(TZ) == 8 ? 1e-11 : 1e-8));
   CK(cudaEventRecord(c->ev[3], c->stream));
   shl::upload_element_constants(K0, W, T, c->stream);
   CK(cudaMemsetAsync(x, 0, nX * sizeof(TX), c->stream));
-  CK(cudaMemsetAsync(z, 0, 3 * nV * sizeof(TV), c->stream));
-  shl::launch_setup<TX, TV>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), ridge, rv,
+  CK(cudaMemsetAsync(p, 0, 2 * nV * sizeof(TV), c->stream));
+  CK(cudaMemsetAsync(z, 0, nV * sizeof(TZ), c->stream));
+  shl::launch_setup<TX, TZ>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), ridge, rv,
                             dinv, c->stream);
-  Vcycle<TX, TV> vc{c, gmg_params()};
-  const bool use_gmg = opt.preconditioner == SHL_PRECOND_GMG ||
-                       (opt.preconditioner == SHL_PRECOND_AUTO && r % 2 == 0 && r / 2 >= vc.gp.min_r);
+  Vcycle<TX, TZ> vc{c, gmg_params()};
   if (use_gmg) {
-    vc.L = gmg_setup<TV>(c, vc.gp, static_cast<TV>(ridge));
+    vc.L = gmg_setup<TZ>(c, vc.gp, static_cast<TZ>(ridge));
     if (vc.L == 0) throw ShlError(SHL_VALIDATION, "multigrid needs r divisible by 2 with r/2 >= 8");
-    c->gmg0.ensure(static_cast<size_t>(3) * nV * sizeof(TV));
-    CK(cudaMemsetAsync(c->gmg0.p, 0, static_cast<size_t>(3) * nV * sizeof(TV), c->stream));
-    const TV* beta_v = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
-                                       : reinterpret_cast<const TV*>(c->beta32.p);
+    c->gmg0.ensure(static_cast<size_t>(3) * nV * sizeof(TZ));
+    CK(cudaMemsetAsync(c->gmg0.p, 0, static_cast<size_t>(3) * nV * sizeof(TZ), c->stream));
+    const TZ* beta_v = sizeof(TZ) == 8 ? reinterpret_cast<const TZ*>(c->beta64.p)
+                                       : reinterpret_cast<const TZ*>(c->beta32.p);
     vc.view.push_back({c->node_list.as<int>(), c->node_map.as<int>(), beta_v, nullptr, dinv, r, n, n,
-                       static_cast<TV>(ridge)});
-    TV* g0 = c->gmg0.as<TV>();
+                       static_cast<TZ>(ridge)});
+    TZ* g0 = c->gmg0.as<TZ>();
     vc.b.push_back(nullptr);
     vc.xa.push_back(g0);
     vc.xb.push_back(g0 + nV);
     vc.res.push_back(g0 + 2 * nV);
     for (int l = 0; l < vc.L; ++l) {
       auto& Lv = c->gmg[l];
-      vc.view.push_back({Lv.list.as<int>(), Lv.map.as<int>(), nullptr, Lv.stencil.as<TV>(), Lv.dinv.as<TV>(),
-                         Lv.r, Lv.n, Lv.n, TV(0)});
-      TV* v = Lv.vec.as<TV>();
+      vc.view.push_back({Lv.list.as<int>(), Lv.map.as<int>(), nullptr, Lv.stencil.as<TZ>(), Lv.dinv.as<TZ>(),
+                         Lv.r, Lv.n, Lv.n, TZ(0)});
+      TZ* v = Lv.vec.as<TZ>();
       const size_t s18 = static_cast<size_t>(18) * Lv.ld;
       vc.b.push_back(v);
       vc.xa.push_back(v + s18);
@@ -442,7 +450,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   }
   shl::PcgState hs{};
   hs.tol = opt.tol;
-  hs.ridge = ridge;
+  hs.ridge = ridge_op;
   hs.max_iter = opt.max_iter > 0 ? opt.max_iter : 20 * r + 2000;
   std::memcpy(c->hstate, &hs, sizeof(hs));
   c->h2d += sizeof(hs) + 576 * 12 + 144 * 16;  // state + element constants
@@ -452,10 +460,10 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   shl::PcgState* dst = c->state.as<shl::PcgState>();
   const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
                                          : reinterpret_cast<const TV*>(c->beta32.p);
-  shl::UpdateArgs<TX, TV> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1,
-                            nullptr, 0, use_gmg ? 1 : 0, use_gmg ? vc.xa[0] : nullptr,
-                            static_cast<TV>(vc.gp.omega)};
-  shl::ApplyArgs<TV> aa{c->node_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p, q,
+  shl::UpdateArgs<TX, TV, TZ> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1,
+                                nullptr, 0, use_gmg ? 1 : 0, use_gmg ? vc.xa[0] : nullptr,
+                                static_cast<TZ>(vc.gp.omega)};
+  shl::ApplyArgs<TV, TZ> aa{c->node_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p, q,
                         c->partials.as<double>(), dst, r, n, ld, n, 0, r, nullptr, 0};
   vc.st = dst;
   // z = M r: block Jacobi inside the update kernel, or the V-cycle
@@ -463,12 +471,14 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
     if (use_gmg) aa.z = vc.level(0, rv, init);
   };
   // z0 = M b, then w0 = A z0, p0 = z0, q0 = w0, alpha0
-  shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+  shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
   precondition(1);
-  shl::launch_apply<TV>(aa, grid_a, c->stream);
+  shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
   ua.init = 0;
   int64_t launches = 2 + 2;
   int check = opt.check_every > 0 ? opt.check_every : (n < 200000 ? 16 : 32);
+  static const bool trace = std::getenv("SHL_TRACE") != nullptr;  // dev aid: per-iteration scalars
+  if (trace) check = 1;
   double apply_ms = 0.0, update_ms = 0.0;
   int64_t apply_launches = 0;
   int64_t issued = 0;
@@ -482,15 +492,15 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
           c->prof_ev.push_back(e);
         }
         CK(cudaEventRecord(c->prof_ev[3 * issued], c->stream));
-        shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+        shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
         precondition(0);
         CK(cudaEventRecord(c->prof_ev[3 * issued + 1], c->stream));
-        shl::launch_apply<TV>(aa, grid_a, c->stream);
+        shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
         CK(cudaEventRecord(c->prof_ev[3 * issued + 2], c->stream));
       } else {
-        shl::launch_update<TX, TV>(ua, grid_u, c->stream);
+        shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
         precondition(0);
-        shl::launch_apply<TV>(aa, grid_a, c->stream);
+        shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
       }
       ++issued;
       launches += 2;
@@ -500,6 +510,14 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
     CK(cudaMemcpyAsync(c->hstate, c->state.p, sizeof(shl::PcgState), cudaMemcpyDeviceToHost,
                        c->stream));
     c->sync();
+    if (trace) {
+      const shl::PcgState& h = *c->hstate;
+      std::fprintf(stderr, "it %3d", h.it);
+      for (int q = 0; q < 6; ++q)
+        std::fprintf(stderr, " | r %.2e g %+.2e pAp %+.2e", h.bnorm[q] > 0 ? std::sqrt(h.rr[q]) / h.bnorm[q] : 0.0,
+                     h.gamma[q], h.pap[q]);
+      std::fprintf(stderr, "\n");
+    }
     if (c->hstate->stop) break;
   }
   if (c->profiling) {
@@ -561,13 +579,40 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   }
 }
 
+bool is_breakdown(const ShlError& e) {
+  return e.code == SHL_SOLVER && std::string(e.what()).find("positive definiteness") != std::string::npos;
+}
+
 void solve_dispatch_once(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
                          shl_stats* st) {
   const int prec = resolve_precision(opt);
+  const int r = c->r;
+  const bool gmg = opt.preconditioner == SHL_PRECOND_GMG ||
+                   (opt.preconditioner == SHL_PRECOND_AUTO && r % 2 == 0 && r / 2 >= gmg_params().min_r);
   switch (prec) {
-    case SHL_PREC_FP64: run_solve<double, double>(c, K0, opt, C_out, st, prec); break;
-    case SHL_PREC_MIXED: run_solve<double, float>(c, K0, opt, C_out, st, prec); break;
-    default: run_solve<float, float>(c, K0, opt, C_out, st, prec); break;
+    case SHL_PREC_FP64: run_solve<double, double, double>(c, K0, opt, C_out, st, prec, gmg); break;
+    case SHL_PREC_MIXED: {
+      // FP32 operator first.  With the FP32 V-cycle, FP32 rounding of A p can
+      // swamp the ridge-sized curvature of a voxel shell's hinge modes (elements
+      // sharing only an edge or a corner) and p^T A p loses its sign; such a
+      // solve is redone with FP64 Krylov vectors and an FP64-accumulated
+      // operator (TV = double, TZ = float), which keeps the reference's 1e-11
+      // ridge and converges in the FP64 iteration count.
+      static const bool op64 = std::getenv("SHL_MIXED_OP64") != nullptr;  // A/B: always FP64 operator
+      if (gmg && op64) {
+        run_solve<double, double, float>(c, K0, opt, C_out, st, prec, gmg);
+        break;
+      }
+      try {
+        run_solve<double, float, float>(c, K0, opt, C_out, st, prec, gmg);
+      } catch (const ShlError& e) {
+        if (!gmg || !is_breakdown(e)) throw;
+        run_solve<double, double, float>(c, K0, opt, C_out, st, prec, gmg);
+        if (st) st->precond_fallback = 2;
+      }
+      break;
+    }
+    default: run_solve<float, float, float>(c, K0, opt, C_out, st, prec, gmg); break;
   }
 }
 
@@ -581,8 +626,7 @@ void solve_dispatch(shl_ctx* c, const double* K0, const shl_solve_options& opt, 
   try {
     solve_dispatch_once(c, K0, opt, C_out, st);
   } catch (const ShlError& e) {
-    if (e.code != SHL_SOLVER || std::string(e.what()).find("positive definiteness") == std::string::npos)
-      throw;
+    if (!is_breakdown(e)) throw;
     shl_solve_options jo = opt;
     jo.preconditioner = SHL_PRECOND_JACOBI;
     solve_dispatch_once(c, K0, jo, C_out, st);

@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "device.cuh"
 #include "solver.cuh"
@@ -313,7 +314,8 @@ struct GatherAcc<double> {
 #pragma unroll
     for (int q = 0; q < 18; ++q) y[q] = 0.0;
   }
-  __device__ __forceinline__ void add(const double (&S)[9], const double* __restrict__ zn) {
+  template <typename TZ>
+  __device__ __forceinline__ void add(const double (&S)[9], const TZ* __restrict__ zn) {
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const double z0 = zn[(0 * 6 + s) * 32], z1 = zn[(1 * 6 + s) * 32], z2 = zn[(2 * 6 + s) * 32];
@@ -328,6 +330,33 @@ struct GatherAcc<double> {
     }
   }
   __device__ __forceinline__ double get(int q) const { return y[q]; }
+};
+
+// FP64 accumulator for three load cases (3h .. 3h+2): the six-warp apply
+// splits the load cases in halves to keep the FP64 register footprint small.
+struct GatherAccHalf {
+  double y[9];  // [comp][load case in half]
+  int off;      // 3h * 32: first load case of the half
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) y[q] = 0.0;
+  }
+  template <typename TZ>
+  __device__ __forceinline__ void add(const double (&S)[9], const TZ* __restrict__ zn) {
+    zn += off;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const double z0 = zn[(0 * 6 + s) * 32], z1 = zn[(1 * 6 + s) * 32], z2 = zn[(2 * 6 + s) * 32];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double v = y[c * 3 + s];
+        v = fma(S[c * 3 + 0], z0, v);
+        v = fma(S[c * 3 + 1], z1, v);
+        v = fma(S[c * 3 + 2], z2, v);
+        y[c * 3 + s] = v;
+      }
+    }
+  }
 };
 
 // w = A x at active node idx (grid id g): the matrix-free level-0 operator.
@@ -386,9 +415,9 @@ __device__ __forceinline__ void fine_gather(GatherAcc<TV>& acc, int idx, int g,
 
 // Partial w = A x over the nine neighbours in plane dz = PLANE-1 (PLANE is a
 // compile-time constant so the K0 indices stay immediates).
-template <typename TV, int PLANE>
-__device__ __forceinline__ void fine_gather_plane(GatherAcc<TV>& acc, int idx, int g,
-                                                  const TV* __restrict__ xv,
+template <typename TV, int PLANE, typename TZ, typename Acc>
+__device__ __forceinline__ void fine_gather_plane(Acc& acc, int idx, int g,
+                                                  const TZ* __restrict__ xv,
                                                   const TV* __restrict__ betav,
                                                   const int* __restrict__ nmap, int r, int zbase,
                                                   int zero_slot) {
@@ -442,9 +471,9 @@ __device__ __forceinline__ void fine_gather_plane(GatherAcc<TV>& acc, int idx, i
 // Three warps cooperate on 32 consecutive nodes: warp p gathers plane dz=p-1,
 // the partial sums meet in shared memory, and the caller's epilogue runs on
 // warp p for load-case pair p (s = 2p, 2p+1).  part_s: [3][18][32].
-template <typename TV>
+template <typename TV, typename TZ>
 __device__ __forceinline__ void gather3_tile(TV* part_s, int part, int lane, int idx, bool valid,
-                                             int g, const TV* __restrict__ xv,
+                                             int g, const TZ* __restrict__ xv,
                                              const TV* __restrict__ betav,
                                              const int* __restrict__ nmap, int r, int zbase,
                                              int zero_slot) {
@@ -529,13 +558,13 @@ __global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(con
 }
 
 // Same contract as apply_kernel, latency-split three ways (gather3_tile).
-template <typename TV>
-__global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV> A) {
+template <typename TV, typename TZ>
+__global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV, TZ> A) {
   __shared__ __align__(16) TV part_s[2][3 * 18 * 32];
   __shared__ double scratch[32 * 6];
   PcgState* st = A.state;
   if (st->stop) return;
-  const TV* __restrict__ zv = A.z;
+  const TZ* __restrict__ zv = A.z;
   TV* __restrict__ pv = A.p;
   TV* __restrict__ qv = A.q;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -553,8 +582,8 @@ __global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV> A) {
     const int idx = tile * 64 + grp * 32 + lane;
     const bool valid = idx < A.n;
     const int g = valid ? A.node_list[idx] : -1;
-    gather3_tile<TV>(part_s[grp], part, lane, idx, valid, g, zv, A.beta, A.node_map, A.r, A.zbase,
-                     A.zero_slot);
+    gather3_tile<TV, TZ>(part_s[grp], part, lane, idx, valid, g, zv, A.beta, A.node_map, A.r, A.zbase,
+                         A.zero_slot);
     __syncthreads();
     if (valid) {
       const size_t ob = vbase(idx, 18);
@@ -564,7 +593,7 @@ __global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV> A) {
         for (int k = 0; k < 2; ++k) {
           const int s_ = 2 * part + k, q = c * 6 + s_;
           const size_t o = ob + q * 32;
-          const TV zq = zv[o];
+          const TV zq = static_cast<TV>(zv[o]);
           const TV wv = g != 0 ? fma_t(ridge, zq, gather3_sum<TV>(part_s[grp], q, lane)) : TV(0);
           TV pn = TV(0), qn = TV(0);
           if (!dn[k]) {
@@ -597,14 +626,92 @@ __global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV> A) {
   }
 }
 
+// FP64 operator: six warps per 32 nodes, warp (plane p, half h) gathers plane
+// dz=p-1 for load cases 3h..3h+2, then finishes load case s = 3h + p.
+template <typename TZ>
+__global__ void __launch_bounds__(384, sizeof(TZ) == 4 ? 2 : 1) apply6_kernel(const ApplyArgs<double, TZ> A) {
+  __shared__ __align__(16) double part_s[2][3 * 18 * 32];
+  __shared__ double scratch[32 * 6];
+  PcgState* st = A.state;
+  if (st->stop) return;
+  const TZ* __restrict__ zv = A.z;
+  double* __restrict__ pv = A.p;
+  double* __restrict__ qv = A.q;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = w / 6, plane = w % 3, half = (w % 6) / 3;
+  const int s_ = 3 * half + plane;  // epilogue load case
+  const double ridge = st->ridge;
+  const bool dn = st->done[s_] != 0;
+  const double bcoef = st->beta[s_];
+  double pq = 0.0;
+  for (int tile = blockIdx.x; tile * 64 < A.n; tile += gridDim.x) {
+    const int idx = tile * 64 + grp * 32 + lane;
+    const bool valid = idx < A.n;
+    const int g = valid ? A.node_list[idx] : -1;
+    {
+      GatherAccHalf acc;
+      acc.off = 3 * half * 32;
+      if (!valid)
+        acc.zero();
+      else if (plane == 0)
+        fine_gather_plane<double, 0>(acc, idx, g, zv, A.beta, A.node_map, A.r, A.zbase, A.zero_slot);
+      else if (plane == 1)
+        fine_gather_plane<double, 1>(acc, idx, g, zv, A.beta, A.node_map, A.r, A.zbase, A.zero_slot);
+      else
+        fine_gather_plane<double, 2>(acc, idx, g, zv, A.beta, A.node_map, A.r, A.zbase, A.zero_slot);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) part_s[grp][(plane * 18 + c * 6 + 3 * half + k) * 32 + lane] = acc.y[c * 3 + k];
+    }
+    __syncthreads();
+    if (valid) {
+      const size_t ob = vbase(idx, 18);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int q = c * 6 + s_;
+        const size_t o = ob + q * 32;
+        const double zq = static_cast<double>(zv[o]);
+        const double wv = g != 0 ? fma(ridge, zq, gather3_sum<double>(part_s[grp], q, lane)) : 0.0;
+        double pn = 0.0, qn = 0.0;
+        if (!dn) {
+          pn = fma(bcoef, pv[o], zq);
+          qn = fma(bcoef, qv[o], wv);
+        }
+        pv[o] = pn;
+        qv[o] = qn;
+        pq += pn * qn;
+      }
+    }
+    __syncthreads();
+  }
+  double pq6[6];
+#pragma unroll
+  for (int t = 0; t < 6; ++t) pq6[t] = t == s_ ? pq : 0.0;
+  block_sum<6>(pq6, scratch);
+  if (publish_partial<6>(pq6, A.partials, &st->counter_apply)) {
+    double tot[6];
+    __syncthreads();
+    reduce_partials<6>(A.partials, tot, scratch);
+    if (threadIdx.x == 0) {
+      if (A.defer) {
+        for (int t = 0; t < 6; ++t) A.totals[t] = tot[t];
+      } else {
+        finalize_apply_state(st, tot);
+      }
+      st->counter_apply = 0;
+    }
+  }
+}
+
 // ---- K5: vector update + preconditioner + dots ------------------------------
 //   x += alpha p, r -= alpha q, z = Dinv r, partial r.r and r.z
 // One thread per (node, load case): 3 components of x, r, p, q, z and the 6
 // Dinv entries -> ~30 registers, full occupancy, every access a coalesced
 // 32-node plane segment.  blockIdx.x = node_block * 6 + s so the six blocks
 // of a node block run together and Dinv is re-read from L2, not DRAM.
-template <typename TX, typename TV>
-__global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U) {
+template <typename TX, typename TV, typename TZ>
+__global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV, TZ> U) {
   __shared__ double scratch[32 * 2];
   PcgState* st = U.state;
   if (st->stop) return;
@@ -612,8 +719,8 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
   TX* __restrict__ rv = U.r;
   const TV* __restrict__ pv = U.p;
   const TV* __restrict__ qv = U.q;
-  TV* __restrict__ zv = U.z;
-  const TV* __restrict__ dv = U.dinv;
+  TZ* __restrict__ zv = U.z;
+  const TZ* __restrict__ dv = U.dinv;
   const int s = blockIdx.x % 6;
   const int nbx = gridDim.x / 6;
   const TX a = static_cast<TX>(st->alpha[s]);
@@ -623,7 +730,8 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
     const size_t od = vbase(idx, 6);
     // all loads first (keeps ~15 independent requests in flight per thread)
     TX xc[3], rc[3];
-    TV pc[3], qc[3], D[6] = {};
+    TV pc[3], qc[3];
+    TZ D[6] = {};
 #pragma unroll
     for (int c = 0; c < 3; ++c) rc[c] = rv[ob + c * 192];
     if (!U.init) {
@@ -656,18 +764,18 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV> U)
         }
       }
       if (U.gmg_x0) {  // fused first smoothing sweep of the V-cycle (x = w Dinv r)
-        const TV r0 = static_cast<TV>(rc[0]), r1 = static_cast<TV>(rc[1]), r2 = static_cast<TV>(rc[2]);
-        const TV w = U.gmg_omega;
+        const TZ r0 = static_cast<TZ>(rc[0]), r1 = static_cast<TZ>(rc[1]), r2 = static_cast<TZ>(rc[2]);
+        const TZ w = U.gmg_omega;
         U.gmg_x0[ob + 0 * 192] = w * (D[0] * r0 + D[1] * r1 + D[2] * r2);
         U.gmg_x0[ob + 1 * 192] = w * (D[1] * r0 + D[3] * r1 + D[4] * r2);
         U.gmg_x0[ob + 2 * 192] = w * (D[2] * r0 + D[4] * r1 + D[5] * r2);
       }
       continue;
     }
-    const TV r0 = static_cast<TV>(rc[0]), r1 = static_cast<TV>(rc[1]), r2 = static_cast<TV>(rc[2]);
-    const TV z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
-    const TV z1 = D[1] * r0 + D[3] * r1 + D[4] * r2;
-    const TV z2 = D[2] * r0 + D[4] * r1 + D[5] * r2;
+    const TZ r0 = static_cast<TZ>(rc[0]), r1 = static_cast<TZ>(rc[1]), r2 = static_cast<TZ>(rc[2]);
+    const TZ z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
+    const TZ z1 = D[1] * r0 + D[3] * r1 + D[4] * r2;
+    const TZ z2 = D[2] * r0 + D[4] * r1 + D[5] * r2;
     if (!U.init) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -878,20 +986,30 @@ void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double
                                                             ridge, rvec, dinv);
 }
 
-template <typename TV>
-void launch_apply(const ApplyArgs<TV>& a, int grid, cudaStream_t s) {
-  if (std::getenv("SHL_APPLY1")) {  // single-warp-per-node variant (A/B checks)
-    apply_kernel<TV><<<grid, 256, 0, s>>>(a);
-    return;
+template <typename TV, typename TZ>
+void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s) {
+  if constexpr (std::is_same<TV, TZ>::value) {
+    static const bool one = std::getenv("SHL_APPLY1") != nullptr;  // thread-per-node variant (A/B checks)
+    if (one) {
+      apply_kernel<TV><<<grid, 256, 0, s>>>(a);
+      return;
+    }
   }
-  apply3_kernel<TV><<<grid, 192, 0, s>>>(a);
+  if constexpr (sizeof(TV) == 8) {
+    static const bool three = std::getenv("SHL_APPLY3") != nullptr;  // A/B: three-warp FP64 variant
+    if (!three) {
+      apply6_kernel<TZ><<<grid, 384, 0, s>>>(a);
+      return;
+    }
+  }
+  apply3_kernel<TV, TZ><<<grid, 192, 0, s>>>(a);
 }
 
 int apply_grid(int n, int num_sms) { return std::max(1, std::min((n + 63) / 64, num_sms * 4)); }
 
-template <typename TX, typename TV>
-void launch_update(const UpdateArgs<TX, TV>& u, int grid, cudaStream_t s) {
-  update_kernel<TX, TV><<<grid, 256, 0, s>>>(u);
+template <typename TX, typename TV, typename TZ>
+void launch_update(const UpdateArgs<TX, TV, TZ>& u, int grid, cudaStream_t s) {
+  update_kernel<TX, TV, TZ><<<grid, 256, 0, s>>>(u);
 }
 
 template <typename TX>
@@ -905,11 +1023,13 @@ template void launch_setup<double, float>(const int*, int, int, int, const doubl
                                           float*, cudaStream_t);
 template void launch_setup<float, float>(const int*, int, int, int, const double*, double, float*,
                                          float*, cudaStream_t);
-template void launch_apply<double>(const ApplyArgs<double>&, int, cudaStream_t);
-template void launch_apply<float>(const ApplyArgs<float>&, int, cudaStream_t);
-template void launch_update<double, double>(const UpdateArgs<double, double>&, int, cudaStream_t);
-template void launch_update<double, float>(const UpdateArgs<double, float>&, int, cudaStream_t);
-template void launch_update<float, float>(const UpdateArgs<float, float>&, int, cudaStream_t);
+template void launch_apply<double, double>(const ApplyArgs<double, double>&, int, cudaStream_t);
+template void launch_apply<double, float>(const ApplyArgs<double, float>&, int, cudaStream_t);
+template void launch_apply<float, float>(const ApplyArgs<float, float>&, int, cudaStream_t);
+template void launch_update<double, double, double>(const UpdateArgs<double, double>&, int, cudaStream_t);
+template void launch_update<double, double, float>(const UpdateArgs<double, double, float>&, int, cudaStream_t);
+template void launch_update<double, float, float>(const UpdateArgs<double, float>&, int, cudaStream_t);
+template void launch_update<float, float, float>(const UpdateArgs<float, float>&, int, cudaStream_t);
 template void launch_chom<double>(const ChomArgs<double>&, int, cudaStream_t);
 template void launch_chom<float>(const ChomArgs<float>&, int, cudaStream_t);
 

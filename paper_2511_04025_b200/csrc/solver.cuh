@@ -10,12 +10,16 @@
 
 namespace shl {
 
-template <typename TV>
+// TV: Krylov vectors p, q and the operator arithmetic; TZ: the preconditioned
+// residual z (the multigrid V-cycle's type).  Mixed multigrid runs TV = double
+// with TZ = float: w = A z is accumulated in FP64 from the FP32 z, so p^T A p
+// keeps its sign on the near-null hinge modes of voxel shells.
+template <typename TV, typename TZ = TV>
 struct ApplyArgs {
   const int* node_list;  // active node -> grid id
   const int* node_map;   // r^3 -> active node id or -1
   const TV* beta;        // r^3 dense, 0 = absent
-  const TV* z;           // 18 planes, slot n is a zero row
+  const TZ* z;           // 18 planes, slot n is a zero row
   TV* p;
   TV* q;
   double* partials;
@@ -30,14 +34,14 @@ struct ApplyArgs {
   int defer;
 };
 
-template <typename TX, typename TV>
+template <typename TX, typename TV, typename TZ = TV>
 struct UpdateArgs {
   TX* x;
   TX* r;
   const TV* p;
   const TV* q;
-  TV* z;
-  const TV* dinv;
+  TZ* z;
+  const TZ* dinv;
   double* partials;
   PcgState* state;
   int n;
@@ -46,8 +50,8 @@ struct UpdateArgs {
   double* totals;  // defer != 0: write the 12 reduced sums here, leave state alone
   int defer;
   int gmg;         // 1: z comes from the multigrid V-cycle (this kernel only reduces r.r)
-  TV* gmg_x0;      // gmg: also write the V-cycle's first sweep omega*Dinv*r here
-  TV gmg_omega;
+  TZ* gmg_x0;      // gmg: also write the V-cycle's first sweep omega*Dinv*r here
+  TZ gmg_omega;
 };
 
 template <typename TX>
@@ -117,13 +121,13 @@ void upload_element_constants(const double* K0, const double* W, const double* T
 template <typename TX, typename TV>
 void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64,
                   double ridge, TX* rvec, TV* dinv, cudaStream_t s);
-template <typename TV>
-void launch_apply(const ApplyArgs<TV>& a, int grid, cudaStream_t s);
+template <typename TV, typename TZ>
+void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s);
 // Grid (block count) launch_apply / launch_level_sweep use for n nodes; the
 // caller sizes its partials buffer as 6 doubles per block.
 int apply_grid(int n, int num_sms);
-template <typename TX, typename TV>
-void launch_update(const UpdateArgs<TX, TV>& u, int grid, cudaStream_t s);
+template <typename TX, typename TV, typename TZ>
+void launch_update(const UpdateArgs<TX, TV, TZ>& u, int grid, cudaStream_t s);
 template <typename TX>
 void launch_chom(const ChomArgs<TX>& c, int grid, cudaStream_t s);
 

@@ -291,3 +291,20 @@ def test_fp32_ridge_keeps_ch(S, seed):
                         S.HomogenizeOptions(residual_tol=1e-8, precision="fp64", preconditioner="gmg"))
     assert max(mixed.iterations) < 60
     assert rel_fro(mixed.tensor, fp64.tensor) < 1e-6
+
+
+@pytest.mark.gpu
+def test_mixed_gmg_hinge_breakdown_retried_in_fp64_operator(S):
+    """Seed 10 at 128^3: the FP32 operator loses p^T A p on the hinge modes of
+    the voxel shell; the mixed solve is redone with FP64 Krylov vectors and an
+    FP64-accumulated operator (precond_fallback 2), never with block Jacobi,
+    and matches the FP64 C^H."""
+    d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), 10)
+    mixed = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), 128,
+                         S.HomogenizeOptions(residual_tol=1e-5, precision="mixed"))
+    fp64 = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), 128,
+                        S.HomogenizeOptions(residual_tol=1e-8, precision="fp64", preconditioner="gmg"))
+    assert mixed.stats.precond_fallback in (0, 2)
+    assert mixed.stats.gmg_levels >= 2
+    assert max(mixed.iterations) < 60
+    assert rel_fro(mixed.tensor, fp64.tensor) < 1e-6

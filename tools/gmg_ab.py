@@ -11,7 +11,7 @@ for r in (int(a) for a in sys.argv[1].split(",")):
         opt = S.HomogenizeOptions(preconditioner="gmg")
         S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, opt)
         res = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, opt)
-        out.append({"r": r, "seed": seed, "it": list(res.iterations), "t_AS": res.timings["t_AS"],
+        out.append({"r": r, "seed": seed, "it": [int(v) for v in res.iterations], "t_AS": res.timings["t_AS"],
                     "t_solve": res.timings["t_solve"], "C": np.asarray(res.tensor).ravel().tolist()})
         print(r, seed, out[-1]["it"], f"AS {res.timings["t_AS"]:.2f} solve {res.timings["t_solve"]:.2f} ms", flush=True)
 if len(sys.argv) > 3:
