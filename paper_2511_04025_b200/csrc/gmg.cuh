@@ -250,13 +250,9 @@ __global__ void __launch_bounds__(192)
 // node-map lookup and one block-times-vector (9 x 6 FMA), a butterfly shuffle
 // sums the 18 outputs, and lanes 0..5 finish load case s = lane.
 template <typename TV>
-__global__ void __launch_bounds__(256) coarse_warp_sweep_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
-                                                                const TV* __restrict__ xin, TV* __restrict__ xout,
-                                                                TV omega, int mode, const PcgState* st) {
-  if (st->stop) return;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= L.n) return;  // whole warps exit together
-  const int idx = warp;
+__device__ __forceinline__ void coarse_warp_node(const LevelArgs<TV>& L, const TV* __restrict__ b,
+                                                 const TV* __restrict__ xin, TV* __restrict__ xout, TV omega,
+                                                 int mode, int idx, int lane) {
   const int g = L.node_list[idx];
   TV y[18];
 #pragma unroll
@@ -315,6 +311,21 @@ __global__ void __launch_bounds__(256) coarse_warp_sweep_kernel(const LevelArgs<
   xout[ob] = fma_t(omega, D[0] * r0 + D[1] * r1 + D[2] * r2, xin[ob]);
   xout[ob + 192] = fma_t(omega, D[1] * r0 + D[3] * r1 + D[4] * r2, xin[ob + 192]);
   xout[ob + 384] = fma_t(omega, D[2] * r0 + D[4] * r1 + D[5] * r2, xin[ob + 384]);
+}
+
+// Stored (Galerkin) levels are small, so a per-node loop over 27 neighbours is
+// a pure dependent-load chain (~30 us per sweep regardless of size).  Here one
+// WARP owns a node and lane m < 27 owns stencil neighbour m: each lane does one
+// node-map lookup and one block-times-vector (9 x 6 FMA), a butterfly shuffle
+// sums the 18 outputs, and lanes 0..5 finish load case s = lane.
+template <typename TV>
+__global__ void __launch_bounds__(256) coarse_warp_sweep_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
+                                                                const TV* __restrict__ xin, TV* __restrict__ xout,
+                                                                TV omega, int mode, const PcgState* st) {
+  if (st->stop) return;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= L.n) return;  // whole warps exit together
+  coarse_warp_node<TV>(L, b, xin, xout, omega, mode, warp, lane);
 }
 
 // first sweep from x = 0: xout = w Dinv b (pointwise)

@@ -239,12 +239,14 @@ int resolve_precision(const shl_solve_options& o) {
 // ---- solve on the resident mesh ----------------------------------------------
 // ---- geometric multigrid hierarchy (gmg.cuh) ---------------------------------
 struct GmgParams {
-  int nu = 2;          // pre/post block-Jacobi sweeps (nu = 1 broke down on ~1.5% of
-                       // 64^3 designs in FP32; nu = 2: none of 256, fewer iterations)
+  int nu = 0;          // pre/post block-Jacobi sweeps; 0 = by operator precision:
+                       // 1 with an FP64 operator (mixed, fp64), 2 with the FP32
+                       // one (nu = 1 broke down on ~1.5% of 64^3 FP32 designs)
   double omega = 0.6;  // Jacobi damping (>= 0.7 loses smoother convergence: lambda_max(D^-1 A) ~ 2.9)
   int min_r = 8;       // coarsest grid (nodes per axis); r = 4 Galerkin levels of a thin shell
                        // made the V-cycle indefinite on half the designs tested
-  int coarse_sweeps = 10;  // damped Jacobi sweeps on the coarsest level
+  int coarse_sweeps = 16;  // damped Jacobi sweeps on the coarsest level (128^3 sweep:
+                           // 16 beats 10 by ~3 iterations, 24 gains nothing more)
   int max_levels = 8;
   double omega_c = 0.6;    // damping on the stored (Galerkin) levels
   int l1 = 0;              // l1-block-Jacobi on the stored levels
@@ -421,6 +423,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   shl::launch_setup<TX, TZ>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), ridge, rv,
                             dinv, c->stream);
   Vcycle<TX, TZ> vc{c, gmg_params()};
+  if (vc.gp.nu <= 0) vc.gp.nu = sizeof(TV) == 8 ? 1 : 2;
   if (use_gmg) {
     vc.L = gmg_setup<TZ>(c, vc.gp, static_cast<TZ>(ridge));
     if (vc.L == 0) throw ShlError(SHL_VALIDATION, "multigrid needs r divisible by 2 with r/2 >= 8");
@@ -482,28 +485,68 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   double apply_ms = 0.0, update_ms = 0.0;
   int64_t apply_launches = 0;
   int64_t issued = 0;
-  for (;;) {
-    for (int it = 0; it < check; ++it) {
-      if (c->profiling) {
-        const size_t need = static_cast<size_t>(3 * (issued + 1));
-        while (c->prof_ev.size() < need) {
-          cudaEvent_t e;
-          CK(cudaEventCreate(&e));
-          c->prof_ev.push_back(e);
-        }
-        CK(cudaEventRecord(c->prof_ev[3 * issued], c->stream));
-        shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
-        precondition(0);
-        CK(cudaEventRecord(c->prof_ev[3 * issued + 1], c->stream));
-        shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
-        CK(cudaEventRecord(c->prof_ev[3 * issued + 2], c->stream));
-      } else {
-        shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
-        precondition(0);
-        shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
-      }
-      ++issued;
+  // Steady state: the iteration (update, V-cycle, apply: ~30 launches with
+  // multigrid) is captured once into a CUDA graph of kGraphIters iterations
+  // and replayed, which removes the per-kernel launch gaps of the small
+  // coarse-level kernels.  Profiling / tracing keep direct launches.
+  static const bool no_graph = std::getenv("SHL_NOGRAPH") != nullptr;  // A/B
+  constexpr int kGraphIters = 4;
+  const bool use_graph = !c->profiling && !trace && !no_graph && check % kGraphIters == 0;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launches = 0;  // kernel launches per graph replay
+  if (use_graph) {
+    const int64_t before = launches + vc.launches;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int it = 0; it < kGraphIters; ++it) {
+      shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
+      precondition(0);
+      shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
       launches += 2;
+    }
+    CK(cudaStreamEndCapture(c->stream, &graph));
+    CK(cudaGraphInstantiate(&gexec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    graph_launches = launches + vc.launches - before;
+    launches -= 2 * kGraphIters;  // counted per replay below
+    vc.launches -= graph_launches - 2 * kGraphIters;
+  }
+  struct GraphGuard {
+    cudaGraphExec_t g;
+    ~GraphGuard() {
+      if (g) cudaGraphExecDestroy(g);
+    }
+  } graph_guard{gexec};
+  for (;;) {
+    if (use_graph) {
+      for (int it = 0; it < check; it += kGraphIters) {
+        CK(cudaGraphLaunch(gexec, c->stream));
+        launches += graph_launches;
+        issued += kGraphIters;
+      }
+    } else {
+      for (int it = 0; it < check; ++it) {
+        if (c->profiling) {
+          const size_t need = static_cast<size_t>(3 * (issued + 1));
+          while (c->prof_ev.size() < need) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            c->prof_ev.push_back(e);
+          }
+          CK(cudaEventRecord(c->prof_ev[3 * issued], c->stream));
+          shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
+          precondition(0);
+          CK(cudaEventRecord(c->prof_ev[3 * issued + 1], c->stream));
+          shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
+          CK(cudaEventRecord(c->prof_ev[3 * issued + 2], c->stream));
+        } else {
+          shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
+          precondition(0);
+          shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
+        }
+        ++issued;
+        launches += 2;
+      }
     }
     CK(cudaGetLastError());
     c->d2h += sizeof(shl::PcgState);
@@ -592,23 +635,26 @@ void solve_dispatch_once(shl_ctx* c, const double* K0, const shl_solve_options& 
   switch (prec) {
     case SHL_PREC_FP64: run_solve<double, double, double>(c, K0, opt, C_out, st, prec, gmg); break;
     case SHL_PREC_MIXED: {
-      // FP32 operator first.  With the FP32 V-cycle, FP32 rounding of A p can
-      // swamp the ridge-sized curvature of a voxel shell's hinge modes (elements
-      // sharing only an edge or a corner) and p^T A p loses its sign; such a
-      // solve is redone with FP64 Krylov vectors and an FP64-accumulated
-      // operator (TV = double, TZ = float), which keeps the reference's 1e-11
-      // ridge and converges in the FP64 iteration count.
-      static const bool op64 = std::getenv("SHL_MIXED_OP64") != nullptr;  // A/B: always FP64 operator
-      if (gmg && op64) {
-        run_solve<double, double, float>(c, K0, opt, C_out, st, prec, gmg);
-        break;
-      }
-      try {
+      // Multigrid: FP32 V-cycle and z, FP64 Krylov vectors and FP64-accumulated
+      // operator (TV = double, TZ = float).  With an FP32 operator, rounding of
+      // A p swamps the ridge-sized curvature of a voxel shell's hinge modes
+      // (elements sharing only an edge or a corner) and p^T A p loses its sign
+      // on ~1 in 16 designs at 128^3; the FP64 operator keeps the reference's
+      // 1e-11 ridge and costs ~3% per design (128^3 sweep).  SHL_MIXED_OP32=1
+      // (A/B) runs the FP32 operator and redoes breakdowns with the FP64 one.
+      static const bool op32 = std::getenv("SHL_MIXED_OP32") != nullptr;
+      if (!gmg) {
         run_solve<double, float, float>(c, K0, opt, C_out, st, prec, gmg);
-      } catch (const ShlError& e) {
-        if (!gmg || !is_breakdown(e)) throw;
+      } else if (!op32) {
         run_solve<double, double, float>(c, K0, opt, C_out, st, prec, gmg);
-        if (st) st->precond_fallback = 2;
+      } else {
+        try {
+          run_solve<double, float, float>(c, K0, opt, C_out, st, prec, gmg);
+        } catch (const ShlError& e) {
+          if (!is_breakdown(e)) throw;
+          run_solve<double, double, float>(c, K0, opt, C_out, st, prec, gmg);
+          if (st) st->precond_fallback = 2;
+        }
       }
       break;
     }
