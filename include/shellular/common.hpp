@@ -144,6 +144,7 @@ inline void check(int code, const shl_ctx* ctx) {
     case SHL_DEGENERATE: throw DegenerateDesignError(msg);
     case SHL_SOLVER: throw SolverError(msg);
     case SHL_IO: throw IoError(msg);
+    case SHL_ERROR: throw Error(msg);
     default: throw DeviceError(msg);
   }
 }

@@ -72,6 +72,7 @@ class Matrix {
   Matrix operator*(T s) const { return map([s](T a) { return a * s; }); }
   Matrix operator/(T s) const { return map([s](T a) { return a / s; }); }
   Matrix& operator*=(T s) { return *this = *this * s; }
+  Matrix& operator/=(T s) { return *this = *this / s; }
   friend Matrix operator*(T s, const Matrix& m) { return m * s; }
 
   template <int C2>

@@ -17,6 +17,8 @@
  *   shl_homogenize_batch   <- (new) many designs, one call (SPEC sample_campaign)
  *   shl_homogenize_slabs / shl_homogenize_zslab
  *                          <- (new) z-slab decomposition of one design (C5)
+ *   shl_extract_isosurface <- extract_isosurface     geomio.hpp:45-108
+ *   shl_voxel_raw          <- VoxelMesh::write_raw   voxel.hpp:105-114 (bytes)
  *   shl_element_stiffness  <- element_stiffness      fem.hpp:50-92
  *   shl_random_design      <- random_design          field.hpp:569-593
  *   shl_expand_symmetry    <- expand_symmetry        field.hpp:236-249
@@ -41,7 +43,8 @@ enum {
   SHL_DEGENERATE = 2, /* DegenerateDesignError */
   SHL_SOLVER = 3,     /* SolverError           */
   SHL_IO = 4,         /* IoError               */
-  SHL_CUDA = 5        /* device / driver failure (no reference analogue) */
+  SHL_CUDA = 5,       /* device / driver failure (no reference analogue) */
+  SHL_ERROR = 6       /* shellular::Error itself (e.g. empty isosurface) */
 };
 
 enum { SHL_SYM_NONE = 0, SHL_SYM_CUBIC_OCTANT = 1, SHL_SYM_TETRAHEDRAL = 2 };
@@ -188,6 +191,21 @@ int shl_homogenize_zslab(shl_ctx* ctx, const uint8_t* nccl_id, int rank, int nra
                          const shl_design* design, const shl_shell_params* sp,
                          const shl_material* mat, int r, const shl_solve_options* opt,
                          double* C_out, shl_stats* stats);
+
+/* Marching cubes on the resident grid's corner samples: the zero level set
+ * with linear edge interpolation, vertices/triangles in exactly the
+ * reference's order.  vertices: 3*n_vertices doubles, triangles:
+ * 3*n_triangles vertex ids.  Counts are always written; the arrays only when
+ * both are non-NULL and their capacities (in vertices / triangles) suffice,
+ * so a NULL first call sizes the buffers.  SHL_ERROR when nothing crosses
+ * zero. */
+int shl_extract_isosurface(shl_ctx* ctx, double* vertices, int64_t vertex_capacity,
+                           uint32_t* triangles, int64_t triangle_capacity, int64_t* n_vertices,
+                           int64_t* n_triangles);
+
+/* write_raw bytes of the resident reduced mesh: r^3 bytes, 0 = absent,
+ * 1 + lround(254 beta) for a mesh element. */
+int shl_voxel_raw(shl_ctx* ctx, uint8_t* occupancy);
 
 /* Host helpers (reference arithmetic, no device work). */
 int shl_element_stiffness(const shl_material* mat, double edge, double* K_out /*576*/);

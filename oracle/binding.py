@@ -65,6 +65,8 @@ def lib():
         L.orc_homogenize.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _ip, _dp, C.c_double,
                                      C.c_double, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
                                      C.c_double, C.c_int, C.c_int, _dp, _ip, _dp, _dp]
+        L.orc_extract_isosurface.argtypes = [C.c_int, _dp, C.c_double, _dp, C.c_int64, _u32,
+                                             C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         _lib = L
     return _lib
 
@@ -88,6 +90,11 @@ def ref():
         L.ref_build_reduced_mesh.argtypes = [C.c_int, _dp, _dp, C.c_double, C.c_double, C.c_double,
                                              C.c_int, _u32, _dp, _i64]
         L.ref_step_function.argtypes = [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]
+        L.ref_extract_isosurface.argtypes = [C.c_int, _dp, _dp, C.c_double, _dp, C.c_int64, _u32,
+                                             C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.ref_write_raw.argtypes = [C.c_int, _dp, _dp, C.c_double, C.c_double, C.c_double, C.c_int,
+                                    C.c_char_p]
+        L.ref_export_mesh.argtypes = [_dp, C.c_int64, _u32, C.c_int64, C.c_char_p, C.c_int]
         _ref = L
     return _ref
 
@@ -308,6 +315,43 @@ def gyroid_design() -> Design:
                 if (h, k, l) != (0, 0, 0) and h * h + k * k + l * l <= 2:
                     w[(h * 3 + k) * 3 + l] = 1.0
     return Design("none", 2, pos, sg, w)
+
+
+def extract_isosurface(g: Grid, use_ref=False):
+    """geomio.hpp:45-108 marching cubes.  Returns (vertices (n,3) f64, triangles (m,3) u32)."""
+    L = ref() if use_ref else lib()
+    cor = np.ascontiguousarray(g.corners.reshape(-1))
+    nv, nt = C.c_int64(0), C.c_int64(0)
+    empty_d, empty_u = np.zeros(1), np.zeros(1, np.uint32)
+    if use_ref:
+        cen = np.ascontiguousarray(g.samples.reshape(-1))
+        call = lambda v, vc, t, tc: L.ref_extract_isosurface(g.r, cen, cor, g.norm, v, vc, t, tc,
+                                                             C.byref(nv), C.byref(nt))
+    else:
+        call = lambda v, vc, t, tc: L.orc_extract_isosurface(g.r, cor, g.norm, v, vc, t, tc,
+                                                             C.byref(nv), C.byref(nt))
+    _check(call(empty_d, 0, empty_u, 0), L, "ref" if use_ref else "orc")
+    v = np.zeros(3 * nv.value)
+    t = np.zeros(3 * nt.value, np.uint32)
+    _check(call(v, nv.value, t, nt.value), L, "ref" if use_ref else "orc")
+    return v.reshape(-1, 3), t.reshape(-1, 3)
+
+
+def ref_write_raw(g: Grid, path: str, sharpness=500.0, floor_ratio=1e-3, expand_layers=0) -> None:
+    """VoxelMesh::write_raw (voxel.hpp:105-114) of the reference's build_reduced_mesh."""
+    L = ref()
+    _check(L.ref_write_raw(g.r, np.ascontiguousarray(g.samples.reshape(-1)),
+                           np.ascontiguousarray(g.corners.reshape(-1)), g.norm, sharpness,
+                           floor_ratio, expand_layers, path.encode()), L, "ref")
+
+
+def ref_export_mesh(vertices: np.ndarray, triangles: np.ndarray, path: str, fmt: str = "stl") -> None:
+    """export_mesh (geomio.hpp:277-316): fmt 'stl' (binary) or 'obj'."""
+    L = ref()
+    v = np.ascontiguousarray(vertices, np.float64).reshape(-1)
+    t = np.ascontiguousarray(triangles, np.uint32).reshape(-1)
+    _check(L.ref_export_mesh(v, len(v) // 3, t, len(t) // 3, path.encode(), 0 if fmt == "stl" else 1),
+           L, "ref")
 
 
 __all__ = [n for n in dir() if not n.startswith("_")]

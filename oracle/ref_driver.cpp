@@ -1,12 +1,25 @@
 // ref_driver.cpp -- TEST INFRASTRUCTURE ONLY.
 //
-// Thin C ABI over the reference's OWN field/voxel code
-// (/root/reference/proj/include/shellular/{common,field,voxel}.hpp, included
+// Thin C ABI over the reference's OWN field/voxel/geomio code
+// (/root/reference/proj/include/shellular/{common,field,voxel,geomio}.hpp, included
 // unmodified; Eigen replaced by oracle/ref_shim).  Built by `make -C oracle ref`
 // into oracle/_ref/ and used only to generate / check tests/golden fixtures and
 // to pin the C++ restatement in oracle/shellular_oracle.cpp.
 #include "shellular/field.hpp"
 #include "shellular/voxel.hpp"
+
+// geomio.hpp uses hex_corner_offsets, defined in fem.hpp (fem.hpp:41-46), which
+// needs Eigen's sparse module and cannot be compiled here; the same eight
+// offsets are declared for it.
+namespace shellular {
+inline const std::array<Vec3i, 8>& hex_corner_offsets() {
+  static const std::array<Vec3i, 8> off = {Vec3i(0, 0, 0), Vec3i(1, 0, 0), Vec3i(1, 1, 0), Vec3i(0, 1, 0),
+                                           Vec3i(0, 0, 1), Vec3i(1, 0, 1), Vec3i(1, 1, 1), Vec3i(0, 1, 1)};
+  return off;
+}
+}  // namespace shellular
+
+#include "shellular/geomio.hpp"
 
 #include <cstring>
 #include <string>
@@ -144,6 +157,46 @@ int ref_step_function(double v, double sharpness, double floor_ratio, double* ou
     sp.sharpness = sharpness;
     sp.floor_ratio = floor_ratio;
     *out = step_function(v, sp);
+  });
+}
+
+// extract_isosurface (geomio.hpp:45-108); counts always, arrays when they fit
+int ref_extract_isosurface(int r, const double* centres, const double* corners, double norm,
+                           double* verts, std::int64_t vcap, std::uint32_t* tris, std::int64_t tcap,
+                           std::int64_t* nv, std::int64_t* nt) {
+  return guard([&] {
+    TriMesh m = extract_isosurface(grid_from(r, centres, corners, norm));
+    *nv = static_cast<std::int64_t>(m.vertices.size());
+    *nt = static_cast<std::int64_t>(m.triangles.size());
+    if (static_cast<std::int64_t>(m.vertices.size()) <= vcap)
+      for (size_t i = 0; i < m.vertices.size(); ++i)
+        for (int a = 0; a < 3; ++a) verts[3 * i + a] = m.vertices[i][a];
+    if (static_cast<std::int64_t>(m.triangles.size()) <= tcap)
+      for (size_t i = 0; i < m.triangles.size(); ++i)
+        for (int a = 0; a < 3; ++a) tris[3 * i + a] = m.triangles[i][a];
+  });
+}
+
+// VoxelMesh::write_raw (voxel.hpp:105-114) of build_reduced_mesh
+int ref_write_raw(int r, const double* centres, const double* corners, double norm, double sharpness,
+                  double floor_ratio, int expand_layers, const char* path) {
+  return guard([&] {
+    ShellParams sp;
+    sp.sharpness = sharpness;
+    sp.floor_ratio = floor_ratio;
+    sp.expand_layers = expand_layers;
+    build_reduced_mesh(grid_from(r, centres, corners, norm), sp).write_raw(path);
+  });
+}
+
+// export_mesh (geomio.hpp:277-316); format 0 = binary STL, 1 = OBJ
+int ref_export_mesh(const double* verts, std::int64_t nv, const std::uint32_t* tris, std::int64_t nt,
+                    const char* path, int format) {
+  return guard([&] {
+    TriMesh m;
+    for (std::int64_t i = 0; i < nv; ++i) m.vertices.emplace_back(verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]);
+    for (std::int64_t i = 0; i < nt; ++i) m.triangles.push_back({tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]});
+    export_mesh(m, path, format == 0 ? MeshFormat::StlBinary : MeshFormat::Obj);
   });
 }
 

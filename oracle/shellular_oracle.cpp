@@ -30,12 +30,16 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
+
+// the standard marching-cubes triangulation, packed (same data the product uses)
+#include "../paper_2511_04025_b200/csrc/mc_table.h"
 
 namespace orc {
 
 // ---- errors (common.hpp:25-48) -------------------------------------------
-enum Status { OK = 0, VALIDATION = 1, DEGENERATE = 2, SOLVER = 3, IO = 4 };
+enum Status { OK = 0, VALIDATION = 1, DEGENERATE = 2, SOLVER = 3, IO = 4, BASE = 6 };
 struct Error : std::runtime_error {
   int code;
   Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
@@ -861,6 +865,83 @@ struct MaskedGridSolver {
   }
 };
 
+// ---- marching cubes (geomio.hpp:45-108) ------------------------------------
+// Sequential restatement: cells in grid order, edges in table order, vertices
+// welded on (low lattice corner, axis) keys by a hash map -- the reference's
+// own algorithm; the GPU replaces the map by owner-cell prefix sums.
+struct TriMesh {
+  std::vector<double> v;          // 3 per vertex
+  std::vector<std::uint32_t> t;   // 3 per triangle
+};
+
+inline TriMesh extract_isosurface(const Grid& g) {
+  static const std::uint64_t kTri[256] = SHL_MC_PACKED;
+  static const int off[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
+                                {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+  if (g.norm == 0.0) fail(DEGENERATE, "cannot extract isosurface of a degenerate field");
+  const int r = g.r, r1 = r + 1;
+  TriMesh m;
+  std::unordered_map<std::uint64_t, std::uint32_t> edge_vertex;
+  auto corner = [&](int i, int j, int k) { return g.corners[(size_t(k) * r1 + j) * r1 + i]; };
+  auto vertex_on_edge = [&](const int* lo, int axis, double va, double vb) {
+    std::uint64_t key = ((std::uint64_t(lo[2]) * r1 + lo[1]) * r1 + lo[0]) * 4 + axis;
+    auto it = edge_vertex.find(key);
+    if (it != edge_vertex.end()) return it->second;
+    double t = (va == vb) ? 0.5 : va / (va - vb);
+    double p[3] = {double(lo[0]) / r, double(lo[1]) / r, double(lo[2]) / r};
+    p[axis] += t / r;
+    auto id = static_cast<std::uint32_t>(m.v.size() / 3);
+    m.v.insert(m.v.end(), p, p + 3);
+    edge_vertex.emplace(key, id);
+    return id;
+  };
+  for (int k = 0; k < r; ++k)
+    for (int j = 0; j < r; ++j)
+      for (int i = 0; i < r; ++i) {
+        double val[8];
+        int cube = 0;
+        for (int n = 0; n < 8; ++n) {
+          val[n] = corner(i + off[n][0], j + off[n][1], k + off[n][2]);
+          if (val[n] < 0.0) cube |= 1 << n;
+        }
+        std::uint32_t ev[12];
+        bool any = false;
+        for (int e = 0; e < 12; ++e) {
+          const int a = shl::mc::edge_a(e), b = shl::mc::edge_b(e);
+          if (!(((cube >> a) ^ (cube >> b)) & 1)) continue;  // kEdgeTable bit
+          any = true;
+          int ca[3], cb[3];
+          for (int d = 0; d < 3; ++d) {
+            ca[d] = (d == 0 ? i : d == 1 ? j : k) + off[a][d];
+            cb[d] = (d == 0 ? i : d == 1 ? j : k) + off[b][d];
+          }
+          int axis = 0;
+          for (int d = 0; d < 3; ++d)
+            if (ca[d] != cb[d]) axis = d;
+          const bool a_low = ca[axis] < cb[axis];
+          ev[e] = vertex_on_edge(a_low ? ca : cb, axis, a_low ? val[a] : val[b], a_low ? val[b] : val[a]);
+        }
+        if (!any) continue;
+        const std::uint64_t w = kTri[cube];
+        for (int t = 0; t < int(w >> 60); ++t) {
+          std::uint32_t tri[3];
+          for (int q = 0; q < 3; ++q) tri[q] = ev[(w >> (12 * t + 4 * q)) & 15];
+          if (tri[0] == tri[1] || tri[1] == tri[2] || tri[0] == tri[2]) continue;
+          const double* v0 = &m.v[3 * size_t(tri[0])];
+          const double* v1 = &m.v[3 * size_t(tri[1])];
+          const double* v2 = &m.v[3 * size_t(tri[2])];
+          double e1[3] = {v1[0] - v0[0], v1[1] - v0[1], v1[2] - v0[2]};
+          double e2[3] = {v2[0] - v0[0], v2[1] - v0[1], v2[2] - v0[2]};
+          double cx = e1[1] * e2[2] - e1[2] * e2[1], cy = e1[2] * e2[0] - e1[0] * e2[2],
+                 cz = e1[0] * e2[1] - e1[1] * e2[0];
+          if (std::sqrt(cx * cx + cy * cy + cz * cz) < 1e-12) continue;
+          m.t.insert(m.t.end(), tri, tri + 3);
+        }
+      }
+  if (m.t.empty()) fail(BASE, "field has no zero crossing: empty isosurface");
+  return m;
+}
+
 template <class Fn>
 int guard(Fn&& fn) {
   try {
@@ -956,6 +1037,22 @@ int orc_build_reduced_mesh(int r, const double* centres, const double* corners, 
     *n_elements = static_cast<std::int64_t>(m.elements.size());
     *n_surface = static_cast<std::int64_t>(m.n_surface);
     *full_fallback = m.full_fallback ? 1 : 0;
+  });
+}
+
+// extract_isosurface on a grid; counts always, arrays when they fit
+int orc_extract_isosurface(int r, const double* corners, double norm, double* verts, std::int64_t vcap,
+                           std::uint32_t* tris, std::int64_t tcap, std::int64_t* nv, std::int64_t* nt) {
+  return orc::guard([&] {
+    orc::Grid g;
+    g.r = r;
+    g.corners.assign(corners, corners + size_t(r + 1) * (r + 1) * (r + 1));
+    g.norm = norm;
+    orc::TriMesh m = orc::extract_isosurface(g);
+    *nv = static_cast<std::int64_t>(m.v.size() / 3);
+    *nt = static_cast<std::int64_t>(m.t.size() / 3);
+    if (*nv <= vcap) std::copy(m.v.begin(), m.v.end(), verts);
+    if (*nt <= tcap) std::copy(m.t.begin(), m.t.end(), tris);
   });
 }
 

@@ -11,7 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SHL_LIB") or os.path.join(HERE, "libshellular_cuda.so")
 
-SHL_OK, SHL_VALIDATION, SHL_DEGENERATE, SHL_SOLVER, SHL_IO, SHL_CUDA = range(6)
+SHL_OK, SHL_VALIDATION, SHL_DEGENERATE, SHL_SOLVER, SHL_IO, SHL_CUDA, SHL_ERROR = range(7)
 PREC_AUTO, PREC_FP64, PREC_MIXED, PREC_FP32 = -1, 0, 1, 2
 PRECOND_JACOBI, PRECOND_GMG, PRECOND_AUTO = 0, 1, 2
 
@@ -57,6 +57,7 @@ EXPORTS = (
     "shl_grid_solve", "shl_solve_mesh", "shl_homogenize", "shl_homogenize_batch",
     "shl_element_stiffness", "shl_random_design", "shl_expand_symmetry",
     "shl_homogenize_slabs", "shl_nccl_unique_id", "shl_homogenize_zslab",
+    "shl_extract_isosurface", "shl_voxel_raw",
 )
 
 _lib = None
@@ -103,5 +104,8 @@ def lib() -> C.CDLL:
     L.shl_homogenize_zslab.argtypes = [vp, vp, C.c_int, C.c_int, P(shl_design),
                                        P(shl_shell_params), P(shl_material), C.c_int,
                                        P(shl_solve_options), vp, P(shl_stats)]
+    L.shl_extract_isosurface.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, P(C.c_int64),
+                                         P(C.c_int64)]
+    L.shl_voxel_raw.argtypes = [vp, vp]
     _lib = L
     return L

@@ -45,7 +45,7 @@ class CudaError(Error):
 
 
 _ERR = {L.SHL_VALIDATION: ValidationError, L.SHL_DEGENERATE: DegenerateDesignError,
-        L.SHL_SOLVER: SolverError, L.SHL_IO: IoError, L.SHL_CUDA: CudaError}
+        L.SHL_SOLVER: SolverError, L.SHL_IO: IoError, L.SHL_CUDA: CudaError, L.SHL_ERROR: Error}
 
 
 def _check(code: int, ctx=None) -> None:
@@ -243,6 +243,22 @@ class VoxelMesh:
     def volume_ratio(self) -> float:
         return float(np.sum(self.beta)) / float(self.resolution) ** 3
 
+    def raw_bytes(self) -> np.ndarray:
+        """voxel.hpp:105-114 occupancy bytes: 0 absent, 1 + lround(254 beta)."""
+        occ = np.zeros(self.resolution ** 3, np.uint8)
+        x = np.asarray(self.beta, np.float64) * 254.0
+        f = np.floor(x)
+        occ[self.elements] = (1 + f + (x - f >= 0.5)).astype(np.uint8)  # lround, x >= 0
+        return occ
+
+    def write_raw(self, path: str) -> None:
+        """VoxelMesh::write_raw (voxel.hpp:105-114)."""
+        try:
+            with open(path, "wb") as f:
+                f.write(self.raw_bytes().tobytes())
+        except OSError as e:
+            raise IoError(f"cannot open '{path}' for writing") from e
+
 
 def classify_surface_elements(grid: FieldGrid, ctx: Context | None = None) -> np.ndarray:
     """voxel.hpp:118-141."""
@@ -272,10 +288,95 @@ def build_reduced_mesh(grid: FieldGrid, sp: ShellParams = ShellParams(),
     return VoxelMesh(r, el[: n.value].copy(), be[: n.value].copy(), bool(ff.value))
 
 
+def voxel_raw(grid: FieldGrid, sp: ShellParams = ShellParams(),
+              ctx: Context | None = None) -> np.ndarray:
+    """write_raw bytes of build_reduced_mesh(grid, sp), quantized on the device (r^3 uint8)."""
+    ctx = ctx or default_context()
+    build_reduced_mesh(grid, sp, ctx)
+    occ = np.zeros(grid.resolution ** 3, np.uint8)
+    _check(L.lib().shl_voxel_raw(ctx.handle, occ.ctypes.data), ctx)
+    return occ
+
+
 def full_solid_mesh(r: int, beta_value: float = 1.0) -> VoxelMesh:
     """voxel.hpp:316-326."""
     return VoxelMesh(r, np.arange(r ** 3, dtype=np.uint32), np.full(r ** 3, float(beta_value)),
                      True)
+
+
+# ---- geometry export (geomio.hpp) --------------------------------------------------
+@dataclass
+class TriMesh:
+    """geomio.hpp:18-39."""
+    vertices: np.ndarray   # (n, 3) float64
+    triangles: np.ndarray  # (m, 3) uint32
+
+    def area(self) -> float:
+        v = self.vertices
+        t = self.triangles.astype(np.int64)
+        e1, e2 = v[t[:, 1]] - v[t[:, 0]], v[t[:, 2]] - v[t[:, 0]]
+        return float(0.5 * np.linalg.norm(np.cross(e1, e2), axis=1).sum())
+
+    def signed_volume(self) -> float:
+        v = self.vertices
+        t = self.triangles.astype(np.int64)
+        return float(np.einsum("ij,ij->i", v[t[:, 0]], np.cross(v[t[:, 1]], v[t[:, 2]])).sum() / 6.0)
+
+
+def extract_isosurface(grid: FieldGrid, ctx: Context | None = None) -> TriMesh:
+    """geomio.hpp:45-108: marching cubes on the device; the reference's vertices,
+    triangles and ordering, bit for bit."""
+    ctx = ctx or default_context()
+    if grid.degenerate():
+        raise DegenerateDesignError("cannot extract isosurface of a degenerate field")
+    _load_grid(grid, ctx)
+    nv, nt = C.c_int64(0), C.c_int64(0)
+    _check(L.lib().shl_extract_isosurface(ctx.handle, None, 0, None, 0, C.byref(nv), C.byref(nt)), ctx)
+    v = np.zeros((nv.value, 3))
+    t = np.zeros((nt.value, 3), np.uint32)
+    _check(L.lib().shl_extract_isosurface(ctx.handle, v.ctypes.data, nv.value, t.ctypes.data, nt.value,
+                                          C.byref(nv), C.byref(nt)), ctx)
+    return TriMesh(v, t)
+
+
+def export_mesh(mesh: TriMesh, path: str, fmt: str = "stl") -> None:
+    """geomio.hpp:272-316: fmt "stl" (binary) or "obj"; same bytes as the reference."""
+    if len(mesh.triangles) == 0:
+        raise ValidationError("refusing to export an empty mesh")
+    if fmt not in ("stl", "obj"):
+        raise ValidationError(f"unknown mesh format '{fmt}'")
+    v = np.asarray(mesh.vertices, np.float64)
+    t = np.asarray(mesh.triangles, np.int64)
+    try:
+        f = open(path, "wb")
+    except OSError as e:
+        raise IoError(f"cannot open '{path}' for writing") from e
+    with f:
+        if fmt == "stl":
+            header = b"shellular voxel cell export".ljust(80, b"\0")
+            a, b, c = v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]
+            # Vec3 cross / norm / division in the reference's order (no FMA in numpy)
+            e1, e2 = b - a, c - a
+            n = np.stack([e1[:, 1] * e2[:, 2] - e1[:, 2] * e2[:, 1],
+                          e1[:, 2] * e2[:, 0] - e1[:, 0] * e2[:, 2],
+                          e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]], axis=1)
+            ln = np.sqrt((n[:, 0] * n[:, 0] + n[:, 1] * n[:, 1]) + n[:, 2] * n[:, 2])
+            nz = ln > 0.0
+            n[nz] = n[nz] / ln[nz, None]
+            rec = np.zeros(len(t), dtype=[("f", "<f4", 12), ("attr", "<u2")])
+            rec["f"] = np.concatenate([n, a, b, c], axis=1).astype(np.float32)
+            f.write(header)
+            f.write(np.uint32(len(t)).tobytes())
+            f.write(rec.tobytes())
+        else:
+            lines = [f"v {_g17(x)} {_g17(y)} {_g17(z)}\n" for x, y, z in v]
+            lines += [f"f {i + 1} {j + 1} {k + 1}\n" for i, j, k in t]
+            f.write("".join(lines).encode())
+
+
+def _g17(x: float) -> str:
+    """std::ostream << double with precision(17) (%.17g)."""
+    return "%.17g" % x
 
 
 # ---- FEM (fem.hpp) ------------------------------------------------------------------

@@ -119,6 +119,8 @@ struct shl_ctx {
   };
   std::vector<GmgLevel> gmg;
   DevBuf gmg0;  // level-0 V-cycle work vectors (xa, xb, res)
+  // marching cubes / raw export (geom.cu)
+  DevBuf mc_owned, mc_cnt, mc_verts, mc_tris;
   Misc* hmisc = nullptr;
   shl::PcgState* hstate = nullptr;
   double* hC = nullptr;

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "shellular/geomio.hpp"
 #include "shellular/pipeline.hpp"
 
 using namespace shellular;
@@ -613,6 +614,63 @@ DEVICE_CASE(self_convergence, "self convergence between r=8 and r=16") {
   HomogenizationResult a = homogenize(seeded_design(77), ShellParams{}, BaseMaterial{}, 8);
   HomogenizationResult b = homogenize(seeded_design(77), ShellParams{}, BaseMaterial{}, 16);
   CHECK(rel_diff(a.tensor.c, b.tensor.c) < 0.6);
+}
+
+// ---- geomio (SPEC.md geomio examples; geomio.hpp:45-108, :272-316) ----------
+DEVICE_CASE(mc_sphere_area, "sphere-field isosurface area within 2% of analytic at r=64") {
+  const double R = 0.3;
+  FieldGrid grid = sample_grid_fn(
+      [R](const Vec3& p) {
+        Vec3 d = p - Vec3(0.5, 0.5, 0.5);
+        return d.squaredNorm() - R * R;
+      },
+      64);
+  TriMesh m = extract_isosurface(grid);
+  const double exact = 4.0 * 3.14159265358979323846 * R * R;
+  CHECK(std::abs(m.area() - exact) < 0.02 * exact);
+  CHECK(std::abs(std::abs(m.signed_volume()) - 4.0 / 3.0 * 3.14159265358979323846 * R * R * R) < 0.02);
+  for (const auto& t : m.triangles)
+    for (int q = 0; q < 3; ++q) CHECK(t[q] < m.vertices.size());
+}
+
+DEVICE_CASE(mc_plane, "plane design isosurface lies within half a voxel of its plane") {
+  const int r = 16;
+  TriMesh m = extract_isosurface(sample_grid(plane_design(0, 0.0), r));
+  CHECK(!m.triangles.empty());
+  size_t near = 0;
+  for (const auto& v : m.vertices) near += std::abs(std::abs(v[0] - 0.5) - 0.5) < 0.5 / r || std::abs(v[0] - 0.5) < 0.5 / r;
+  CHECK(near == m.vertices.size());
+}
+
+DEVICE_CASE(mc_empty, "a field without zero crossing has no isosurface") {
+  CHECK_THROWS_AS(extract_isosurface(sample_grid_fn([](const Vec3&) { return 1.0; }, 8)), Error);
+  FieldGrid zero = sample_grid_fn([](const Vec3&) { return 0.0; }, 8);
+  CHECK_THROWS_AS(extract_isosurface(zero), DegenerateDesignError);
+}
+
+DEVICE_CASE(stl_roundtrip, "binary STL byte layout reads back with an independent reader") {
+  TriMesh m = extract_isosurface(sample_grid(seeded_design(3), 8));
+  std::string path = "mc_test_export.stl";
+  export_mesh(m, path, MeshFormat::StlBinary);
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  CHECK(f != nullptr);
+  std::vector<unsigned char> bytes(84 + 50 * m.triangles.size() + 16);
+  size_t n = std::fread(bytes.data(), 1, bytes.size(), f);
+  std::fclose(f);
+  std::remove(path.c_str());
+  CHECK(n == 84 + 50 * m.triangles.size());
+  std::uint32_t count = 0;
+  std::memcpy(&count, bytes.data() + 80, 4);
+  CHECK(count == m.triangles.size());
+  size_t bad = 0;
+  for (size_t t = 0; t < m.triangles.size(); ++t) {
+    float rec[12];
+    std::memcpy(rec, bytes.data() + 84 + 50 * t, 48);
+    for (int q = 0; q < 3; ++q)
+      for (int a = 0; a < 3; ++a) bad += rec[3 + 3 * q + a] != float(m.vertices[m.triangles[t][q]][a]);
+  }
+  CHECK(bad == 0);
+  CHECK_THROWS_AS(export_mesh(TriMesh{}, path, MeshFormat::Obj), ValidationError);
 }
 
 int main(int argc, char** argv) {
