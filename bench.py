@@ -46,8 +46,10 @@ ITERS_128 = {1: 1117, 2: 1106, 3: 1524, 4: 1164, 5: 1181, 6: 950, 7: 916, 8: 106
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--steps", type=int, default=16)
+    p.add_argument("--warmup", type=int, default=4)
+    p.add_argument("--lanes", type=int, default=4,
+                   help="designs in flight at once per GPU (shl_set_batch_lanes)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--r", type=int, default=128)
     p.add_argument("--tol", type=float, default=1e-5)
@@ -72,6 +74,9 @@ def config(args, world):
             "rtol": args.tol, "precision": args.precision, "preconditioner": args.preconditioner,
             "global_batch": world,
             "designs_per_rank_per_step": 1, "parallelism": f"design-sharded x{world}",
+            "designs_in_flight_per_gpu": args.lanes,
+            "timed_region": f"one shl_homogenize_batch call over {args.steps} designs per rank, "
+                            f"{args.lanes} lanes (streams + host threads) in flight",
             "l2": "inputs larger than L2 (solver working set ~300 MB per design, new design each step)"}
 
 
@@ -218,8 +223,9 @@ def run_ours(args, rank, world, local):
                               preconditioner=args.preconditioner)
     warm, timed = seeds_for(rank, args.steps, args.warmup)
     designs = [S.random_design(spec, s) for s in timed]
-    for s in warm:
-        S.homogenize(S.random_design(spec, s), sp, mat, args.r, opt, ctx=ctx)
+    # warm-up: same batch path (creates the lane contexts, sizes every workspace)
+    S.homogenize_batch([S.random_design(spec, s) for s in warm], sp, mat, args.r, opt, ctx=ctx,
+                       lanes=args.lanes)
 
     def barrier():
         torch.cuda.synchronize()
@@ -227,28 +233,39 @@ def run_ours(args, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize()
 
-    ctx.set_profiling(True)
     barrier()
-    results = []
     with ClockSampler(local) as clk:
         w0 = time.perf_counter()
-        for d in designs:
-            results.append(S.homogenize(d, sp, mat, args.r, opt, ctx=ctx))
+        Cb, status, st = S.homogenize_batch(designs, sp, mat, args.r, opt, ctx=ctx, lanes=args.lanes)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
     barrier()
-    ctx.set_profiling(False)
+    if (status != 0).any():
+        raise RuntimeError(f"designs failed in the timed batch: {status.tolist()}")
+    # device time: each lane runs its designs back to back on its own stream, so
+    # the job's device time is the busiest lane's summed CUDA-event span
+    # (field -> C^H per design, events inside the library)
+    lane_s = {}
+    for s_ in st:
+        lane_s[s_.lane] = lane_s.get(s_.lane, 0.0) + s_.timings["t_fwd"] / 1e3
+    dev_s = max(lane_s.values())
+    gpu_launches = sum(s_.kernel_launches for s_ in st)
+    h2d = sum(s_.h2d_bytes for s_ in st) / len(st)
+    d2h = sum(s_.d2h_bytes for s_ in st) / len(st)
+    nodes = statistics.mean(s_.n_nodes for s_ in st)
+    iters = [int(max(s_.iterations)) for s_ in st]
 
-    dev_s = sum(r.timings["t_fwd"] for r in results) / 1e3  # CUDA-event time per design, summed
-    st = [r.stats for r in results]
-    apply_ms = sum(s.apply_ms for s in st)
-    update_ms = sum(s.update_ms for s in st)
-    launches_apply = sum(s.apply_launches for s in st)
-    gpu_launches = sum(s.kernel_launches for s in st)
-    h2d = sum(s.h2d_bytes for s in st) / len(st)
-    d2h = sum(s.d2h_bytes for s in st) / len(st)
-    nodes = statistics.mean(s.n_nodes for s in st)
-    iters = [int(max(r.iterations)) for r in results]
+    # untimed profiling pass (one lane, per-launch CUDA events around the apply
+    # and the update + V-cycle) for the roofline of the dominant kernel
+    ctx.set_profiling(True)
+    prof = [S.homogenize(d, sp, mat, args.r, opt, ctx=ctx) for d in designs[:2]]
+    ctx.set_profiling(False)
+    pst = [r_.stats for r_ in prof]
+    apply_ms = sum(s_.apply_ms for s_ in pst)
+    update_ms = sum(s_.update_ms for s_ in pst)
+    launches_apply = sum(s_.apply_launches for s_ in pst)
+    prof_nodes = statistics.mean(s_.n_nodes for s_ in pst)
+    solve_ms = sum(r_.timings["t_solve"] for r_ in prof)
 
     t = torch.tensor([dev_s, wall], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -259,9 +276,12 @@ def run_ours(args, rank, world, local):
     # dominant kernel of the timed region and its roofline (per launch)
     xb = 8 if args.precision in ("mixed", "fp64") else 4
     vb = 8 if args.precision == "fp64" else 4
-    bytes_apply = 18 * vb * 5 + 0  # z gather (once), p r/w, q r/w  per node
-    bytes_update = 18 * xb * 4 + 18 * vb * 3 + 6 * vb  # x r/w, r r/w, p, q, z w, Dinv
     gmg = any(s_.gmg_levels for s_ in st)
+    if gmg and args.precision == "mixed":
+        vb = 8  # multigrid mixed mode: FP64 p, q and operator, FP32 z (shl_api.cu solve_dispatch)
+    zb = 4 if args.precision in ("mixed", "fp32") else 8
+    bytes_apply = 18 * zb + 18 * vb * 4  # z gather (once), p r/w, q r/w  per node
+    bytes_update = 18 * xb * 4 + 18 * vb * 3 + 6 * vb  # x r/w, r r/w, p, q, z w, Dinv
     if gmg or apply_ms >= update_ms:
         # with multigrid, update_ms also holds the V-cycle; the apply stays the
         # largest single kernel of an iteration
@@ -269,15 +289,15 @@ def run_ours(args, rank, world, local):
     else:
         kname, per_node, tot_ms = "update_kernel (x,r,z update + dots)", bytes_update, update_ms
     avg_launch_s = tot_ms / 1e3 / max(launches_apply, 1)
-    alg_bytes = per_node * nodes
+    alg_bytes = per_node * prof_nodes
     peak, peak_src = peaks()
     achieved = alg_bytes / avg_launch_s / 1e9
     nt = ncu_traffic()
     traffic = None
     kn = kname.split(" ")[0]
     if nt and kn in nt.get("kernels", {}):
-        traffic = nt["kernels"][kn]["per_node_bytes"] * nodes
-    iter_bytes = (bytes_apply + bytes_update) * nodes
+        traffic = nt["kernels"][kn]["per_node_bytes"] * prof_nodes
+    iter_bytes = (bytes_apply + bytes_update) * prof_nodes
     iter_s = (apply_ms + update_ms) / 1e3 / max(launches_apply, 1)
 
     line = {"metric": METRIC, "value": total_designs / dev_max, "unit": UNIT, "n_gpus": world,
@@ -289,22 +309,28 @@ def run_ours(args, rank, world, local):
             "config": config(args, world),
             "e2e": {"value": total_designs / wall_max, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "how": "wall clock around the C-ABI call shl_homogenize with host design "
+                    "how": "wall clock around the C-ABI call shl_homogenize_batch with host design "
                            "arrays in, host C^H out (host cosine tables + H2D + D2H inside)"},
             "gpu_launches": int(gpu_launches),
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_us": avg_launch_s * 1e6,
                          "peak_source": peak_src,
+                         "share_of_solve": tot_ms / solve_ms if solve_ms else None,
+                         "measured_on": "untimed profiling pass over 2 of the designs (one lane, "
+                                        "CUDA events around every launch on the library stream)",
                          "pcg_iteration": None if gmg else
                          {"bytes": iter_bytes, "us": iter_s * 1e6,
                           "achieved_gbs": iter_bytes / iter_s / 1e9 if iter_s else None,
                           "frac": iter_bytes / iter_s / 1e9 / peak if iter_s else None},
                          "iteration_us": iter_s * 1e6},
-            "stages_ms": {k: statistics.mean(r.timings[k] for r in results)
+            "stages_ms": {k: statistics.mean(s_.timings[k] for s_ in st)
                           for k in ("t_field", "t_mesh", "t_AS", "t_solve", "t_C", "t_fwd")},
+            "stages_ms_single_lane": {k: statistics.mean(r_.timings[k] for r_ in prof)
+                                      for k in ("t_field", "t_mesh", "t_AS", "t_solve", "t_C", "t_fwd")},
             "iterations_lockstep": iters, "active_nodes_mean": nodes,
             "gmg_levels": max(s_.gmg_levels for s_ in st),
+            "lane_device_s": {str(k): v for k, v in sorted(lane_s.items())},
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -105,7 +105,7 @@ typedef struct {
   int32_t converged;
   int32_t full_fallback;
   int32_t precision; /* resolved SHL_PREC_* */
-  int32_t reserved0;
+  int32_t lane;      /* batch lane that ran this design (shl_set_batch_lanes) */
   int64_t n_surface;  /* surface elements before dilation */
   int64_t n_elements; /* active (reduced-mesh) elements */
   int64_t n_nodes;    /* active torus nodes */
@@ -169,6 +169,10 @@ int shl_homogenize(shl_ctx* ctx, const shl_design* design, const shl_shell_param
 /* n designs at one resolution; C_out: n*36, stats: n (may be NULL), status:
  * n per-design codes (may be NULL).  Returns SHL_OK unless a device error
  * stops the batch; per-design failures are reported through status. */
+/* Designs a batch keeps in flight concurrently (default 1): lanes >= 2 run
+ * that many designs at once on sub-contexts of ctx (same device, one stream
+ * and host thread each); results and per-design stats are unchanged. */
+int shl_set_batch_lanes(shl_ctx* ctx, int lanes);
 int shl_homogenize_batch(shl_ctx* ctx, int n, const shl_design* designs,
                          const shl_shell_params* sp, const shl_material* mat, int r,
                          const shl_solve_options* opt, double* C_out, shl_stats* stats,

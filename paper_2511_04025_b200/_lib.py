@@ -41,7 +41,7 @@ class shl_stats(C.Structure):
                 ("t_AS", C.c_double), ("t_RHS", C.c_double), ("t_solve", C.c_double),
                 ("t_C", C.c_double), ("t_fwd", C.c_double),
                 ("iterations", C.c_int32 * 6), ("converged", C.c_int32),
-                ("full_fallback", C.c_int32), ("precision", C.c_int32), ("reserved0", C.c_int32),
+                ("full_fallback", C.c_int32), ("precision", C.c_int32), ("lane", C.c_int32),
                 ("n_surface", C.c_int64), ("n_elements", C.c_int64), ("n_nodes", C.c_int64),
                 ("n_tiles", C.c_int64), ("norm", C.c_double), ("volume_ratio", C.c_double),
                 ("apply_ms", C.c_double), ("update_ms", C.c_double),
@@ -57,7 +57,7 @@ EXPORTS = (
     "shl_grid_solve", "shl_solve_mesh", "shl_homogenize", "shl_homogenize_batch",
     "shl_element_stiffness", "shl_random_design", "shl_expand_symmetry",
     "shl_homogenize_slabs", "shl_nccl_unique_id", "shl_homogenize_zslab",
-    "shl_extract_isosurface", "shl_voxel_raw",
+    "shl_extract_isosurface", "shl_voxel_raw", "shl_set_batch_lanes",
 )
 
 _lib = None
@@ -107,5 +107,6 @@ def lib() -> C.CDLL:
     L.shl_extract_isosurface.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, P(C.c_int64),
                                          P(C.c_int64)]
     L.shl_voxel_raw.argtypes = [vp, vp]
+    L.shl_set_batch_lanes.argtypes = [vp, C.c_int]
     _lib = L
     return L

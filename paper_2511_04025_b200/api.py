@@ -461,6 +461,7 @@ class SolveStats:
     d2h_bytes: int = 0
     gmg_levels: int = 0
     precond_fallback: int = 0  # 1: block-Jacobi redo, 2: FP64-operator redo (shellular_cuda.h)
+    lane: int = 0              # batch lane (homogenize_batch(lanes=...))
 
     @classmethod
     def from_abi(cls, s: L.shl_stats) -> "SolveStats":
@@ -468,7 +469,8 @@ class SolveStats:
                    bool(s.converged), PRECISION_NAME.get(s.precision, "?"), s.n_surface,
                    s.n_elements, s.n_nodes, s.n_tiles, s.norm, s.volume_ratio,
                    bool(s.full_fallback), s.apply_ms, s.update_ms, s.apply_launches,
-                   s.kernel_launches, s.h2d_bytes, s.d2h_bytes, s.gmg_levels, s.precond_fallback)
+                   s.kernel_launches, s.h2d_bytes, s.d2h_bytes, s.gmg_levels, s.precond_fallback,
+                   s.lane)
 
 
 class GridSolver:
@@ -556,9 +558,11 @@ def homogenize(params: DesignParams, sp: ShellParams, mat: BaseMaterial, r: int,
 
 def homogenize_batch(designs: Sequence[DesignParams], sp: ShellParams, mat: BaseMaterial, r: int,
                      opt: HomogenizeOptions = HomogenizeOptions(),
-                     ctx: Context | None = None):
-    """Many designs in one C-ABI call (shl_homogenize_batch). Returns (C[n,6,6], status[n], stats)."""
+                     ctx: Context | None = None, lanes: int = 1):
+    """Many designs in one C-ABI call (shl_homogenize_batch), `lanes` of them in
+    flight at once on the device. Returns (C[n,6,6], status[n], stats)."""
     ctx = ctx or default_context()
+    _check(L.lib().shl_set_batch_lanes(ctx.handle, int(lanes)), ctx)
     n = len(designs)
     arr = (L.shl_design * max(n, 1))()
     keep = []

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -29,6 +30,11 @@ namespace shl {
 namespace host {
 
 extern thread_local std::string g_thread_error;
+// Stream of the context the calling thread is working in (set by guarded()):
+// workspaces grow with stream-ordered cudaMallocAsync / cudaFreeAsync on it, so
+// a growing buffer never synchronizes the device (and with it the other batch
+// lanes), as cudaFree would.
+extern thread_local cudaStream_t g_alloc_stream;
 
 // Owning device allocation that only grows.  Move-only: a copied raw pointer
 // would be freed twice (e.g. when a std::vector of levels reallocates).
@@ -54,11 +60,24 @@ struct DevBuf {
   }
   void ensure(size_t bytes) {
     if (bytes <= cap) return;
-    if (p) cudaFree(p);
+    static const bool sync_alloc = std::getenv("SHL_SYNC_ALLOC") != nullptr;  // A/B
+    const cudaStream_t as = sync_alloc ? nullptr : g_alloc_stream;
+    if (p) {
+      if (as)
+        CK(cudaFreeAsync(p, as));
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     cap = 0;
     size_t want = bytes + bytes / 8 + 256;
-    CK(cudaMalloc(&p, want));
+    if (as) {
+      CK(cudaMallocAsync(&p, want, as));
+      // host-synchronous copies (legacy stream) may touch it next
+      CK(cudaStreamSynchronize(as));
+    } else {
+      CK(cudaMalloc(&p, want));
+    }
     cap = want;
   }
   template <class T>
@@ -94,6 +113,7 @@ struct shl_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t cap_stream = nullptr;  // only ever in capture mode (iteration graph)
   std::string err;
   bool profiling = false;
   int64_t launches = 0;
@@ -128,6 +148,10 @@ struct shl_ctx {
   void* nccl = nullptr;  // z-slab communicator (slab.cu), created on demand
   void (*nccl_deleter)(void*) = nullptr;
   std::vector<cudaEvent_t> prof_ev;
+  // concurrent batch lanes (shl_homogenize_batch): sub-contexts on the same
+  // device, each with its own stream and workspaces, driven by one host thread
+  int n_lanes = 1;
+  std::vector<shl_ctx*> lanes;
 
   void sync() { CK(cudaStreamSynchronize(stream)); }
   float ms(int a, int b) {
@@ -142,6 +166,11 @@ namespace host {
 
 template <class Fn>
 int guarded(shl_ctx* ctx, Fn&& fn) {
+  struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+    ~StreamScope() { g_alloc_stream = prev; }
+  } scope(ctx ? ctx->stream : nullptr);
   try {
     if (ctx) CK(cudaSetDevice(ctx->device));
     fn();

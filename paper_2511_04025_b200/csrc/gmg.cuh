@@ -149,10 +149,10 @@ __device__ __forceinline__ void stencil_gather_plane(GatherAcc<TV>& acc, int idx
 
 // level_sweep_kernel latency-split three ways: three warps per 32 nodes, warp p
 // gathers plane dz=p-1, warp p then finishes load-case pair p (gather3_tile).
-template <typename TB, typename TV, bool kFine>
+template <typename TB, typename TV, bool kFine, typename TO = TV>
 __global__ void __launch_bounds__(192)
     level_sweep3_kernel(const LevelArgs<TV> L, const TB* __restrict__ b, const TV* __restrict__ xin,
-                        TV* __restrict__ xout, TV omega, int mode, PcgState* st, double* partials,
+                        TO* __restrict__ xout, TV omega, int mode, PcgState* st, double* partials,
                         int init) {
   __shared__ __align__(16) TV part_s[2][3 * 18 * 32];
   __shared__ double scratch[32 * 6];
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(192)
         }
         if (mode == 1) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s_) * 32] = g == 0 ? TV(0) : res[c];
+          for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s_) * 32] = static_cast<TO>(g == 0 ? TV(0) : res[c]);
           continue;
         }
         const TV z0 = D[0] * res[0] + D[1] * res[1] + D[2] * res[2];
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(192)
         xo[2] = fma_t(omega, z2, xo[2]);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          xout[ob + (c * 6 + s_) * 32] = xo[c];
+          xout[ob + (c * 6 + s_) * 32] = static_cast<TO>(xo[c]);
           if (mode == 2) gam2[k] += static_cast<double>(b[ob + (c * 6 + s_) * 32]) * static_cast<double>(xo[c]);
         }
       }
@@ -731,6 +731,144 @@ __global__ void coarse_dinv_kernel(const int* __restrict__ list_c, int n_c,
   for (int q = 0; q < 6; ++q) dinv[vbase(idx, 6) + q * 32] = static_cast<TV>(inv[q]);
 }
 
+// ---- coarsest level: every Jacobi sweep in one cluster launch ---------------
+// The coarsest grid (8^3 torus, <= 512 active nodes) used to take one kernel
+// per damped Jacobi sweep, each a few microseconds of dependent L2 loads plus a
+// launch.  Here a cluster of kCoarseCluster CTAs owns it: CTA k holds the
+// stencils, right-hand side, Dinv and neighbour ids of nodes [k*per, (k+1)*per)
+// in shared memory, and EVERY CTA holds a full copy of x (ping-pong).  A sweep
+// computes the owned nodes' new values (thread = node x load case x stencil
+// plane, planes summed in fixed order), writes them into the next x buffer of
+// all CTAs through distributed shared memory, and ends with a cluster barrier.
+// Same arithmetic as jacobi_first + (sweeps-1) coarse_warp_sweep launches.
+constexpr int kCoarseCluster = 16;
+
+template <typename TV>
+__global__ void __cluster_dims__(kCoarseCluster, 1, 1) __launch_bounds__(576)
+    coarsest_cluster_kernel(const LevelArgs<TV> L, const TV* __restrict__ b, TV* __restrict__ xout, TV omega,
+                            int sweeps, const PcgState* st) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  if (st->stop) return;  // the same value in every CTA of the cluster
+  const int n = L.n;
+  const int per = (n + kCoarseCluster - 1) / kCoarseCluster;  // <= 32
+  const int rank = static_cast<int>(cl.block_rank());
+  const int n0 = rank * per;
+  const int nown = max(0, min(n, n0 + per) - n0);
+  extern __shared__ __align__(16) unsigned char csm[];
+  TV* xs0 = reinterpret_cast<TV*>(csm);                // [n][18]
+  TV* xs1 = xs0 + static_cast<size_t>(n) * 18;         // [n][18]
+  TV* sten = xs1 + static_cast<size_t>(n) * 18;        // [per][243]
+  TV* bo = sten + static_cast<size_t>(per) * kStencil;  // [per][18]
+  TV* dv = bo + per * 18;                              // [per][6]
+  TV* part = dv + per * 6;                             // [3][per][18]
+  int* nbr = reinterpret_cast<int*>(part + 3 * per * 18);  // [per][27], -1 = absent
+  int* gid = nbr + per * 27;                                 // [per]
+  const int tid = threadIdx.x;
+  // stage the owned nodes
+  for (int t = tid; t < nown * kStencil; t += blockDim.x) {
+    const int li = t / kStencil, q = t % kStencil;
+    sten[li * kStencil + q] = L.stencil[vbase(n0 + li, kStencil) + q * 32];
+  }
+  for (int t = tid; t < nown * 18; t += blockDim.x) {
+    const int li = t / 18, q = t % 18;
+    bo[t] = b[vbase(n0 + li, 18) + q * 32];
+  }
+  for (int t = tid; t < nown * 6; t += blockDim.x) {
+    const int li = t / 6, q = t % 6;
+    dv[t] = L.dinv[vbase(n0 + li, 6) + q * 32];
+  }
+  const int r = L.r, rr = r * r;
+  for (int t = tid; t < nown * 27; t += blockDim.x) {
+    const int li = t / 27, m = t % 27;
+    const int g = L.node_list[n0 + li];
+    if (m == 0) gid[li] = g;
+    const int i = g % r, j = (g / r) % r, k = g / rr;
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+    const int xi = (i + dx + r) % r, yj = (j + dy + r) % r, zk = (k + dz + r) % r;
+    nbr[t] = (m == 13) ? n0 + li : L.node_map[(zk * r + yj) * r + xi];
+  }
+  __syncthreads();
+  // thread -> (owned node li, load case s, stencil plane p)
+  const int p = tid / 192, rem = tid % 192, li = rem / 6, s_ = rem % 6;
+  const bool owner = li < nown;
+  // x0 = omega Dinv b (jacobi_first), broadcast to every CTA
+  if (p == 0 && owner) {
+    const TV* D = dv + li * 6;
+    const TV r0 = bo[li * 18 + s_], r1 = bo[li * 18 + 6 + s_], r2 = bo[li * 18 + 12 + s_];
+    const TV v[3] = {omega * (D[0] * r0 + D[1] * r1 + D[2] * r2), omega * (D[1] * r0 + D[3] * r1 + D[4] * r2),
+                     omega * (D[2] * r0 + D[4] * r1 + D[5] * r2)};
+    for (int dst = 0; dst < kCoarseCluster; ++dst) {
+      TV* xr = cl.map_shared_rank(xs0, dst);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) xr[(n0 + li) * 18 + c * 6 + s_] = v[c];
+    }
+  }
+  cl.sync();
+  TV* cur = xs0;
+  TV* nxt = xs1;
+  for (int k = 1; k < sweeps; ++k) {
+    if (owner) {
+      TV y[3] = {TV(0), TV(0), TV(0)};
+      if (gid[li] != 0) {
+#pragma unroll 3
+        for (int mm = 0; mm < 9; ++mm) {
+          const int m = p * 9 + mm;
+          const int jn = nbr[li * 27 + m];
+          if (jn < 0) continue;
+          const TV* S = sten + li * kStencil + m * 9;
+          const TV* xm = cur + jn * 18 + s_;
+          const TV x0 = xm[0], x1 = xm[6], x2 = xm[12];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) y[c] = fma_t(S[c * 3 + 0], x0, fma_t(S[c * 3 + 1], x1, fma_t(S[c * 3 + 2], x2, y[c])));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) part[(p * per + li) * 18 + c * 6 + s_] = y[c];
+    }
+    __syncthreads();
+    if (p == 0 && owner) {
+      TV v[3];
+      if (gid[li] == 0) {
+        v[0] = v[1] = v[2] = TV(0);
+      } else {
+        TV res[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int q = c * 6 + s_;
+          const TV yy = part[(0 * per + li) * 18 + q] + part[(1 * per + li) * 18 + q] + part[(2 * per + li) * 18 + q];
+          res[c] = bo[li * 18 + q] - yy;
+        }
+        const TV* D = dv + li * 6;
+        const TV* xo = cur + (n0 + li) * 18 + s_;
+        v[0] = fma_t(omega, D[0] * res[0] + D[1] * res[1] + D[2] * res[2], xo[0]);
+        v[1] = fma_t(omega, D[1] * res[0] + D[3] * res[1] + D[4] * res[2], xo[6]);
+        v[2] = fma_t(omega, D[2] * res[0] + D[4] * res[1] + D[5] * res[2], xo[12]);
+      }
+      for (int dst = 0; dst < kCoarseCluster; ++dst) {
+        TV* xr = cl.map_shared_rank(nxt, dst);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xr[(n0 + li) * 18 + c * 6 + s_] = v[c];
+      }
+    }
+    cl.sync();
+    TV* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  if (p == 0 && owner) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) xout[vbase(n0 + li, 18) + (c * 6 + s_) * 32] = cur[(n0 + li) * 18 + c * 6 + s_];
+  }
+}
+
+template <typename TV>
+size_t coarsest_smem_bytes(int n) {
+  const int per = (n + kCoarseCluster - 1) / kCoarseCluster;
+  return sizeof(TV) * (static_cast<size_t>(n) * 36 + static_cast<size_t>(per) * (kStencil + 18 + 6 + 54)) +
+         sizeof(int) * static_cast<size_t>(per) * 28;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -787,6 +925,32 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
   }
 }
 
+// false when the level does not fit the cluster kernel (caller keeps per-sweep launches)
+template <typename TV>
+bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xout, TV omega, int sweeps, const PcgState* st,
+                     cudaStream_t s) {
+  static const bool off = std::getenv("SHL_COARSE_LAUNCHES") != nullptr;  // A/B: one launch per sweep
+  const int per = (L.n + kCoarseCluster - 1) / kCoarseCluster;
+  const size_t smem = coarsest_smem_bytes<TV>(L.n);
+  if (off || L.n == 0 || per > 32 || smem > 227 * 1024) return false;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(coarsest_cluster_kernel<TV>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(coarsest_cluster_kernel<TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = true;
+  }
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
+  coarsest_cluster_kernel<TV><<<kCoarseCluster, 576, smem, s>>>(a, b, xout, omega, sweeps, st);
+  return true;
+}
+
+template <typename TB, typename TV, typename TO>
+void launch_level_sweep_out(const GmgLevelView<TV>& L, const TB* b, const TV* xin, TO* xout, TV omega,
+                            PcgState* st, double* partials, int init, int grid, cudaStream_t s) {
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
+  level_sweep3_kernel<TB, TV, true, TO><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, 2, st, partials, init);
+}
+
 template <typename TB, typename TV>
 void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
                          cudaStream_t s) {
@@ -822,6 +986,21 @@ template void launch_level_sweep<float, float>(const GmgLevelView<float>&, bool,
 template void launch_level_sweep<double, double>(const GmgLevelView<double>&, bool, const double*,
                                                  const double*, double*, double, int, PcgState*, double*,
                                                  int, int, cudaStream_t);
+template bool launch_coarsest<float>(const GmgLevelView<float>&, const float*, float*, float, int, const PcgState*,
+                                     cudaStream_t);
+template bool launch_coarsest<double>(const GmgLevelView<double>&, const double*, double*, double, int,
+                                      const PcgState*, cudaStream_t);
+template void launch_level_sweep_out<double, float, double>(const GmgLevelView<float>&, const double*,
+                                                           const float*, double*, float, PcgState*, double*,
+                                                           int, int, cudaStream_t);
+template void launch_level_sweep_out<double, float, float>(const GmgLevelView<float>&, const double*,
+                                                          const float*, float*, float, PcgState*, double*,
+                                                          int, int, cudaStream_t);
+template void launch_level_sweep_out<float, float, float>(const GmgLevelView<float>&, const float*, const float*,
+                                                          float*, float, PcgState*, double*, int, int, cudaStream_t);
+template void launch_level_sweep_out<double, double, double>(const GmgLevelView<double>&, const double*,
+                                                             const double*, double*, double, PcgState*, double*,
+                                                             int, int, cudaStream_t);
 template void launch_jacobi_first<double, float>(const GmgLevelView<float>&, const double*, float*, float,
                                                  const PcgState*, cudaStream_t);
 template void launch_jacobi_first<float, float>(const GmgLevelView<float>&, const float*, float*, float,

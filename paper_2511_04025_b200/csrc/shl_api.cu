@@ -14,11 +14,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "context.h"
@@ -29,6 +31,7 @@ namespace shl {
 namespace host {
 
 thread_local std::string g_thread_error;
+thread_local cudaStream_t g_alloc_stream = nullptr;
 
 __global__ void finalize_counts_kernel(Misc* m, const int* node_flag, const int* node_off,
                                        const int* elem_flag, const int* elem_off, int n3,
@@ -316,8 +319,9 @@ int gmg_setup(shl_ctx* c, const GmgParams& gp, TV ridge) {
   return L;
 }
 
-// Symmetric V(nu, nu) cycle: z = M r on level 0; returns the buffer holding z.
-template <typename TX, typename TV>
+// Symmetric V(nu, nu) cycle: z = M r on level 0, written by the last level-0
+// sweep into zout (type TO).
+template <typename TX, typename TV, typename TO>
 struct Vcycle {
   shl_ctx* c;
   GmgParams gp;
@@ -327,6 +331,8 @@ struct Vcycle {
   shl::PcgState* st;
   double* partials;
   int64_t launches = 0;
+  TO* zout = nullptr;
+  cudaStream_t s = nullptr;  // launch stream (the capture stream while recording the iteration graph)
 
   int grid(int n) const { return shl::apply_grid(n, c->num_sms); }
 
@@ -338,14 +344,18 @@ struct Vcycle {
     TV* oth = xb[l];
     auto sweep = [&](TV* xin, TV* xout, int mode) {
       if (fine)
-        shl::launch_level_sweep<TX, TV>(V, true, b0, xin, xout, w, mode, st, partials, init, grid(V.n), c->stream);
+        shl::launch_level_sweep<TX, TV>(V, true, b0, xin, xout, w, mode, st, partials, init, grid(V.n), s);
       else
         shl::launch_level_sweep<TV, TV>(V, false, b[l], xin, xout, w, mode, st, partials, init, grid(V.n),
-                                        c->stream);
+                                        s);
       ++launches;
     };
+    if (l == L && !fine && shl::launch_coarsest<TV>(V, b[l], cur, w, gp.coarse_sweeps, st, s)) {
+      ++launches;  // the whole coarsest solve in one cluster launch
+      return cur;
+    }
     if (!fine) {
-      shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, c->stream);
+      shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, s);
       ++launches;
     }  // level 0: the update kernel already wrote w Dinv r into xa[0]
     const int nu = gp.nu_at(l);
@@ -356,12 +366,17 @@ struct Vcycle {
     }
     if (l == L) return cur;
     sweep(cur, res[l], 1);
-    shl::launch_restrict<TV>(view[l + 1], V, res[l], b[l + 1], st, c->stream);
+    shl::launch_restrict<TV>(view[l + 1], V, res[l], b[l + 1], st, s);
     TV* xc = level(l + 1, b0, init);
-    shl::launch_prolong<TV>(V, view[l + 1], xc, cur, st, c->stream);
+    shl::launch_prolong<TV>(V, view[l + 1], xc, cur, st, s);
     launches += 2;
     for (int k = 1; k <= nu; ++k) {
-      sweep(cur, oth, (fine && k == nu) ? 2 : 0);
+      if (fine && k == nu) {
+        shl::launch_level_sweep_out<TX, TV, TO>(V, b0, cur, zout, w, st, partials, init, grid(V.n), s);
+        ++launches;
+        return nullptr;
+      }
+      sweep(cur, oth, 0);
       std::swap(cur, oth);
     }
     return cur;
@@ -380,6 +395,10 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   // 32-node blocked vectors (solver.cu vbase); node n is an always-zero row
   const int ld = round_up(n + 1, 32);
   const size_t nX = static_cast<size_t>(18) * ld, nV = nX;
+  // z: written by the update kernel (block Jacobi) or by the V-cycle's last
+  // sweep (multigrid) in TZ, read by the apply.  (An FP64 z for the FP64
+  // operator of mixed multigrid removes the FP32->FP64 conversions from the
+  // apply but doubles its L1 traffic; measured slower, 364 vs 330 us at 128^3.)
   c->vec.ensure(2 * nX * sizeof(TX) + 2 * nV * sizeof(TV) + (nV + 6 * static_cast<size_t>(ld)) * sizeof(TZ));
   TX* x = c->vec.as<TX>();
   TX* rv = x + nX;
@@ -422,7 +441,9 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   CK(cudaMemsetAsync(z, 0, nV * sizeof(TZ), c->stream));
   shl::launch_setup<TX, TZ>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), ridge, rv,
                             dinv, c->stream);
-  Vcycle<TX, TZ> vc{c, gmg_params()};
+  Vcycle<TX, TZ, TZ> vc{c, gmg_params()};
+  vc.zout = z;
+  vc.s = c->stream;
   if (vc.gp.nu <= 0) vc.gp.nu = sizeof(TV) == 8 ? 1 : 2;
   if (use_gmg) {
     vc.L = gmg_setup<TZ>(c, vc.gp, static_cast<TZ>(ridge));
@@ -471,7 +492,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   vc.st = dst;
   // z = M r: block Jacobi inside the update kernel, or the V-cycle
   auto precondition = [&](int init) {
-    if (use_gmg) aa.z = vc.level(0, rv, init);
+    if (use_gmg) vc.level(0, rv, init);
   };
   // z0 = M b, then w0 = A z0, p0 = z0, q0 = w0, alpha0
   shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
@@ -495,16 +516,21 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;  // kernel launches per graph replay
   if (use_graph) {
+    // recorded on a side stream: capture + instantiation (host work) overlap the
+    // device executing the setup and first iteration already queued on c->stream
     const int64_t before = launches + vc.launches;
     cudaGraph_t graph = nullptr;
-    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const cudaStream_t cs = c->cap_stream;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    vc.s = cs;
     for (int it = 0; it < kGraphIters; ++it) {
-      shl::launch_update<TX, TV, TZ>(ua, grid_u, c->stream);
+      shl::launch_update<TX, TV, TZ>(ua, grid_u, cs);
       precondition(0);
-      shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
+      shl::launch_apply<TV, TZ>(aa, grid_a, cs);
       launches += 2;
     }
-    CK(cudaStreamEndCapture(c->stream, &graph));
+    vc.s = c->stream;
+    CK(cudaStreamEndCapture(cs, &graph));
     CK(cudaGraphInstantiate(&gexec, graph, 0));
     CK(cudaGraphDestroy(graph));
     graph_launches = launches + vc.launches - before;
@@ -769,7 +795,14 @@ int shl_ctx_create(int device, shl_ctx** out) {
   int rc = guarded(nullptr, [&] {
     CK(cudaSetDevice(device));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    // keep freed stream-ordered workspace memory in the device pool (no trim at syncs)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     CK(cudaMallocHost(&c->hmisc, sizeof(Misc)));
     CK(cudaMallocHost(&c->hstate, sizeof(shl::PcgState)));
@@ -782,6 +815,7 @@ int shl_ctx_create(int device, shl_ctx** out) {
 
 void shl_ctx_destroy(shl_ctx* c) {
   if (!c) return;
+  for (shl_ctx* l : c->lanes) shl_ctx_destroy(l);
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->nccl && c->nccl_deleter) c->nccl_deleter(c->nccl);
@@ -793,6 +827,7 @@ void shl_ctx_destroy(shl_ctx* c) {
   if (c->hstate) cudaFreeHost(c->hstate);
   if (c->hC) cudaFreeHost(c->hC);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
 }
 
@@ -975,17 +1010,55 @@ int shl_homogenize(shl_ctx* c, const shl_design* design, const shl_shell_params*
   return guarded(c, [&] { homogenize_one(c, design, sp, mat, r, opt, C_out, st); });
 }
 
+int shl_set_batch_lanes(shl_ctx* c, int lanes) {
+  if (!c || lanes < 1 || lanes > 16) return SHL_VALIDATION;
+  c->n_lanes = lanes;
+  return SHL_OK;
+}
+
+// Designs are independent, so a batch keeps several in flight: lane 0 is this
+// context, lanes 1.. are sub-contexts on the same device (own stream, own
+// workspaces, created once), each driven by a host thread pulling the next
+// design index from a shared counter.  One design's latency-bound phases
+// (coarse multigrid levels, host polls, graph launch gaps) then overlap
+// another's bandwidth-bound kernels.
 int shl_homogenize_batch(shl_ctx* c, int n, const shl_design* designs, const shl_shell_params* sp,
                          const shl_material* mat, int r, const shl_solve_options* opt,
                          double* C_out, shl_stats* stats, int32_t* status) {
   if (!c || n < 0 || (n > 0 && (!designs || !C_out))) return SHL_VALIDATION;
-  for (int i = 0; i < n; ++i) {
-    shl_stats* st = stats ? stats + i : nullptr;
-    if (st) std::memset(st, 0, sizeof(*st));
-    const int rc =
-        guarded(c, [&] { homogenize_one(c, designs + i, sp, mat, r, opt, C_out + 36 * i, st); });
-    if (status) status[i] = rc;
-    if (rc == SHL_CUDA) return rc;
+  const int L = std::max(1, std::min(c->n_lanes, n));
+  while (static_cast<int>(c->lanes.size()) < L - 1) {
+    shl_ctx* sub = nullptr;
+    const int rc = shl_ctx_create(c->device, &sub);
+    if (rc != SHL_OK) return rc;
+    c->lanes.push_back(sub);
+  }
+  std::atomic<int> next{0};
+  std::atomic<int> device_failed{0};
+  std::string device_msg;
+  auto work = [&](shl_ctx* lc, int lane) {
+    cudaSetDevice(c->device);
+    lc->profiling = c->profiling;
+    for (;;) {
+      const int i = next.fetch_add(1);
+      if (i >= n || device_failed.load()) break;
+      shl_stats* st = stats ? stats + i : nullptr;
+      if (st) std::memset(st, 0, sizeof(*st));
+      const int rc =
+          guarded(lc, [&] { homogenize_one(lc, designs + i, sp, mat, r, opt, C_out + 36 * i, st); });
+      if (st) st->lane = lane;
+      if (status) status[i] = rc;
+      if (rc == SHL_CUDA && !device_failed.exchange(1)) device_msg = lc->err;
+    }
+  };
+  std::vector<std::thread> threads;
+  for (int l = 1; l < L; ++l) threads.emplace_back(work, c->lanes[l - 1], l);
+  work(c, 0);
+  for (auto& t : threads) t.join();
+  if (device_failed.load()) {
+    c->err = device_msg;
+    g_thread_error = device_msg;
+    return SHL_CUDA;
   }
   return SHL_OK;
 }

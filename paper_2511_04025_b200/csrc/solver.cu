@@ -21,6 +21,7 @@
 // Scalars never leave the device: the last block of each reduction kernel
 // (fixed-order sum of the per-block partials -> deterministic) updates the
 // PcgState, so the host only polls a flag every few iterations.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -627,10 +628,11 @@ __global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV, TZ> A) 
 }
 
 // FP64 operator: six warps per 32 nodes, warp (plane p, half h) gathers plane
-// dz=p-1 for load cases 3h..3h+2, then finishes load case s = 3h + p.
-template <typename TZ>
-__global__ void __launch_bounds__(384, sizeof(TZ) == 4 ? 2 : 1) apply6_kernel(const ApplyArgs<double, TZ> A) {
-  __shared__ __align__(16) double part_s[2][3 * 18 * 32];
+// dz=p-1 for load cases 3h..3h+2, then finishes load case s = 3h + p.  G groups
+// of six warps per block, MINB blocks per SM (register budget).
+template <typename TZ, int G, int MINB>
+__global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<double, TZ> A) {
+  __shared__ __align__(16) double part_s[G][3 * 18 * 32];
   __shared__ double scratch[32 * 6];
   PcgState* st = A.state;
   if (st->stop) return;
@@ -644,8 +646,8 @@ __global__ void __launch_bounds__(384, sizeof(TZ) == 4 ? 2 : 1) apply6_kernel(co
   const bool dn = st->done[s_] != 0;
   const double bcoef = st->beta[s_];
   double pq = 0.0;
-  for (int tile = blockIdx.x; tile * 64 < A.n; tile += gridDim.x) {
-    const int idx = tile * 64 + grp * 32 + lane;
+  for (int tile = blockIdx.x; tile * (32 * G) < A.n; tile += gridDim.x) {
+    const int idx = tile * (32 * G) + grp * 32 + lane;
     const bool valid = idx < A.n;
     const int g = valid ? A.node_list[idx] : -1;
     {
@@ -997,8 +999,25 @@ void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s) {
   }
   if constexpr (sizeof(TV) == 8) {
     static const bool three = std::getenv("SHL_APPLY3") != nullptr;  // A/B: three-warp FP64 variant
+    static const int variant = [] {  // A/B: SHL_APPLY6 = 22 (2 groups, 2 blocks/SM), 13, 14
+      const char* e = std::getenv("SHL_APPLY6");
+      return e ? std::atoi(e) : 22;
+    }();
     if (!three) {
-      apply6_kernel<TZ><<<grid, 384, 0, s>>>(a);
+      // one CTA per resident slot: the grid-stride loop then has no tail wave
+      static const int nsm = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+      }();
+      if (variant == 22) {
+        apply6_kernel<TZ, 2, 2><<<std::min(grid, 2 * nsm), 384, 0, s>>>(a);
+      } else if (variant == 14) {
+        apply6_kernel<TZ, 1, 4><<<std::min(grid, 4 * nsm), 192, 0, s>>>(a);
+      } else {
+        apply6_kernel<TZ, 1, 3><<<std::min(grid, 3 * nsm), 192, 0, s>>>(a);
+      }
       return;
     }
   }

@@ -229,6 +229,24 @@ def test_batch_matches_single(S):
         assert np.array_equal(Cs, Cb[i])  # deterministic reductions
 
 
+@pytest.mark.parametrize("r,lanes", [(32, 3), (64, 4)])
+def test_batch_lanes_match_single(S, r, lanes):
+    """Designs in flight on concurrent lanes give bit-identical C^H and iteration
+    counts (each design's reductions are fixed-order, whatever runs beside it)."""
+    designs = [S.random_design(S.RandomDesignSpec("cubic_octant", 4), s) for s in range(7)]
+    opt = S.HomogenizeOptions(residual_tol=1e-5, precision="mixed")
+    ctx = S.Context(0)
+    Cb, status, stats = S.homogenize_batch(designs, S.ShellParams(), S.BaseMaterial(), r, opt,
+                                           ctx=ctx, lanes=lanes)
+    assert np.all(status == 0)
+    assert len({s.lane for s in stats}) > 1
+    for i, d in enumerate(designs):
+        res = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, opt, ctx=ctx)
+        assert np.array_equal(res.tensor, Cb[i])
+        assert np.array_equal(res.iterations, stats[i].iterations)
+    ctx.close()
+
+
 @pytest.mark.parametrize("r,G,prec,tol", [(16, 2, "fp64", 1e-10), (32, 3, "mixed", 1e-6),
                                           (32, 4, "fp32", 1e-5), (64, 8, "mixed", 1e-5)])
 def test_zslab_matches_single_device(S, r, G, prec, tol):
