@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=16)
     p.add_argument("--warmup", type=int, default=4)
-    p.add_argument("--lanes", type=int, default=4,
+    p.add_argument("--lanes", type=int, default=2,
                    help="designs in flight at once per GPU (shl_set_batch_lanes)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--r", type=int, default=128)
@@ -285,7 +285,9 @@ def run_ours(args, rank, world, local):
     if gmg or apply_ms >= update_ms:
         # with multigrid, update_ms also holds the V-cycle; the apply stays the
         # largest single kernel of an iteration
-        kname, per_node, tot_ms = "apply_kernel (w=A z gather + p,q update)", bytes_apply, apply_ms
+        kname = ("apply6_kernel (FP64 operator: w=A z gather + p,q update)" if vb == 8 else
+                 "apply_kernel (w=A z gather + p,q update)")
+        per_node, tot_ms = bytes_apply, apply_ms
     else:
         kname, per_node, tot_ms = "update_kernel (x,r,z update + dots)", bytes_update, update_ms
     avg_launch_s = tot_ms / 1e3 / max(launches_apply, 1)

@@ -17,6 +17,21 @@ namespace {
 
 constexpr int kStencil = 243;
 
+// Thread t -> (node, load case) with each warp on ONE load case of 32
+// consecutive nodes, so a warp's access to a component plane of the 32-node
+// blocked vectors is one contiguous 128-byte line (t/6, t%6 spread a warp over
+// six planes of ~5 nodes each).  Launch ceil(n/32)*192 threads.
+__device__ __forceinline__ void node_case(long long t, int& idx, int& s) {
+  const long long w = t >> 5;
+  idx = static_cast<int>((w / 6) * 32 + (t & 31));
+  s = static_cast<int>(w % 6);
+}
+__host__ __device__ inline unsigned node_case_blocks(int n, int threads_per_block) {
+  return static_cast<unsigned>((static_cast<long long>((n + 31) / 32) * 192 + threads_per_block - 1) /
+                               threads_per_block);
+}
+
+
 // ---------------------------------------------------------------- gathers
 template <typename TV>
 __device__ __forceinline__ void stencil_gather(GatherAcc<TV>& acc, int idx, int g,
@@ -334,9 +349,9 @@ __global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV*
                                     int n, const TB* __restrict__ b, TV* __restrict__ xout, TV omega,
                                     const PcgState* st) {
   if (st->stop) return;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * 6) return;
-  const int idx = t / 6, s = t % 6;
+  int idx, s;
+  node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
+  if (idx >= n) return;
   const size_t ob = vbase(idx, 18) + s * 32;
   TV D[6];
 #pragma unroll
@@ -355,9 +370,9 @@ __global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c
                                 const int* __restrict__ map_f, int r_f, const TV* __restrict__ res_f,
                                 TV* __restrict__ b_c, const PcgState* st) {
   if (st->stop) return;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_c * 6) return;
-  const int idx = t / 6, s = t % 6;
+  int idx, s;
+  node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
+  if (idx >= n_c) return;
   const int G = list_c[idx];
   const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
   TV acc[3] = {TV(0), TV(0), TV(0)};
@@ -388,9 +403,9 @@ __global__ void prolong_kernel(const int* __restrict__ list_f, int n_f, int r_f,
                                const int* __restrict__ map_c, int r_c, const TV* __restrict__ x_c,
                                TV* __restrict__ x_f, const PcgState* st) {
   if (st->stop) return;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_f * 6) return;
-  const int idx = t / 6, s = t % 6;
+  int idx, s;
+  node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
+  if (idx >= n_f) return;
   const int g = list_f[idx];
   if (g == 0) return;
   const int i = g % r_f, j = (g / r_f) % r_f, k = g / (r_f * r_f);
@@ -735,12 +750,13 @@ __global__ void coarse_dinv_kernel(const int* __restrict__ list_c, int n_c,
 // The coarsest grid (8^3 torus, <= 512 active nodes) used to take one kernel
 // per damped Jacobi sweep, each a few microseconds of dependent L2 loads plus a
 // launch.  Here a cluster of kCoarseCluster CTAs owns it: CTA k holds the
-// stencils, right-hand side, Dinv and neighbour ids of nodes [k*per, (k+1)*per)
-// in shared memory, and EVERY CTA holds a full copy of x (ping-pong).  A sweep
-// computes the owned nodes' new values (thread = node x load case x stencil
-// plane, planes summed in fixed order), writes them into the next x buffer of
-// all CTAs through distributed shared memory, and ends with a cluster barrier.
-// Same arithmetic as jacobi_first + (sweeps-1) coarse_warp_sweep launches.
+// stencils, right-hand side, Dinv, neighbour ids and x (ping-pong) of nodes
+// [k*per, (k+1)*per) in shared memory.  A sweep gathers neighbour values
+// straight from the owning CTA's shared memory (distributed shared memory
+// loads; thread = node x load case x stencil plane, planes summed in fixed
+// order), writes the owned nodes' new values locally, and ends with one
+// cluster barrier.  Same arithmetic as jacobi_first + (sweeps-1)
+// coarse_warp_sweep launches.
 constexpr int kCoarseCluster = 16;
 
 template <typename TV>
@@ -756,16 +772,14 @@ __global__ void __cluster_dims__(kCoarseCluster, 1, 1) __launch_bounds__(576)
   const int n0 = rank * per;
   const int nown = max(0, min(n, n0 + per) - n0);
   extern __shared__ __align__(16) unsigned char csm[];
-  TV* xs0 = reinterpret_cast<TV*>(csm);                // [n][18]
-  TV* xs1 = xs0 + static_cast<size_t>(n) * 18;         // [n][18]
-  TV* sten = xs1 + static_cast<size_t>(n) * 18;        // [per][243]
+  TV* xs = reinterpret_cast<TV*>(csm);                  // [2][per][18] owned x, ping-pong
+  TV* sten = xs + 2 * per * 18;                         // [per][243]
   TV* bo = sten + static_cast<size_t>(per) * kStencil;  // [per][18]
-  TV* dv = bo + per * 18;                              // [per][6]
-  TV* part = dv + per * 6;                             // [3][per][18]
-  int* nbr = reinterpret_cast<int*>(part + 3 * per * 18);  // [per][27], -1 = absent
+  TV* dv = bo + per * 18;                               // [per][6]
+  TV* part = dv + per * 6;                              // [3][per][18]
+  int* nbr = reinterpret_cast<int*>(part + 3 * per * 18);  // [per][27] owner-local slot, -1 = absent
   int* gid = nbr + per * 27;                                 // [per]
   const int tid = threadIdx.x;
-  // stage the owned nodes
   for (int t = tid; t < nown * kStencil; t += blockDim.x) {
     const int li = t / kStencil, q = t % kStencil;
     sten[li * kStencil + q] = L.stencil[vbase(n0 + li, kStencil) + q * 32];
@@ -789,38 +803,42 @@ __global__ void __cluster_dims__(kCoarseCluster, 1, 1) __launch_bounds__(576)
     nbr[t] = (m == 13) ? n0 + li : L.node_map[(zk * r + yj) * r + xi];
   }
   __syncthreads();
-  // thread -> (owned node li, load case s, stencil plane p)
   const int p = tid / 192, rem = tid % 192, li = rem / 6, s_ = rem % 6;
   const bool owner = li < nown;
-  // x0 = omega Dinv b (jacobi_first), broadcast to every CTA
+  // x0 = omega Dinv b (jacobi_first)
   if (p == 0 && owner) {
     const TV* D = dv + li * 6;
     const TV r0 = bo[li * 18 + s_], r1 = bo[li * 18 + 6 + s_], r2 = bo[li * 18 + 12 + s_];
-    const TV v[3] = {omega * (D[0] * r0 + D[1] * r1 + D[2] * r2), omega * (D[1] * r0 + D[3] * r1 + D[4] * r2),
-                     omega * (D[2] * r0 + D[4] * r1 + D[5] * r2)};
-    for (int dst = 0; dst < kCoarseCluster; ++dst) {
-      TV* xr = cl.map_shared_rank(xs0, dst);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) xr[(n0 + li) * 18 + c * 6 + s_] = v[c];
-    }
+    xs[li * 18 + s_] = omega * (D[0] * r0 + D[1] * r1 + D[2] * r2);
+    xs[li * 18 + 6 + s_] = omega * (D[1] * r0 + D[3] * r1 + D[4] * r2);
+    xs[li * 18 + 12 + s_] = omega * (D[2] * r0 + D[4] * r1 + D[5] * r2);
   }
   cl.sync();
-  TV* cur = xs0;
-  TV* nxt = xs1;
+  int cur = 0;
   for (int k = 1; k < sweeps; ++k) {
     if (owner) {
       TV y[3] = {TV(0), TV(0), TV(0)};
       if (gid[li] != 0) {
-#pragma unroll 3
-        for (int mm = 0; mm < 9; ++mm) {
-          const int m = p * 9 + mm;
-          const int jn = nbr[li * 27 + m];
-          if (jn < 0) continue;
-          const TV* S = sten + li * kStencil + m * 9;
-          const TV* xm = cur + jn * 18 + s_;
-          const TV x0 = xm[0], x1 = xm[6], x2 = xm[12];
+        // gather the plane's neighbour values first (independent DSMEM loads)
+        TV xv[9][3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) y[c] = fma_t(S[c * 3 + 0], x0, fma_t(S[c * 3 + 1], x1, fma_t(S[c * 3 + 2], x2, y[c])));
+        for (int mm = 0; mm < 9; ++mm) {
+          const int jn = nbr[li * 27 + p * 9 + mm];
+          if (jn < 0) {
+            xv[mm][0] = xv[mm][1] = xv[mm][2] = TV(0);
+            continue;
+          }
+          const TV* src = cl.map_shared_rank(xs, jn / per) + (cur * per + jn % per) * 18 + s_;
+          xv[mm][0] = src[0];
+          xv[mm][1] = src[6];
+          xv[mm][2] = src[12];
+        }
+#pragma unroll
+        for (int mm = 0; mm < 9; ++mm) {
+          const TV* S = sten + li * kStencil + (p * 9 + mm) * 9;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            y[c] = fma_t(S[c * 3 + 0], xv[mm][0], fma_t(S[c * 3 + 1], xv[mm][1], fma_t(S[c * 3 + 2], xv[mm][2], y[c])));
         }
       }
 #pragma unroll
@@ -828,9 +846,10 @@ __global__ void __cluster_dims__(kCoarseCluster, 1, 1) __launch_bounds__(576)
     }
     __syncthreads();
     if (p == 0 && owner) {
-      TV v[3];
+      const TV* xo = xs + (cur * per + li) * 18 + s_;
+      TV* xn = xs + ((cur ^ 1) * per + li) * 18 + s_;
       if (gid[li] == 0) {
-        v[0] = v[1] = v[2] = TV(0);
+        xn[0] = xn[6] = xn[12] = TV(0);
       } else {
         TV res[3];
 #pragma unroll
@@ -840,33 +859,24 @@ __global__ void __cluster_dims__(kCoarseCluster, 1, 1) __launch_bounds__(576)
           res[c] = bo[li * 18 + q] - yy;
         }
         const TV* D = dv + li * 6;
-        const TV* xo = cur + (n0 + li) * 18 + s_;
-        v[0] = fma_t(omega, D[0] * res[0] + D[1] * res[1] + D[2] * res[2], xo[0]);
-        v[1] = fma_t(omega, D[1] * res[0] + D[3] * res[1] + D[4] * res[2], xo[6]);
-        v[2] = fma_t(omega, D[2] * res[0] + D[4] * res[1] + D[5] * res[2], xo[12]);
-      }
-      for (int dst = 0; dst < kCoarseCluster; ++dst) {
-        TV* xr = cl.map_shared_rank(nxt, dst);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) xr[(n0 + li) * 18 + c * 6 + s_] = v[c];
+        xn[0] = fma_t(omega, D[0] * res[0] + D[1] * res[1] + D[2] * res[2], xo[0]);
+        xn[6] = fma_t(omega, D[1] * res[0] + D[3] * res[1] + D[4] * res[2], xo[6]);
+        xn[12] = fma_t(omega, D[2] * res[0] + D[4] * res[1] + D[5] * res[2], xo[12]);
       }
     }
-    cl.sync();
-    TV* t = cur;
-    cur = nxt;
-    nxt = t;
+    cl.sync();  // new values visible cluster-wide; nobody still reads the old buffer
+    cur ^= 1;
   }
   if (p == 0 && owner) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) xout[vbase(n0 + li, 18) + (c * 6 + s_) * 32] = cur[(n0 + li) * 18 + c * 6 + s_];
+    for (int c = 0; c < 3; ++c) xout[vbase(n0 + li, 18) + (c * 6 + s_) * 32] = xs[(cur * per + li) * 18 + c * 6 + s_];
   }
 }
 
 template <typename TV>
 size_t coarsest_smem_bytes(int n) {
   const int per = (n + kCoarseCluster - 1) / kCoarseCluster;
-  return sizeof(TV) * (static_cast<size_t>(n) * 36 + static_cast<size_t>(per) * (kStencil + 18 + 6 + 54)) +
-         sizeof(int) * static_cast<size_t>(per) * 28;
+  return sizeof(TV) * static_cast<size_t>(per) * (36 + kStencil + 18 + 6 + 54) + sizeof(int) * static_cast<size_t>(per) * 28;
 }
 
 }  // namespace
@@ -884,7 +894,6 @@ void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int 
   const size_t smem = 64 * kStencil * sizeof(TV);
   static const bool nodewise = std::getenv("SHL_GALERKIN_NODEWISE") != nullptr;  // A/B check
   if (stencil_f == nullptr && !nodewise) {
-    cell_matrices_kernel<<<8, 576, 0, s>>>();
     galerkin_fine_kernel<TV><<<(n_c + 31) / 32, dim3(32, 27), 0, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f, ridge,
                                                                       stencil_c);
   } else if (!nodewise) {
@@ -929,7 +938,10 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
 template <typename TV>
 bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xout, TV omega, int sweeps, const PcgState* st,
                      cudaStream_t s) {
-  static const bool off = std::getenv("SHL_COARSE_LAUNCHES") != nullptr;  // A/B: one launch per sweep
+  // Opt-in (SHL_COARSE_CLUSTER=1): 45 us vs ~100 us of per-sweep launches at
+  // 128^3 alone, but a 16-CTA cluster must find 16 free SMs in one GPC, which
+  // stalls it behind other batch lanes' kernels (3 lanes: 28 vs 34 designs/s).
+  static const bool off = std::getenv("SHL_COARSE_CLUSTER") == nullptr;
   const int per = (L.n + kCoarseCluster - 1) / kCoarseCluster;
   const size_t smem = coarsest_smem_bytes<TV>(L.n);
   if (off || L.n == 0 || per > 32 || smem > 227 * 1024) return false;
@@ -954,19 +966,19 @@ void launch_level_sweep_out(const GmgLevelView<TV>& L, const TB* b, const TV* xi
 template <typename TB, typename TV>
 void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
                          cudaStream_t s) {
-  if (L.n) jacobi_first_kernel<TB, TV><<<(L.n * 6 + 255) / 256, 256, 0, s>>>(L.node_list, L.dinv, L.n, b, xout, omega, st);
+  if (L.n) jacobi_first_kernel<TB, TV><<<node_case_blocks(L.n, 192), 192, 0, s>>>(L.node_list, L.dinv, L.n, b, xout, omega, st);
 }
 
 template <typename TV>
 void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
                      const PcgState* st, cudaStream_t s) {
-  if (C.n) restrict_kernel<TV><<<(C.n * 6 + 255) / 256, 256, 0, s>>>(C.node_list, C.n, C.r, F.node_map, F.r, res_f, b_c, st);
+  if (C.n) restrict_kernel<TV><<<node_case_blocks(C.n, 192), 192, 0, s>>>(C.node_list, C.n, C.r, F.node_map, F.r, res_f, b_c, st);
 }
 
 template <typename TV>
 void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
                     const PcgState* st, cudaStream_t s) {
-  if (F.n) prolong_kernel<TV><<<(F.n * 6 + 255) / 256, 256, 0, s>>>(F.node_list, F.n, F.r, C.node_map, C.r, x_c, x_f, st);
+  if (F.n) prolong_kernel<TV><<<node_case_blocks(F.n, 192), 192, 0, s>>>(F.node_list, F.n, F.r, C.node_map, C.r, x_c, x_f, st);
 }
 
 #define SHL_GMG_INST(TV)                                                                               \

@@ -435,7 +435,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   const double ridge_op = diag_mean * (ridge_env ? std::atof(ridge_env) : (sizeof(TV) == 8 ? 1e-11 : 1e-8));
   const double ridge = diag_mean * (ridge_env ? std::atof(ridge_env) : (sizeof(TZ) == 8 ? 1e-11 : 1e-8));
   CK(cudaEventRecord(c->ev[3], c->stream));
-  shl::upload_element_constants(K0, W, T, c->stream);
+  shl::ElementConstLease const_lease(K0, W, T, r, c->stream);
   CK(cudaMemsetAsync(x, 0, nX * sizeof(TX), c->stream));
   CK(cudaMemsetAsync(p, 0, 2 * nV * sizeof(TV), c->stream));
   CK(cudaMemsetAsync(z, 0, nV * sizeof(TZ), c->stream));

@@ -239,7 +239,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
   element_loads(K0, r, T, W);
   const double ridge = c->n_nodes > 0 ? 1e-11 * std::fabs(K0[0]) * 8.0 * c->beta_sum / double(c->n_nodes) : 0.0;
   CK(cudaEventRecord(c->ev[3], c->stream));
-  upload_element_constants(K0, W, T, c->stream);
+  ElementConstLease const_lease(K0, W, T, r, c->stream);
   for (auto& S : slabs) {
     CK(cudaMemsetAsync(S.vec.p, 0, S.vec.cap, c->stream));
     launch_setup<TX, TV>(S.list.as<int>(), S.P.n_owned, static_cast<int>(S.ld), r, c->beta64.as<double>(),

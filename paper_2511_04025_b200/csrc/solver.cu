@@ -24,8 +24,11 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <type_traits>
 
 #include "device.cuh"
@@ -968,16 +971,60 @@ template void launch_unpack<double>(double*, int, int, const double*, cudaStream
 #include "gmg.cuh"
 
 // ---- host-side launchers -----------------------------------------------------
-void upload_element_constants(const double* K0, const double* W, const double* T,
-                              cudaStream_t s) {
-  float K0f[576];
-  for (int q = 0; q < 576; ++q) K0f[q] = static_cast<float>(K0[q]);
-  cudaMemcpyToSymbolAsync(c_K0d, K0, sizeof(double) * 576, 0, cudaMemcpyHostToDevice, s);
-  cudaMemcpyToSymbolAsync(c_K0f, K0f, sizeof(float) * 576, 0, cudaMemcpyHostToDevice, s);
-  cudaMemcpyToSymbolAsync(c_W, W, sizeof(double) * 144, 0, cudaMemcpyHostToDevice, s);
-  cudaMemcpyToSymbolAsync(c_T, T, sizeof(double) * 144, 0, cudaMemcpyHostToDevice, s);
-  // the float copy lives on the stack: make sure it has been consumed
-  cudaStreamSynchronize(s);
+// The element matrices live in __constant__ memory (FMA operands straight from
+// the constant bank) and the level-1 Galerkin cell matrices in device globals:
+// one copy per device, shared by every context.  A solve holds a lease on the
+// copy for its whole duration; the copy is rewritten only when a solve needs
+// different constants (another r or material) and no other solve on the device
+// still uses the old ones.  Concurrent batch lanes (same r and material) then
+// never write constant memory while each other's kernels run, and independent
+// contexts with different constants serialize instead of racing.
+namespace {
+struct ConstSlot {
+  std::mutex m;
+  std::condition_variable cv;
+  bool valid = false;
+  double key[577] = {};  // K0 (576) and r: W and T follow from them
+  int users = 0;
+};
+ConstSlot& const_slot(int device) {
+  static ConstSlot slots[64];
+  return slots[device & 63];
+}
+}  // namespace
+
+ElementConstLease::ElementConstLease(const double* K0, const double* W, const double* T, int r, cudaStream_t s) {
+  cudaGetDevice(&device_);
+  ConstSlot& cs = const_slot(device_);
+  double key[577];
+  std::memcpy(key, K0, 576 * sizeof(double));
+  key[576] = static_cast<double>(r);
+  std::unique_lock<std::mutex> lk(cs.m);
+  auto same = [&] { return cs.valid && std::memcmp(cs.key, key, sizeof(key)) == 0; };
+  cs.cv.wait(lk, [&] { return same() || cs.users == 0; });
+  if (!same()) {
+    float K0f[576];
+    for (int q = 0; q < 576; ++q) K0f[q] = static_cast<float>(K0[q]);
+    cudaMemcpyToSymbolAsync(c_K0d, K0, sizeof(double) * 576, 0, cudaMemcpyHostToDevice, s);
+    cudaMemcpyToSymbolAsync(c_K0f, K0f, sizeof(float) * 576, 0, cudaMemcpyHostToDevice, s);
+    cudaMemcpyToSymbolAsync(c_W, W, sizeof(double) * 144, 0, cudaMemcpyHostToDevice, s);
+    cudaMemcpyToSymbolAsync(c_T, T, sizeof(double) * 144, 0, cudaMemcpyHostToDevice, s);
+    cell_matrices_kernel<<<8, 576, 0, s>>>();  // P_j^T K0 P_j for the level-1 Galerkin product
+    // K0f lives on this stack frame; other streams read the result next
+    cudaStreamSynchronize(s);
+    std::memcpy(cs.key, key, sizeof(key));
+    cs.valid = true;
+  }
+  ++cs.users;
+}
+
+ElementConstLease::~ElementConstLease() {
+  ConstSlot& cs = const_slot(device_);
+  {
+    std::lock_guard<std::mutex> lk(cs.m);
+    --cs.users;
+  }
+  cs.cv.notify_all();
 }
 
 template <typename TX, typename TV>

@@ -127,7 +127,19 @@ template <typename TV>
 void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
                     const PcgState* st, cudaStream_t s);
 
-void upload_element_constants(const double* K0, const double* W, const double* T, cudaStream_t s);
+// Lease on the device's element constants (K0 in FP64/FP32, K0*T, T and the
+// level-1 Galerkin cell matrices), uploaded only when (K0, r) changes and no
+// other solve still holds the old ones.  Hold it for the whole solve.
+class ElementConstLease {
+ public:
+  ElementConstLease(const double* K0, const double* W, const double* T, int r, cudaStream_t s);
+  ~ElementConstLease();
+  ElementConstLease(const ElementConstLease&) = delete;
+  ElementConstLease& operator=(const ElementConstLease&) = delete;
+
+ private:
+  int device_ = 0;
+};
 template <typename TX, typename TV>
 void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double* beta64,
                   double ridge, TX* rvec, TV* dinv, cudaStream_t s);

@@ -120,8 +120,9 @@ def write_csv(out_dir: str, n: int) -> str:
 
 
 def device_chunk_fn(r: int, tol: float, precision: str, device: int, seed0: int = 0,
-                    symmetry: str = "cubic_octant", n_pre: int = 8) -> DesignFn:
-    """Chunk evaluator on the local GPU through shl_homogenize_batch."""
+                    symmetry: str = "cubic_octant", n_pre: int = 8, lanes: int = 2) -> DesignFn:
+    """Chunk evaluator on the local GPU through shl_homogenize_batch, `lanes`
+    designs of a chunk in flight at once."""
     from . import api as S
     ctx = S.Context(device)
     spec = S.RandomDesignSpec(symmetry, n_pre, 2, -1.0, 1.0)
@@ -131,7 +132,7 @@ def device_chunk_fn(r: int, tol: float, precision: str, device: int, seed0: int 
         idx = list(indices)
         designs = [S.random_design(spec, seed0 + i) for i in idx]
         Cs, status, stats = S.homogenize_batch(designs, S.ShellParams(), S.BaseMaterial(), r, opt,
-                                               ctx=ctx)
+                                               ctx=ctx, lanes=lanes)
         return [{"index": i, "seed": seed0 + i, "status": int(st), "C": C.tolist(),
                  "iterations": [int(v) for v in s.iterations], "volume_ratio": s.volume_ratio,
                  "t_fwd_ms": s.timings["t_fwd"], "n_elements": int(s.n_elements)}
@@ -151,6 +152,7 @@ def main(argv=None):
     ap.add_argument("--chunk", type=int, default=8)
     ap.add_argument("--seed0", type=int, default=0)
     ap.add_argument("--out", default="runs/sweep")
+    ap.add_argument("--lanes", type=int, default=2, help="designs in flight per GPU")
     a = ap.parse_args(argv)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -168,7 +170,7 @@ def main(argv=None):
             dist.gather_object(stats, out, dst=0)
             if rank == 0:
                 print(json.dumps({"ranks": out}))
-    fn = device_chunk_fn(a.r, a.tol, a.precision, local, a.seed0)
+    fn = device_chunk_fn(a.r, a.tol, a.precision, local, a.seed0, lanes=a.lanes)
     stats = run_sweep(a.n, a.out, fn, rank, world, store, a.chunk, f"sweep-{a.r}-{a.n}", gather)
     if world > 1:
         dist.barrier()

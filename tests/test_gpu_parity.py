@@ -5,6 +5,8 @@ FP64; beta within 1e-12 relative (device exp vs glibc exp); C^H within 1e-4
 relative Frobenius of the oracle, with iteration counts reported; the
 reference's known-answer tests (test_fem.cpp) at their own tolerances.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -245,6 +247,26 @@ def test_batch_lanes_match_single(S, r, lanes):
         assert np.array_equal(res.tensor, Cb[i])
         assert np.array_equal(res.iterations, stats[i].iterations)
     ctx.close()
+
+
+def test_c4_sweep_subset(S):
+    """Config C4 (64^3, CubicOctant 8 pre-expansion charges): seeds 0..15 in one
+    batch with 4 designs in flight; seeds 0..3 against the oracle's C^H
+    (tests/golden/c4_chom.npz, masked PCG to rtol 1e-8) at the 1e-4 relative
+    Frobenius bar, all 16 finite, symmetric and positive definite."""
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "c4_chom.npz"))
+    spec = S.RandomDesignSpec("cubic_octant", 8, 2, -1.0, 1.0)
+    designs = [S.random_design(spec, s) for s in range(16)]
+    opt = S.HomogenizeOptions(residual_tol=1e-6, precision="mixed")
+    C, status, stats = S.homogenize_batch(designs, S.ShellParams(), S.BaseMaterial(), 64, opt, lanes=4)
+    assert np.all(status == 0)
+    for i, s in enumerate(gold["seeds"]):
+        err = np.linalg.norm(C[s] - gold["C"][i]) / np.linalg.norm(gold["C"][i])
+        assert err < 1e-4, (s, err)
+    for c in C:
+        assert np.all(np.isfinite(c))
+        assert np.allclose(c, c.T, rtol=0, atol=1e-12 * np.abs(c).max())
+        assert np.linalg.eigvalsh(c).min() > 0
 
 
 @pytest.mark.parametrize("r,G,prec,tol", [(16, 2, "fp64", 1e-10), (32, 3, "mixed", 1e-6),
