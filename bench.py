@@ -99,6 +99,28 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        # in-process NVML when available (a spawned nvidia-smi every few hundred
+        # ms contends with the CUDA driver of the process being timed)
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            reasons_fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+            while not self._stop.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                    rs = reasons_fn(h)
+                    self.samples.append([str(sm), str(mx), hex(rs)] +
+                                        ["Active" if rs & b else "Not Active" for b in bits])
+                except Exception:
+                    pass
+                self._stop.wait(0.25)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -108,7 +130,7 @@ class ClockSampler:
                     self.samples.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.5)
 
     def __enter__(self):
         self._t.start()
@@ -183,6 +205,7 @@ def run_reference(args, rank, world):
         return
     threads = os.cpu_count() or 1
     warm, timed = seeds_for(0, args.steps, 0)
+    timed = timed[:12]  # ~12 s of CPU work per design: keep the whole arm within a few minutes
     times, samples = [], []
     for s in timed:
         r = cpu_reference_design(s, args, threads)
@@ -195,7 +218,7 @@ def run_reference(args, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference", "config": config(args, 1),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} designs at {args.r}^3: field+mesh in full "
+                             "sample": f"{len(timed)} designs at {args.r}^3: field+mesh in full "
                                        f"({samples[0]['field_from']}), {args.cpu_iters} masked PCG "
                                        f"iterations timed, solve extrapolated to the design's "
                                        f"lockstep count (~{samples[0]['iters']})"},

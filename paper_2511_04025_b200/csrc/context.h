@@ -153,7 +153,18 @@ struct shl_ctx {
   int n_lanes = 1;
   std::vector<shl_ctx*> lanes;
 
-  void sync() { CK(cudaStreamSynchronize(stream)); }
+  // Host waits block (yield the core) instead of spinning: batch lanes each
+  // wait on their own stream, and spinning threads starved the other lanes'
+  // host work (graph launches, polls) when the process has few cores.
+  cudaEvent_t sync_ev = nullptr;
+  void sync() {
+    if (!sync_ev) {
+      CK(cudaStreamSynchronize(stream));
+      return;
+    }
+    CK(cudaEventRecord(sync_ev, stream));
+    CK(cudaEventSynchronize(sync_ev));
+  }
   float ms(int a, int b) {
     float t = 0.f;
     CK(cudaEventElapsedTime(&t, ev[a], ev[b]));

@@ -175,7 +175,13 @@ __global__ void __launch_bounds__(192)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = w / 3, part = w % 3;
   double gam2[2] = {0, 0};
-  for (int tile = blockIdx.x; tile * 64 < L.n; tile += gridDim.x) {
+  // tiles from the shared counter; mode 2 reduces r.z per tile (fixed order,
+  // see apply6_kernel) so the sum does not depend on which CTA ran which tile
+  __shared__ double red[2][6];
+  for (;;) {
+    const int tile = grab_tile(&st->tile_next[1]);
+    if (tile * 64 >= L.n) break;
+    gam2[0] = gam2[1] = 0.0;
     const int idx = tile * 64 + grp * 32 + lane;
     const bool valid = idx < L.n;
     const int g = valid ? L.node_list[idx] : -1;
@@ -241,21 +247,36 @@ __global__ void __launch_bounds__(192)
         }
       }
     }
-    __syncthreads();
-  }
-  if (mode != 2) return;
-  double gam[6];
+    if (mode == 2) {
 #pragma unroll
-  for (int s_ = 0; s_ < 6; ++s_) gam[s_] = (s_ >> 1) == part ? gam2[s_ & 1] : 0.0;
-  block_sum<6>(gam, scratch);
-  if (publish_partial<6>(gam, partials, &st->counter_misc)) {
-    double tot[6];
-    __syncthreads();
-    reduce_partials<6>(partials, tot, scratch);
-    if (threadIdx.x == 0) {
-      finalize_gamma_state(st, tot, init);
-      st->counter_misc = 0;
+      for (int k = 0; k < 2; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gam2[k] += __shfl_xor_sync(0xffffffffu, gam2[k], o);
+        if (lane == 0) red[grp][2 * part + k] = gam2[k];
+      }
     }
+    __syncthreads();
+    if (mode == 2 && threadIdx.x < 6) partials[tile * 6 + threadIdx.x] = red[0][threadIdx.x] + red[1][threadIdx.x];
+  }
+  tiles_done(&st->tile_next[1], &st->tile_done[1]);
+  if (mode != 2) return;
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&st->counter_misc, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int ntiles = (L.n + 63) / 64;
+  double tot[6] = {0, 0, 0, 0, 0, 0};
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) tot[q] += __ldcg(partials + t * 6 + q);
+  block_sum<6>(tot, scratch);
+  if (threadIdx.x == 0) {
+    finalize_gamma_state(st, tot, init);
+    st->counter_misc = 0;
   }
 }
 

@@ -407,11 +407,14 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   TZ* z = reinterpret_cast<TZ*>(q + nV);
   TZ* dinv = z + nV;
   // update: (node block, load case) blocks; apply: grid-stride over active nodes
-  const int grid_u = 6 * std::max(1, std::min((n + 255) / 256, c->num_sms * 2));
+  // one 256-node tile per CTA (not a resident-sized grid-stride grid): with
+  // concurrent lanes a partly resident persistent grid runs in waves
+  const int grid_u = 6 * std::max(1, (n + 255) / 256);
   const int grid_a = shl::apply_grid(n, c->num_sms);
   const int grid_c = std::max(1, std::min(static_cast<int>((c->n_elem + 31) / 32), c->num_sms * 16));
   c->partials.ensure(sizeof(double) *
-                     std::max<size_t>({static_cast<size_t>(grid_a) * 6,
+                     std::max<size_t>({static_cast<size_t>(std::max(grid_a, 6 * c->num_sms)) * 6,
+                                       static_cast<size_t>((n + 31) / 32) * 6,  // per-tile p.q / r.z
                                        static_cast<size_t>(grid_u) * 2,
                                        static_cast<size_t>(grid_c) * 21, 64}));
   c->state.ensure(sizeof(shl::PcgState));
@@ -804,6 +807,7 @@ int shl_ctx_create(int device, shl_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    CK(cudaEventCreateWithFlags(&c->sync_ev, cudaEventBlockingSync | cudaEventDisableTiming));
     CK(cudaMallocHost(&c->hmisc, sizeof(Misc)));
     CK(cudaMallocHost(&c->hstate, sizeof(shl::PcgState)));
     CK(cudaMallocHost(&c->hC, 36 * sizeof(double)));
@@ -821,6 +825,7 @@ void shl_ctx_destroy(shl_ctx* c) {
   if (c->nccl && c->nccl_deleter) c->nccl_deleter(c->nccl);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->sync_ev) cudaEventDestroy(c->sync_ev);
   for (auto& e : c->prof_ev)
     if (e) cudaEventDestroy(e);
   if (c->hmisc) cudaFreeHost(c->hmisc);

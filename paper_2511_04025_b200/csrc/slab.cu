@@ -217,7 +217,8 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     S.ld = round_up(P.n_local + 1, 32);
     const size_t nX = 18 * S.ld;
     S.vec.ensure(2 * nX * sizeof(TX) + (3 * nX + 6 * S.ld) * sizeof(TV));
-    S.partials.ensure(sizeof(double) * 21 * 2400);
+    // per-block partials (<= 2400 blocks x 21) and per-32-node-tile partials of the apply
+    S.partials.ensure(sizeof(double) * std::max<size_t>(21 * 2400, static_cast<size_t>((P.n_owned + 31) / 32) * 6));
     max_local = std::max(max_local, P.n_local);
     max_plane = std::max({max_plane, P.n_glo, P.n_ghi, P.cnt_first, P.cnt_last});
   }

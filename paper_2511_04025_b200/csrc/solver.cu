@@ -127,6 +127,28 @@ __device__ __forceinline__ void reduce_partials(const double* partials, double (
   block_sum<NV>(out, scratch);
 }
 
+// ---- dynamic tile scheduling ------------------------------------------------
+// The gather kernels keep one CTA per resident slot and hand out 32/64-node
+// tiles from an atomic counter instead of a fixed grid stride.  With several
+// designs in flight (batch lanes) a kernel is often only partly resident; a
+// fixed stride then runs the late CTAs' full shares as a second wave (measured:
+// two lanes at half the throughput of one), while a shared counter lets the
+// resident CTAs take the work.  The last CTA to finish resets the counter.
+__device__ __forceinline__ int grab_tile(uint32_t* next) {
+  __shared__ int s_tile;
+  __syncthreads();  // everyone has read the previous tile
+  if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(next, 1u));
+  __syncthreads();
+  return s_tile;
+}
+
+__device__ __forceinline__ void tiles_done(uint32_t* next, uint32_t* done) {
+  if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
+    atomicExch(next, 0u);
+    atomicExch(done, 0u);
+  }
+}
+
 // ---- scalar updates (shared by the last block and the cross-slab finalize) --
 __device__ void finalize_apply_state(PcgState* st, const double (&tot)[6]) {
   for (int s = 0; s < 6; ++s) {
@@ -648,8 +670,14 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
   const double ridge = st->ridge;
   const bool dn = st->done[s_] != 0;
   const double bcoef = st->beta[s_];
-  double pq = 0.0;
-  for (int tile = blockIdx.x; tile * (32 * G) < A.n; tile += gridDim.x) {
+  __shared__ double red[G][6];
+  // Tiles come from the shared counter (grab_tile); p.q is reduced PER TILE
+  // (warp butterfly, groups in fixed order) into partials[tile][6], and the
+  // last CTA sums the tiles in index order: the same bits whichever CTA ran
+  // which tile (reproducible C^H under any residency).
+  for (;;) {
+    const int tile = grab_tile(&st->tile_next[0]);
+    if (tile * (32 * G) >= A.n) break;
     const int idx = tile * (32 * G) + grp * 32 + lane;
     const bool valid = idx < A.n;
     const int g = valid ? A.node_list[idx] : -1;
@@ -670,6 +698,7 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
         for (int k = 0; k < 3; ++k) part_s[grp][(plane * 18 + c * 6 + 3 * half + k) * 32 + lane] = acc.y[c * 3 + k];
     }
     __syncthreads();
+    double pq = 0.0;
     if (valid) {
       const size_t ob = vbase(idx, 18);
 #pragma unroll
@@ -688,24 +717,39 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
         pq += pn * qn;
       }
     }
-    __syncthreads();
-  }
-  double pq6[6];
 #pragma unroll
-  for (int t = 0; t < 6; ++t) pq6[t] = t == s_ ? pq : 0.0;
-  block_sum<6>(pq6, scratch);
-  if (publish_partial<6>(pq6, A.partials, &st->counter_apply)) {
-    double tot[6];
+    for (int o = 16; o > 0; o >>= 1) pq += __shfl_xor_sync(0xffffffffu, pq, o);
+    if (lane == 0) red[grp][s_] = pq;
     __syncthreads();
-    reduce_partials<6>(A.partials, tot, scratch);
-    if (threadIdx.x == 0) {
-      if (A.defer) {
-        for (int t = 0; t < 6; ++t) A.totals[t] = tot[t];
-      } else {
-        finalize_apply_state(st, tot);
-      }
-      st->counter_apply = 0;
+    if (threadIdx.x < 6) {
+      double t = red[0][threadIdx.x];
+#pragma unroll
+      for (int gg = 1; gg < G; ++gg) t += red[gg][threadIdx.x];
+      A.partials[tile * 6 + threadIdx.x] = t;
     }
+  }
+  tiles_done(&st->tile_next[0], &st->tile_done[0]);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&st->counter_apply, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int ntiles = (A.n + 32 * G - 1) / (32 * G);
+  double tot[6] = {0, 0, 0, 0, 0, 0};
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) tot[q] += __ldcg(A.partials + t * 6 + q);
+  block_sum<6>(tot, scratch);
+  if (threadIdx.x == 0) {
+    if (A.defer) {
+      for (int t = 0; t < 6; ++t) A.totals[t] = tot[t];
+    } else {
+      finalize_apply_state(st, tot);
+    }
+    st->counter_apply = 0;
   }
 }
 
@@ -1060,6 +1104,10 @@ void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s) {
       }();
       if (variant == 22) {
         apply6_kernel<TZ, 2, 2><<<std::min(grid, 2 * nsm), 384, 0, s>>>(a);
+      } else if (variant == 15) {  // partials hold 6 * nsm blocks (shl_api.cu run_solve)
+        apply6_kernel<TZ, 1, 5><<<std::max(1, std::min((a.n + 31) / 32, 5 * nsm)), 192, 0, s>>>(a);
+      } else if (variant == 16) {
+        apply6_kernel<TZ, 1, 6><<<std::max(1, std::min((a.n + 31) / 32, 6 * nsm)), 192, 0, s>>>(a);
       } else if (variant == 14) {
         apply6_kernel<TZ, 1, 4><<<std::min(grid, 4 * nsm), 192, 0, s>>>(a);
       } else {
