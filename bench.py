@@ -325,6 +325,15 @@ def run_ours(args, rank, world, local):
     iter_bytes = (bytes_apply + bytes_update) * prof_nodes
     iter_s = (apply_ms + update_ms) / 1e3 / max(launches_apply, 1)
 
+    # SURVEY.md §8(d) solver figure: B_iter * lockstep iterations / t_solve, with
+    # B_iter = N_node*(5*144 + 5*72) + N_elem*12 bytes (mixed: FP64 x,r; FP32 p,q
+    # as SURVEY states it) -- the block-Jacobi PCG iteration; the multigrid
+    # V-cycle's own traffic is not in it
+    # (single-lane profiling pass, so t_solve is one design's own solve time)
+    sv_bytes = sum((s_.n_nodes * 1080 + s_.n_elements * 12) * int(max(s_.iterations)) for s_ in pst)
+    sv_time = sum(r_.timings["t_solve"] for r_ in prof) / 1e3
+    survey_formula = {"bytes": sv_bytes, "solve_s": sv_time, "achieved_gbs": sv_bytes / sv_time / 1e9,
+                      "frac": sv_bytes / sv_time / 1e9 / peaks()[0], "designs": len(prof)}
     line = {"metric": METRIC, "value": total_designs / dev_max, "unit": UNIT, "n_gpus": world,
             "steps": len(designs), "warmup": args.warmup, "ms_per_step": dev_max / len(designs) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -348,7 +357,8 @@ def run_ours(args, rank, world, local):
                          {"bytes": iter_bytes, "us": iter_s * 1e6,
                           "achieved_gbs": iter_bytes / iter_s / 1e9 if iter_s else None,
                           "frac": iter_bytes / iter_s / 1e9 / peak if iter_s else None},
-                         "iteration_us": iter_s * 1e6},
+                         "iteration_us": iter_s * 1e6,
+                         "survey_solver_formula": survey_formula},
             "stages_ms": {k: statistics.mean(s_.timings[k] for s_ in st)
                           for k in ("t_field", "t_mesh", "t_AS", "t_solve", "t_C", "t_fwd")},
             "stages_ms_single_lane": {k: statistics.mean(r_.timings[k] for r_ in prof)

@@ -120,7 +120,7 @@ def write_csv(out_dir: str, n: int) -> str:
 
 
 def device_chunk_fn(r: int, tol: float, precision: str, device: int, seed0: int = 0,
-                    symmetry: str = "cubic_octant", n_pre: int = 8, lanes: int = 2) -> DesignFn:
+                    symmetry: str = "cubic_octant", n_pre: int = 8, lanes: int = 4) -> DesignFn:
     """Chunk evaluator on the local GPU through shl_homogenize_batch, `lanes`
     designs of a chunk in flight at once."""
     from . import api as S
@@ -152,7 +152,7 @@ def main(argv=None):
     ap.add_argument("--chunk", type=int, default=8)
     ap.add_argument("--seed0", type=int, default=0)
     ap.add_argument("--out", default="runs/sweep")
-    ap.add_argument("--lanes", type=int, default=2, help="designs in flight per GPU")
+    ap.add_argument("--lanes", type=int, default=4, help="designs in flight per GPU")
     a = ap.parse_args(argv)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
