@@ -706,8 +706,9 @@ __global__ void __launch_bounds__(256) galerkin_stored_kernel(const int* __restr
         const int ex = nx + dx - 2 * Dx, ey = ny + dy - 2 * Dy, ez = nz + dz - 2 * Dz;
         if (ex < -1 || ex > 1 || ey < -1 || ey > 1 || ez < -1 || ez > 1) continue;
         const int mi = (fi + dx + r_f) % r_f, mj = (fj + dy + r_f) % r_f, mk = (fk + dz + r_f) % r_f;
-        const size_t gm = (static_cast<size_t>(mk) * r_f + mj) * r_f + mi;
-        if (gm == 0 || map_f[gm] < 0) continue;
+        // an inactive fine neighbour's block is exactly zero (no active element
+        // couples to it on any level), so only the pinned node needs skipping
+        if (mi == 0 && mj == 0 && mk == 0) continue;
         const TV w = wn * TV((ex ? 0.5 : 1.0) * (ey ? 0.5 : 1.0) * (ez ? 0.5 : 1.0));
 #pragma unroll
         for (int q = 0; q < 9; ++q) S[q] = fma_t(w, sb[(m * 9 + q) * 32], S[q]);

@@ -503,7 +503,11 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
   ua.init = 0;
   int64_t launches = 2 + 2;
-  int check = opt.check_every > 0 ? opt.check_every : (n < 200000 ? 16 : 32);
+  static const int check_env = [] {  // A/B: SHL_CHECK_EVERY
+    const char* e = std::getenv("SHL_CHECK_EVERY");
+    return e ? std::atoi(e) : 0;
+  }();
+  int check = opt.check_every > 0 ? opt.check_every : (check_env > 0 ? check_env : (n < 200000 ? 16 : 32));
   static const bool trace = std::getenv("SHL_TRACE") != nullptr;  // dev aid: per-iteration scalars
   if (trace) check = 1;
   double apply_ms = 0.0, update_ms = 0.0;
