@@ -67,6 +67,8 @@ struct LevelArgs {
   const TV* dinv;     // 6 per node
   int r, n, zero_slot;
   TV ridge;           // level 0 only
+  int zbase;          // level 0 of a z-slab (0 otherwise)
+  double* totals;     // mode 2: write the r.z sums here instead of finalizing (slabs)
 };
 
 // mode: 0 smooth   xout = xin + w Dinv (b - A xin)
@@ -191,11 +193,11 @@ __global__ void __launch_bounds__(192)
         acc.zero();
       } else if (kFine) {
         if (part == 0)
-          fine_gather_plane<TV, 0>(acc, idx, g, xin, L.beta, L.node_map, L.r, 0, L.zero_slot);
+          fine_gather_plane<TV, 0>(acc, idx, g, xin, L.beta, L.node_map, L.r, L.zbase, L.zero_slot);
         else if (part == 1)
-          fine_gather_plane<TV, 1>(acc, idx, g, xin, L.beta, L.node_map, L.r, 0, L.zero_slot);
+          fine_gather_plane<TV, 1>(acc, idx, g, xin, L.beta, L.node_map, L.r, L.zbase, L.zero_slot);
         else
-          fine_gather_plane<TV, 2>(acc, idx, g, xin, L.beta, L.node_map, L.r, 0, L.zero_slot);
+          fine_gather_plane<TV, 2>(acc, idx, g, xin, L.beta, L.node_map, L.r, L.zbase, L.zero_slot);
       } else {
         if (part == 0)
           stencil_gather_plane<TV, 0>(acc, idx, g, xin, L.stencil, L.node_map, L.r, L.zero_slot);
@@ -275,7 +277,11 @@ __global__ void __launch_bounds__(192)
     for (int q = 0; q < 6; ++q) tot[q] += __ldcg(partials + t * 6 + q);
   block_sum<6>(tot, scratch);
   if (threadIdx.x == 0) {
-    finalize_gamma_state(st, tot, init);
+    if (L.totals) {
+      for (int q = 0; q < 6; ++q) L.totals[q] = tot[q];
+    } else {
+      finalize_gamma_state(st, tot, init);
+    }
     st->counter_misc = 0;
   }
 }
@@ -416,6 +422,47 @@ __global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c
   b_c[oc] = acc[0];
   b_c[oc + 192] = acc[1];
   b_c[oc + 384] = acc[2];
+}
+
+// z-slab restriction: the slab's OWNED fine nodes only, accumulated into b_c
+template <typename TV>
+__global__ void restrict_slab_kernel(const int* __restrict__ list_c, int n_c, int r_c, const int* __restrict__ map_s,
+                                     int zbase, int nzl, int z0, int z1, int r_f, const TV* __restrict__ res_f,
+                                     TV* __restrict__ b_c, const PcgState* st) {
+  if (st->stop) return;
+  int idx, s;
+  node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
+  if (idx >= n_c) return;
+  const int G = list_c[idx];
+  const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
+  TV acc[3] = {TV(0), TV(0), TV(0)};
+  bool any = false;
+  if (G != 0) {
+    for (int dk = -1; dk <= 1; ++dk) {
+      const int fk = (2 * K + dk + r_f) % r_f;
+      if (fk < z0 || fk >= z1) continue;  // not owned by this slab
+      int lz = fk - zbase;
+      lz += lz < 0 ? r_f : 0;
+      if (lz >= nzl) continue;
+      for (int dj = -1; dj <= 1; ++dj)
+        for (int di = -1; di <= 1; ++di) {
+          const int fi = (2 * I + di + r_f) % r_f, fj = (2 * J + dj + r_f) % r_f;
+          const int nf = map_s[(static_cast<size_t>(lz) * r_f + fj) * r_f + fi];
+          if (nf < 0) continue;
+          const TV w = TV((di ? 0.5 : 1.0) * (dj ? 0.5 : 1.0) * (dk ? 0.5 : 1.0));
+          const size_t o = vbase(nf, 18) + s * 32;
+          acc[0] = fma_t(w, res_f[o], acc[0]);
+          acc[1] = fma_t(w, res_f[o + 192], acc[1]);
+          acc[2] = fma_t(w, res_f[o + 384], acc[2]);
+          any = true;
+        }
+    }
+  }
+  if (!any) return;
+  const size_t oc = vbase(idx, 18) + s * 32;
+  b_c[oc] += acc[0];
+  b_c[oc + 192] += acc[1];
+  b_c[oc + 384] += acc[2];
 }
 
 // x_f(n) += sum_N w(n,N) x_c(N) over the 1..8 coarse parents of n
@@ -942,7 +989,7 @@ template <typename TB, typename TV>
 void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const TV* xin, TV* xout,
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s) {
-  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
   static const bool one = std::getenv("SHL_APPLY1") != nullptr;  // A/B: thread-per-node kernels
   if (fine && one) {
     level_sweep_kernel<TB, TV, true><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
@@ -973,7 +1020,7 @@ bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xout, TV omega,
     cudaFuncSetAttribute(coarsest_cluster_kernel<TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
-  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
   coarsest_cluster_kernel<TV><<<kCoarseCluster, 576, smem, s>>>(a, b, xout, omega, sweeps, st);
   return true;
 }
@@ -981,7 +1028,7 @@ bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xout, TV omega,
 template <typename TB, typename TV, typename TO>
 void launch_level_sweep_out(const GmgLevelView<TV>& L, const TB* b, const TV* xin, TO* xout, TV omega,
                             PcgState* st, double* partials, int init, int grid, cudaStream_t s) {
-  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge};
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
   level_sweep3_kernel<TB, TV, true, TO><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, 2, st, partials, init);
 }
 
@@ -998,6 +1045,14 @@ void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const
 }
 
 template <typename TV>
+void launch_restrict_slab(const GmgLevelView<TV>& C, const int* map_s, int zbase, int nzl, int z0, int z1, int r_f,
+                          const TV* res_f, TV* b_c, const PcgState* st, cudaStream_t s) {
+  if (C.n)
+    restrict_slab_kernel<TV><<<node_case_blocks(C.n, 192), 192, 0, s>>>(C.node_list, C.n, C.r, map_s, zbase, nzl, z0,
+                                                                          z1, r_f, res_f, b_c, st);
+}
+
+template <typename TV>
 void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
                     const PcgState* st, cudaStream_t s) {
   if (F.n) prolong_kernel<TV><<<node_case_blocks(F.n, 192), 192, 0, s>>>(F.node_list, F.n, F.r, C.node_map, C.r, x_c, x_f, st);
@@ -1010,7 +1065,9 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
   template void launch_restrict<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,  \
                                     const PcgState*, cudaStream_t);                                   \
   template void launch_prolong<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,   \
-                                   const PcgState*, cudaStream_t);
+                                   const PcgState*, cudaStream_t);                                   \
+  template void launch_restrict_slab<TV>(const GmgLevelView<TV>&, const int*, int, int, int, int, int,   \
+                                         const TV*, TV*, const PcgState*, cudaStream_t);
 SHL_GMG_INST(float)
 SHL_GMG_INST(double)
 template void launch_level_sweep<double, float>(const GmgLevelView<float>&, bool, const double*, const float*,

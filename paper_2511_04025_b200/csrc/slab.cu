@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "context.h"
+#include "gmg_host.h"
 
 namespace shl {
 namespace host {
@@ -199,9 +200,15 @@ void build_slabs(shl_ctx* c, int G, int first, int count, std::vector<Slab>& sla
 }
 
 // ---------------------------------------------------------------- solve
-template <typename TX, typename TV>
+// TX: x, r; TV: p, q and the operator; TZ: z, Dinv and the V-cycle (as in the
+// single-device solve).  use_gmg: multigrid-preconditioned, with level 0
+// distributed over the slabs (ghost exchange before every level-0 sweep, the
+// restriction of the owned fine nodes summed across slabs) and the coarse
+// levels 1..L replicated on every process (built from the full mesh each
+// process holds; their vectors are small next to level 0).
+template <typename TX, typename TV, typename TZ>
 void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
-                     shl_stats* st, int prec, int G, NcclComm* comm) {
+                     shl_stats* st, int prec, int G, NcclComm* comm, bool use_gmg) {
   const int r = c->r;
   if (!c->node0_active)
     throw ShlError(SHL_SOLVER, "mesh has no corner node group: cannot prescribe the strain gauge");
@@ -211,18 +218,17 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
   std::vector<Slab> slabs;
   build_slabs(c, G, first, nloc, slabs);
 
-  int max_local = 0, max_plane = 0;
+  int max_plane = 0;
   for (auto& S : slabs) {
     const SlabPlan& P = S.P;
     S.ld = round_up(P.n_local + 1, 32);
     const size_t nX = 18 * S.ld;
-    S.vec.ensure(2 * nX * sizeof(TX) + (3 * nX + 6 * S.ld) * sizeof(TV));
+    // x, r (TX) | p, q (TV) | z, Dinv (TZ) | multigrid level-0 work: xa, xb, res (TZ)
+    S.vec.ensure(2 * nX * sizeof(TX) + 2 * nX * sizeof(TV) + (nX + 6 * S.ld + (use_gmg ? 3 * nX : 0)) * sizeof(TZ));
     // per-block partials (<= 2400 blocks x 21) and per-32-node-tile partials of the apply
     S.partials.ensure(sizeof(double) * std::max<size_t>(21 * 2400, static_cast<size_t>((P.n_owned + 31) / 32) * 6));
-    max_local = std::max(max_local, P.n_local);
     max_plane = std::max({max_plane, P.n_glo, P.n_ghi, P.cnt_first, P.cnt_last});
   }
-  (void)max_local;
   DevBuf tot, xfer;
   tot.ensure(sizeof(double) * 21 * nloc);
   xfer.ensure(4 * 18 * static_cast<size_t>(std::max(max_plane, 1)) * sizeof(double));
@@ -231,29 +237,64 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
 
   auto X = [&](Slab& S) { return S.vec.as<TX>(); };
   auto R = [&](Slab& S) { return S.vec.as<TX>() + 18 * S.ld; };
-  auto Z = [&](Slab& S) { return reinterpret_cast<TV*>(S.vec.as<TX>() + 36 * S.ld); };
-  auto Pv = [&](Slab& S) { return Z(S) + 18 * S.ld; };
-  auto Q = [&](Slab& S) { return Z(S) + 36 * S.ld; };
-  auto D = [&](Slab& S) { return Z(S) + 54 * S.ld; };
+  auto Pv = [&](Slab& S) { return reinterpret_cast<TV*>(S.vec.as<TX>() + 36 * S.ld); };
+  auto Q = [&](Slab& S) { return Pv(S) + 18 * S.ld; };
+  auto Z = [&](Slab& S) { return reinterpret_cast<TZ*>(Pv(S) + 36 * S.ld); };
+  auto D = [&](Slab& S) { return Z(S) + 18 * S.ld; };
+  auto XA = [&](Slab& S) { return D(S) + 6 * S.ld; };
+  auto XB = [&](Slab& S) { return XA(S) + 18 * S.ld; };
+  auto RES = [&](Slab& S) { return XB(S) + 18 * S.ld; };
 
   double T[144], W[144];
   element_loads(K0, r, T, W);
-  const double ridge = c->n_nodes > 0 ? 1e-11 * std::fabs(K0[0]) * 8.0 * c->beta_sum / double(c->n_nodes) : 0.0;
+  // ridges as in the single-device solve (shl_api.cu run_solve)
+  const double diag_mean = c->n_nodes > 0 ? std::fabs(K0[0]) * 8.0 * c->beta_sum / double(c->n_nodes) : 0.0;
+  const double ridge_op = diag_mean * (sizeof(TV) == 8 ? 1e-11 : 1e-8);
+  const double ridge = diag_mean * (sizeof(TZ) == 8 ? 1e-11 : 1e-8);
   CK(cudaEventRecord(c->ev[3], c->stream));
   ElementConstLease const_lease(K0, W, T, r, c->stream);
   for (auto& S : slabs) {
     CK(cudaMemsetAsync(S.vec.p, 0, S.vec.cap, c->stream));
-    launch_setup<TX, TV>(S.list.as<int>(), S.P.n_owned, static_cast<int>(S.ld), r, c->beta64.as<double>(),
+    launch_setup<TX, TZ>(S.list.as<int>(), S.P.n_owned, static_cast<int>(S.ld), r, c->beta64.as<double>(),
                          ridge, R(S), D(S), c->stream);
+  }
+  // replicated coarse hierarchy (levels 1..L) and its V-cycle driver
+  Vcycle<TX, TZ, TZ> vc{c, gmg_params()};
+  vc.s = c->stream;
+  if (vc.gp.nu <= 0) vc.gp.nu = sizeof(TV) == 8 ? 1 : 2;
+  const TZ* beta_z = sizeof(TZ) == 8 ? reinterpret_cast<const TZ*>(c->beta64.p)
+                                     : reinterpret_cast<const TZ*>(c->beta32.p);
+  if (use_gmg) {
+    vc.L = gmg_setup<TZ>(c, vc.gp, static_cast<TZ>(ridge));
+    if (vc.L == 0) throw ShlError(SHL_VALIDATION, "multigrid needs r divisible by 2 with r/2 >= 8");
+    vc.view.push_back({c->node_list.as<int>(), c->node_map.as<int>(), beta_z, nullptr, nullptr, r, c->n_nodes,
+                       c->n_nodes, static_cast<TZ>(ridge)});  // level 0 placeholder (slab views below)
+    vc.b.push_back(nullptr);
+    vc.xa.push_back(nullptr);
+    vc.xb.push_back(nullptr);
+    vc.res.push_back(nullptr);
+    for (int l = 0; l < vc.L; ++l) {
+      auto& Lv = c->gmg[l];
+      vc.view.push_back({Lv.list.as<int>(), Lv.map.as<int>(), nullptr, Lv.stencil.as<TZ>(), Lv.dinv.as<TZ>(),
+                         Lv.r, Lv.n, Lv.n, TZ(0)});
+      TZ* v = Lv.vec.as<TZ>();
+      const size_t s18 = static_cast<size_t>(18) * Lv.ld;
+      vc.b.push_back(v);
+      vc.xa.push_back(v + s18);
+      vc.xb.push_back(v + 2 * s18);
+      vc.res.push_back(v + 3 * s18);
+    }
   }
   PcgState hs{};
   hs.tol = opt.tol;
-  hs.ridge = ridge;
+  hs.ridge = ridge_op;
   hs.max_iter = opt.max_iter > 0 ? opt.max_iter : 20 * r + 2000;
   std::memcpy(c->hstate, &hs, sizeof(hs));
   CK(cudaMemcpyAsync(c->state.p, c->hstate, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
   CK(cudaEventRecord(c->ev[4], c->stream));
   PcgState* dst = c->state.as<PcgState>();
+  vc.st = dst;
+  vc.partials = slabs[0].partials.as<double>();  // coarse levels never defer
   const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
                                          : reinterpret_cast<const TV*>(c->beta32.p);
   double* totals = tot.as<double>();
@@ -296,40 +337,105 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     launch_unpack<T>(vec_of(me), me.P.n_owned + me.P.n_glo, me.P.n_ghi, recv_hi, c->stream);
   };
   auto grid_u = [&](const Slab& S) { return 6 * std::max(1, std::min((S.P.n_owned + 255) / 256, c->num_sms * 2)); };
-  auto grid_a = [&](const Slab& S) {
-    return apply_grid(S.P.n_owned, c->num_sms);
-  };
+  auto grid_a = [&](const Slab& S) { return apply_grid(S.P.n_owned, c->num_sms); };
   auto update_all = [&](int init) {
     for (int s = 0; s < nloc; ++s) {
       Slab& S = slabs[s];
-      UpdateArgs<TX, TV> ua{X(S), R(S), Pv(S), Q(S), Z(S), D(S), S.partials.as<double>(), dst,
-                            S.P.n_owned, static_cast<int>(S.ld), init, totals + 12 * s, 1, 0,
-                            nullptr, TV(0)};
-      launch_update<TX, TV>(ua, grid_u(S), c->stream);
+      UpdateArgs<TX, TV, TZ> ua{X(S), R(S), Pv(S), Q(S), Z(S), D(S), S.partials.as<double>(), dst,
+                                S.P.n_owned, static_cast<int>(S.ld), init, totals + 12 * s, 1,
+                                use_gmg ? 1 : 0, use_gmg ? XA(S) : nullptr, static_cast<TZ>(vc.gp.omega)};
+      launch_update<TX, TV, TZ>(ua, grid_u(S), c->stream);
     }
     reduce(12);
-    launch_finalize_update(dst, totals, nloc, init, c->stream);
+    if (use_gmg)
+      launch_finalize_update_gmg(dst, totals, nloc, init, c->stream);
+    else
+      launch_finalize_update(dst, totals, nloc, init, c->stream);
+  };
+  // level-0 view of slab s: owned nodes, slab-local map, ghost planes
+  auto fine_view = [&](Slab& S, double* tot_s) {
+    GmgLevelView<TZ> v{S.list.as<int>(), S.map.as<int>(), beta_z, nullptr, D(S), r, S.P.n_owned, S.P.n_local,
+                       static_cast<TZ>(ridge)};
+    v.zbase = S.P.zbase;
+    v.totals = tot_s;
+    return v;
+  };
+  std::vector<TZ*> cur(nloc), oth(nloc);
+  // z = M r: the V-cycle with level 0 on the slabs
+  auto precondition_all = [&](int init) {
+    const TZ w = static_cast<TZ>(vc.gp.omega);
+    const int nu = vc.gp.nu_at(0);
+    for (int s = 0; s < nloc; ++s) {
+      cur[s] = XA(slabs[s]);  // omega Dinv r, written by the update kernel
+      oth[s] = XB(slabs[s]);
+    }
+    auto sweep_all = [&](int mode) {  // mode 0: cur -> oth (swap); 1: cur -> RES
+      exchange([&](Slab& S) { return cur[&S - slabs.data()]; });
+      for (int s = 0; s < nloc; ++s) {
+        Slab& S = slabs[s];
+        const auto V = fine_view(S, nullptr);
+        launch_level_sweep<TX, TZ>(V, true, R(S), cur[s], mode == 1 ? RES(S) : oth[s], w, mode, dst,
+                                   S.partials.as<double>(), init, apply_grid(S.P.n_owned, c->num_sms), c->stream);
+        if (mode == 0) std::swap(cur[s], oth[s]);
+      }
+    };
+    for (int k = 1; k < nu; ++k) sweep_all(0);
+    sweep_all(1);
+    // restriction of the owned fine residuals, summed over slabs / ranks
+    TZ* b1 = vc.b[1];
+    const auto& C1 = vc.view[1];
+    CK(cudaMemsetAsync(b1, 0, static_cast<size_t>(18) * c->gmg[0].ld * sizeof(TZ), c->stream));
+    for (int s = 0; s < nloc; ++s) {
+      Slab& S = slabs[s];
+      launch_restrict_slab<TZ>(C1, S.map.as<int>(), S.P.zbase, S.P.nzl, S.P.z0, S.P.z1, r, RES(S), b1, dst,
+                               c->stream);
+    }
+    if (dist)
+      NK(nccl().AllReduce(b1, b1, 18 * static_cast<size_t>(c->gmg[0].ld), sizeof(TZ) == 8 ? ncclFloat64 : ncclFloat32,
+                          ncclSum, comm->comm, c->stream));
+    TZ* x1 = vc.level(1, nullptr, init);  // coarse levels, replicated
+    for (int s = 0; s < nloc; ++s) {
+      Slab& S = slabs[s];
+      launch_prolong<TZ>(fine_view(S, nullptr), C1, x1, cur[s], dst, c->stream);
+    }
+    for (int k = 1; k <= nu; ++k) {
+      if (k < nu) {
+        sweep_all(0);
+        continue;
+      }
+      exchange([&](Slab& S) { return cur[&S - slabs.data()]; });
+      for (int s = 0; s < nloc; ++s) {
+        Slab& S = slabs[s];
+        launch_level_sweep_out<TX, TZ, TZ>(fine_view(S, totals + 6 * s), R(S), cur[s], Z(S), w, dst,
+                                           S.partials.as<double>(), init, apply_grid(S.P.n_owned, c->num_sms),
+                                           c->stream);
+      }
+      reduce(6);
+      launch_finalize_gamma(dst, totals, nloc, init, c->stream);
+    }
   };
   auto apply_all = [&]() {
     exchange([&](Slab& S) { return Z(S); });
     for (int s = 0; s < nloc; ++s) {
       Slab& S = slabs[s];
-      ApplyArgs<TV> aa{S.list.as<int>(), S.map.as<int>(), beta_apply, Z(S), Pv(S), Q(S),
-                       S.partials.as<double>(), dst, r, S.P.n_owned, static_cast<int>(S.ld),
-                       S.P.n_local, S.P.zbase, S.P.nzl, totals + 6 * s, 1};
-      launch_apply<TV>(aa, grid_a(S), c->stream);
+      ApplyArgs<TV, TZ> aa{S.list.as<int>(), S.map.as<int>(), beta_apply, Z(S), Pv(S), Q(S),
+                           S.partials.as<double>(), dst, r, S.P.n_owned, static_cast<int>(S.ld),
+                           S.P.n_local, S.P.zbase, S.P.nzl, totals + 6 * s, 1};
+      launch_apply<TV, TZ>(aa, grid_a(S), c->stream);
     }
     reduce(6);
     launch_finalize_apply(dst, totals, nloc, c->stream);
   };
 
   update_all(1);
+  if (use_gmg) precondition_all(1);
   apply_all();
   const int check = opt.check_every > 0 ? opt.check_every : 16;
   int64_t launches = 0;
   for (;;) {
     for (int it = 0; it < check; ++it) {
       update_all(0);
+      if (use_gmg) precondition_all(0);
       apply_all();
       launches += 2 * nloc + 2 + 8 * nloc;
     }
@@ -376,6 +482,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     for (int s = 0; s < 6; ++s) st->iterations[s] = fin.iters[s];
     st->converged = 1;
     st->precision = prec;
+    st->gmg_levels = use_gmg ? vc.L + 1 : 0;
   }
 }
 
@@ -401,11 +508,32 @@ void homogenize_slabs(shl_ctx* c, int G, NcclComm* comm, const shl_design* desig
   });
   CK(cudaEventRecord(c->ev[2], c->stream));
   const int prec = resolve_precision(opt);
-  tagged("solve", [&] {
+  // preconditioner choice as in the single-device solve (shl_api.cu)
+  const bool gmg = opt.preconditioner == SHL_PRECOND_GMG ||
+                   (opt.preconditioner == SHL_PRECOND_AUTO && r % 2 == 0 && r / 2 >= gmg_params().min_r);
+  auto once = [&](bool use_gmg) {
     switch (prec) {
-      case SHL_PREC_FP64: run_solve_slabs<double, double>(c, K0, opt, C_out, st, prec, G, comm); break;
-      case SHL_PREC_MIXED: run_solve_slabs<double, float>(c, K0, opt, C_out, st, prec, G, comm); break;
-      default: run_solve_slabs<float, float>(c, K0, opt, C_out, st, prec, G, comm); break;
+      case SHL_PREC_FP64: run_solve_slabs<double, double, double>(c, K0, opt, C_out, st, prec, G, comm, use_gmg); break;
+      case SHL_PREC_MIXED:
+        if (use_gmg)  // FP64 operator with the FP32 V-cycle (see solve_dispatch_once)
+          run_solve_slabs<double, double, float>(c, K0, opt, C_out, st, prec, G, comm, true);
+        else
+          run_solve_slabs<double, float, float>(c, K0, opt, C_out, st, prec, G, comm, false);
+        break;
+      default: run_solve_slabs<float, float, float>(c, K0, opt, C_out, st, prec, G, comm, use_gmg); break;
+    }
+  };
+  tagged("solve", [&] {
+    if (!gmg || opt.preconditioner != SHL_PRECOND_AUTO) {
+      once(gmg);
+      return 0;
+    }
+    try {
+      once(true);
+    } catch (const ShlError& e) {  // AUTO: a multigrid breakdown is redone with block Jacobi
+      if (e.code != SHL_SOLVER || std::string(e.what()).find("positive definiteness") == std::string::npos) throw;
+      once(false);
+      if (st) st->precond_fallback = 1;
     }
     return 0;
   });

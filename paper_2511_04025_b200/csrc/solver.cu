@@ -951,6 +951,28 @@ __global__ void finalize_update_kernel(PcgState* st, const double* totals, int n
   finalize_update_state(st, tot, init);
 }
 
+__global__ void finalize_update_gmg_kernel(PcgState* st, const double* totals, int nslab, int init) {
+  double rr[6];
+  for (int q = 0; q < 6; ++q) {
+    double s = 0.0;
+    for (int b = 0; b < nslab; ++b) s += totals[b * 12 + q];
+    rr[q] = s;
+  }
+  if (st->stop && !init) return;
+  finalize_update_gmg(st, rr, init);
+}
+
+__global__ void finalize_gamma_kernel(PcgState* st, const double* totals, int nslab, int init) {
+  if (st->stop) return;
+  double g[6];
+  for (int q = 0; q < 6; ++q) {
+    double s = 0.0;
+    for (int b = 0; b < nslab; ++b) s += totals[b * 6 + q];
+    g[q] = s;
+  }
+  finalize_gamma_state(st, g, init);
+}
+
 __global__ void finalize_apply_kernel(PcgState* st, const double* totals, int nslab) {
   if (st->stop) return;
   double tot[6];
@@ -992,6 +1014,12 @@ __global__ void unpack_kernel(T* __restrict__ vec, int first, int count, const T
 
 void launch_finalize_update(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s) {
   finalize_update_kernel<<<1, 1, 0, s>>>(st, totals, nslab, init);
+}
+void launch_finalize_update_gmg(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s) {
+  finalize_update_gmg_kernel<<<1, 1, 0, s>>>(st, totals, nslab, init);
+}
+void launch_finalize_gamma(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s) {
+  finalize_gamma_kernel<<<1, 1, 0, s>>>(st, totals, nslab, init);
 }
 void launch_finalize_apply(PcgState* st, const double* totals, int nslab, cudaStream_t s) {
   finalize_apply_kernel<<<1, 1, 0, s>>>(st, totals, nslab);

@@ -94,9 +94,20 @@ struct GmgLevelView {
   const TV* dinv;
   int r, n, zero_slot;
   TV ridge;
+  int zbase = 0;             // level 0 of a z-slab: global z of local node-map plane 0
+  double* totals = nullptr;  // non-null: the last sweep writes its 6 r.z sums here (slabs)
 };
 
 void launch_coarse_flags(const int* map_f, int r_f, int r_c, int* flag_c, cudaStream_t s);
+// z-slab restriction: b_c += P^T res over the fine nodes the slab owns (planes
+// [z0, z1), slab-local node map over planes zbase..).  The slabs' calls (or the
+// ranks' all-reduce) sum to the undecomposed restriction.
+template <typename TV>
+void launch_restrict_slab(const GmgLevelView<TV>& C, const int* map_s, int zbase, int nzl, int z0, int z1, int r_f,
+                          const TV* res_f, TV* b_c, const PcgState* st, cudaStream_t s);
+// cross-slab finalize of the multigrid update (r.r only) and of the last sweep's r.z
+void launch_finalize_update_gmg(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s);
+void launch_finalize_gamma(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s);
 template <typename TV>
 void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int r_f, const TV* beta_f,
                      const TV* stencil_f, TV ridge, TV* stencil_c, cudaStream_t s);

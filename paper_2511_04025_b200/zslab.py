@@ -6,7 +6,9 @@
 Rank 0 creates the NCCL unique id through the library (shl_nccl_unique_id),
 torch.distributed (gloo) broadcasts the 128 bytes, and every rank calls
 shl_homogenize_zslab for its slab; C^H is identical on every rank.  With one
-process the same slab code runs emulated (`--emulate G`).
+process the same slab code runs emulated (`--emulate G`).  The default
+preconditioner is multigrid: level 0 on the slabs (ghost exchange before every
+sweep, restriction all-reduced), coarse levels replicated on every rank.
 """
 from __future__ import annotations
 
@@ -24,13 +26,14 @@ def main(argv=None):
     ap.add_argument("--tol", type=float, default=1e-5)
     ap.add_argument("--precision", default="mixed")
     ap.add_argument("--emulate", type=int, default=0, help="G slabs on one device")
+    ap.add_argument("--preconditioner", default="auto", choices=["auto", "gmg", "jacobi"])
     a = ap.parse_args(argv)
     from . import api as S
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
     d = S.random_design(S.RandomDesignSpec("cubic_octant", 8, 2, -1.0, 1.0), a.seed)
-    opt = S.HomogenizeOptions(residual_tol=a.tol, precision=a.precision)
+    opt = S.HomogenizeOptions(residual_tol=a.tol, precision=a.precision, preconditioner=a.preconditioner)
     ctx = S.Context(local)
     if world == 1:
         if a.emulate >= 2:

@@ -283,6 +283,21 @@ def test_zslab_matches_single_device(S, r, G, prec, tol):
     assert got.stats.n_nodes == ref.stats.n_nodes
 
 
+@pytest.mark.parametrize("r,G,prec,tol", [(32, 2, "fp64", 1e-10), (64, 3, "mixed", 1e-6),
+                                          (64, 4, "fp32", 1e-5), (128, 4, "mixed", 1e-5)])
+def test_zslab_multigrid_matches_single_device(S, r, G, prec, tol):
+    """Multigrid z-slab solve (level 0 on the slabs with ghost exchanges before
+    every sweep, restriction summed over slabs, coarse levels replicated): same
+    C^H as the undecomposed multigrid solve, iteration counts within 1."""
+    d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), 3)
+    opt = S.HomogenizeOptions(residual_tol=tol, precision=prec, preconditioner="gmg")
+    ref = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, opt)
+    got = S.homogenize_slabs(d, S.ShellParams(), S.BaseMaterial(), r, G, opt)
+    assert got.stats.gmg_levels == ref.stats.gmg_levels > 1
+    assert rel_fro(got.tensor, ref.tensor) < (1e-10 if prec == "fp64" else 1e-6)
+    assert np.abs(got.iterations - ref.iterations).max() <= 1
+
+
 def test_zslab_validation(S):
     d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), 3)
     with pytest.raises(S.ValidationError):
