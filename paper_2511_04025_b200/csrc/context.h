@@ -142,6 +142,7 @@ struct shl_ctx {
   // marching cubes / raw export (geom.cu)
   DevBuf mc_owned, mc_cnt, mc_verts, mc_tris;
   Misc* hmisc = nullptr;
+  int* hlevels = nullptr;  // pinned: per multigrid level (last scan offset, last flag)
   shl::PcgState* hstate = nullptr;
   double* hC = nullptr;
   cudaEvent_t ev[12] = {};

@@ -43,50 +43,65 @@ inline GmgParams gmg_params() {
 }
 
 // Coarse levels 1..L: active set, ordered ids, Galerkin stencils, Dinv.
+// Two passes so the host waits once, not once per level: the active sets and
+// ids of every level depend only on the level above's node map, so they are
+// all computed first and their sizes read back together; then the stencils.
+// (With concurrent batch lanes every host wait also waits out whatever the
+// other lanes have in flight on the GPU.)
 template <typename TV>
 int gmg_setup(shl_ctx* c, const GmgParams& gp, TV ridge) {
+  int L = 0;
+  {
+    int rf = c->r;
+    const int* map_f = c->node_map.as<int>();
+    while (L < gp.max_levels && L < 32 && rf % 2 == 0 && rf / 2 >= gp.min_r) {
+      const int rc = rf / 2;
+      const int n3 = rc * rc * rc;
+      if (static_cast<int>(c->gmg.size()) <= L) c->gmg.emplace_back();
+      auto& Lv = c->gmg[L];
+      Lv.flag.ensure(static_cast<size_t>(n3) * sizeof(int));
+      Lv.off.ensure(static_cast<size_t>(n3) * sizeof(int));
+      Lv.map.ensure(static_cast<size_t>(n3) * sizeof(int));
+      Lv.list.ensure(static_cast<size_t>(n3) * sizeof(int));
+      Lv.scan_tmp.ensure(shl::scan_temp_bytes(n3));
+      shl::launch_coarse_flags(map_f, rf, rc, Lv.flag.as<int>(), c->stream);
+      shl::launch_exclusive_scan(Lv.flag.as<int>(), Lv.off.as<int>(), n3, Lv.scan_tmp.p, Lv.scan_tmp.cap,
+                                 c->stream);
+      shl::launch_scatter_compact(Lv.flag.as<int>(), Lv.off.as<int>(), n3, Lv.map.as<int>(),
+                                  Lv.list.as<int>(), c->stream);
+      CK(cudaMemcpyAsync(&c->hlevels[2 * L], Lv.off.as<int>() + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost,
+                         c->stream));
+      CK(cudaMemcpyAsync(&c->hlevels[2 * L + 1], Lv.flag.as<int>() + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost,
+                         c->stream));
+      Lv.r = rc;
+      map_f = Lv.map.as<int>();
+      rf = rc;
+      ++L;
+    }
+  }
+  c->sync();
   int rf = c->r;
   const int* map_f = c->node_map.as<int>();
   const TV* beta_f = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
                                      : reinterpret_cast<const TV*>(c->beta32.p);
   const TV* stencil_f = nullptr;
-  int L = 0;
-  while (L < gp.max_levels && rf % 2 == 0 && rf / 2 >= gp.min_r) {
-    const int rc = rf / 2;
-    const int n3 = rc * rc * rc;
-    if (static_cast<int>(c->gmg.size()) <= L) c->gmg.emplace_back();
-    auto& Lv = c->gmg[L];
-    Lv.flag.ensure(static_cast<size_t>(n3) * sizeof(int));
-    Lv.off.ensure(static_cast<size_t>(n3) * sizeof(int));
-    Lv.map.ensure(static_cast<size_t>(n3) * sizeof(int));
-    Lv.list.ensure(static_cast<size_t>(n3) * sizeof(int));
-    Lv.scan_tmp.ensure(shl::scan_temp_bytes(n3));
-    shl::launch_coarse_flags(map_f, rf, rc, Lv.flag.as<int>(), c->stream);
-    shl::launch_exclusive_scan(Lv.flag.as<int>(), Lv.off.as<int>(), n3, Lv.scan_tmp.p, Lv.scan_tmp.cap,
-                               c->stream);
-    shl::launch_scatter_compact(Lv.flag.as<int>(), Lv.off.as<int>(), n3, Lv.map.as<int>(),
-                                Lv.list.as<int>(), c->stream);
-    int last[2];
-    CK(cudaMemcpyAsync(&last[0], Lv.off.as<int>() + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(&last[1], Lv.flag.as<int>() + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
-    Lv.r = rc;
-    Lv.n = last[0] + last[1];
+  for (int l = 0; l < L; ++l) {
+    auto& Lv = c->gmg[l];
+    const int rc = Lv.r;
+    Lv.n = c->hlevels[2 * l] + c->hlevels[2 * l + 1];
     Lv.ld = round_up(Lv.n + 1, 32);
     Lv.stencil.ensure(static_cast<size_t>(243) * Lv.ld * sizeof(TV));
     Lv.dinv.ensure(static_cast<size_t>(6) * Lv.ld * sizeof(TV));
     Lv.vec.ensure(static_cast<size_t>(4) * 18 * Lv.ld * sizeof(TV));
     CK(cudaMemsetAsync(Lv.vec.p, 0, static_cast<size_t>(4) * 18 * Lv.ld * sizeof(TV), c->stream));
-    shl::launch_galerkin<TV>(Lv.list.as<int>(), Lv.n, rc, map_f, rf, L == 0 ? beta_f : nullptr,
-                             stencil_f, L == 0 ? ridge : TV(0), Lv.stencil.as<TV>(), c->stream);
-    shl::launch_coarse_dinv<TV>(Lv.list.as<int>(), Lv.n, Lv.stencil.as<TV>(), Lv.dinv.as<TV>(), gp.l1,
-                                c->stream);
-    c->launches += L == 0 ? 6 : 5;  // level 1 adds the cell-matrix kernel
+    shl::launch_galerkin<TV>(Lv.list.as<int>(), Lv.n, rc, map_f, rf, l == 0 ? beta_f : nullptr, stencil_f,
+                             l == 0 ? ridge : TV(0), Lv.stencil.as<TV>(), c->stream);
+    shl::launch_coarse_dinv<TV>(Lv.list.as<int>(), Lv.n, Lv.stencil.as<TV>(), Lv.dinv.as<TV>(), gp.l1, c->stream);
+    c->launches += 5;
     CK(cudaGetLastError());
     map_f = Lv.map.as<int>();
     stencil_f = Lv.stencil.as<TV>();
     rf = rc;
-    ++L;
   }
   return L;
 }

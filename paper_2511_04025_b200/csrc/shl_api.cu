@@ -619,12 +619,16 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
     return 0;
   });
   CK(cudaEventRecord(c->ev[1], c->stream));
-  read_norm(c);
-  if (c->norm == 0.0) throw ShlError(SHL_DEGENERATE, "field: design is degenerate (norm = 0)");
+  // The norm comes back with the mesh stage's count readback instead of its
+  // own host wait (the mesh kernels read it on the device); a degenerate
+  // design (norm 0) still fails with the field-stage error, before any solve.
+  c->norm = 1.0;  // placeholder for run_mesh's host-side check
   tagged("mesh", [&] {
     run_mesh(c, *sp);
     return 0;
   });
+  std::memcpy(&c->norm, &c->hmisc->norm_bits, sizeof(double));
+  if (c->norm == 0.0) throw ShlError(SHL_DEGENERATE, "field: design is degenerate (norm = 0)");
   CK(cudaEventRecord(c->ev[2], c->stream));
   tagged("solve", [&] {
     solve_dispatch(c, K0, opt, C_out, st);
@@ -671,6 +675,7 @@ int shl_ctx_create(int device, shl_ctx** out) {
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     CK(cudaEventCreateWithFlags(&c->sync_ev, cudaEventBlockingSync | cudaEventDisableTiming));
     CK(cudaMallocHost(&c->hmisc, sizeof(Misc)));
+    CK(cudaMallocHost(&c->hlevels, 64 * sizeof(int)));
     CK(cudaMallocHost(&c->hstate, sizeof(shl::PcgState)));
     CK(cudaMallocHost(&c->hC, 36 * sizeof(double)));
   });
@@ -691,6 +696,7 @@ void shl_ctx_destroy(shl_ctx* c) {
   for (auto& e : c->prof_ev)
     if (e) cudaEventDestroy(e);
   if (c->hmisc) cudaFreeHost(c->hmisc);
+  if (c->hlevels) cudaFreeHost(c->hlevels);
   if (c->hstate) cudaFreeHost(c->hstate);
   if (c->hC) cudaFreeHost(c->hC);
   if (c->stream) cudaStreamDestroy(c->stream);
