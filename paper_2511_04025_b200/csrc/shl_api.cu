@@ -380,22 +380,64 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   const bool use_graph = !c->profiling && !trace && !no_graph && check % kGraphIters == 0;
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;  // kernel launches per graph replay
+  // The whole solve loop as ONE graph launch when the driver supports
+  // conditional nodes: a WHILE node whose body is kGraphIters iterations plus a
+  // one-thread kernel setting the condition to !stop.  No host polls during the
+  // solve (host scheduling delays no longer idle the design's stream) and at
+  // most kGraphIters-1 no-op iterations after convergence.
+  static const bool no_while = std::getenv("SHL_NO_WHILE") != nullptr;  // A/B: host-polled replay
+  bool use_while = false;
   if (use_graph) {
     // recorded on a side stream: capture + instantiation (host work) overlap the
     // device executing the setup and first iteration already queued on c->stream
     const int64_t before = launches + vc.launches;
-    cudaGraph_t graph = nullptr;
     const cudaStream_t cs = c->cap_stream;
-    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    vc.s = cs;
-    for (int it = 0; it < kGraphIters; ++it) {
-      shl::launch_update<TX, TV, TZ>(ua, grid_u, cs);
-      precondition(0);
-      shl::launch_apply<TV, TZ>(aa, grid_a, cs);
-      launches += 2;
+    cudaGraph_t graph = nullptr;
+    if (!no_while) {
+      cudaGraph_t g = nullptr;
+      CK(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle h;
+      cudaGraphNode_t wnode;
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess) {
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        if (cudaGraphAddNode(&wnode, g, nullptr, 0, &cp) == cudaSuccess) {
+          cudaGraph_t body = cp.conditional.phGraph_out[0];
+          CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+          vc.s = cs;
+          for (int it = 0; it < kGraphIters; ++it) {
+            shl::launch_update<TX, TV, TZ>(ua, grid_u, cs);
+            precondition(0);
+            shl::launch_apply<TV, TZ>(aa, grid_a, cs);
+            launches += 2;
+          }
+          shl::launch_set_while(h, dst, cs);
+          vc.s = c->stream;
+          CK(cudaStreamEndCapture(cs, &body));
+          use_while = true;
+          graph = g;
+        }
+      }
+      if (!use_while) {
+        cudaGetLastError();  // clear a refused conditional node; fall back to host polls
+        cudaGraphDestroy(g);
+      }
     }
-    vc.s = c->stream;
-    CK(cudaStreamEndCapture(cs, &graph));
+    if (!use_while) {
+      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      vc.s = cs;
+      for (int it = 0; it < kGraphIters; ++it) {
+        shl::launch_update<TX, TV, TZ>(ua, grid_u, cs);
+        precondition(0);
+        shl::launch_apply<TV, TZ>(aa, grid_a, cs);
+        launches += 2;
+      }
+      vc.s = c->stream;
+      CK(cudaStreamEndCapture(cs, &graph));
+    }
     CK(cudaGraphInstantiate(&gexec, graph, 0));
     CK(cudaGraphDestroy(graph));
     graph_launches = launches + vc.launches - before;
@@ -408,7 +450,17 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
       if (g) cudaGraphExecDestroy(g);
     }
   } graph_guard{gexec};
+  if (use_while) {
+    CK(cudaGraphLaunch(gexec, c->stream));
+    CK(cudaMemcpyAsync(c->hstate, c->state.p, sizeof(shl::PcgState), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h += sizeof(shl::PcgState);
+    c->sync();
+    const int trips = (c->hstate->it + kGraphIters - 1) / kGraphIters;
+    launches += static_cast<int64_t>(std::max(trips, 1)) * (graph_launches + 1);
+    issued = c->hstate->it;
+  }
   for (;;) {
+    if (use_while) break;  // the device loop ran the whole solve
     if (use_graph) {
       for (int it = 0; it < check; it += kGraphIters) {
         CK(cudaGraphLaunch(gexec, c->stream));

@@ -1015,6 +1015,15 @@ __global__ void unpack_kernel(T* __restrict__ vec, int first, int count, const T
 void launch_finalize_update(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s) {
   finalize_update_kernel<<<1, 1, 0, s>>>(st, totals, nslab, init);
 }
+// Device-side loop control of the solve graph: keep iterating while the PCG
+// state has not stopped (converged, broken down or out of iterations).
+__global__ void set_while_kernel(cudaGraphConditionalHandle h, const PcgState* st) {
+  cudaGraphSetConditional(h, st->stop ? 0u : 1u);
+}
+void launch_set_while(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s) {
+  set_while_kernel<<<1, 1, 0, s>>>(h, st);
+}
+
 void launch_finalize_update_gmg(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s) {
   finalize_update_gmg_kernel<<<1, 1, 0, s>>>(st, totals, nslab, init);
 }
@@ -1131,7 +1140,11 @@ void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s) {
         return v;
       }();
       if (variant == 22) {
-        apply6_kernel<TZ, 2, 2><<<std::min(grid, 2 * nsm), 384, 0, s>>>(a);
+        static const int per_sm = [] {  // A/B: CTAs per SM of the apply (tiles are dynamic)
+          const char* e = std::getenv("SHL_APPLY_CTAS_PER_SM");
+          return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+        }();
+        apply6_kernel<TZ, 2, 2><<<std::min(grid, per_sm * nsm), 384, 0, s>>>(a);
       } else if (variant == 15) {  // partials hold 6 * nsm blocks (shl_api.cu run_solve)
         apply6_kernel<TZ, 1, 5><<<std::max(1, std::min((a.n + 31) / 32, 5 * nsm)), 192, 0, s>>>(a);
       } else if (variant == 16) {

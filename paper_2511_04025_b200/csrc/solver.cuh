@@ -107,6 +107,8 @@ void launch_restrict_slab(const GmgLevelView<TV>& C, const int* map_s, int zbase
                           const TV* res_f, TV* b_c, const PcgState* st, cudaStream_t s);
 // cross-slab finalize of the multigrid update (r.r only) and of the last sweep's r.z
 void launch_finalize_update_gmg(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s);
+// set a graph WHILE node's condition to !st->stop (the solve loop runs on the device)
+void launch_set_while(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s);
 void launch_finalize_gamma(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s);
 template <typename TV>
 void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int r_f, const TV* beta_f,
