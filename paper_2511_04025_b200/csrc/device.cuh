@@ -33,7 +33,7 @@ struct PcgState {
   uint32_t counter_apply;
   uint32_t counter_update;
   uint32_t counter_misc;
-  // dynamic tile schedulers (grab_tile / tiles_done): [0] apply, [1] V-cycle sweeps
+  // dynamic tile schedulers (TileQueue / tiles_done): [0] apply, [1] V-cycle sweeps
   uint32_t tile_next[2];
   uint32_t tile_done[2];
 };

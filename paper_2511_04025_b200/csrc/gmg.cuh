@@ -180,9 +180,11 @@ __global__ void __launch_bounds__(192)
   // tiles from the shared counter; mode 2 reduces r.z per tile (fixed order,
   // see apply6_kernel) so the sum does not depend on which CTA ran which tile
   __shared__ double red[2][6];
-  for (;;) {
-    const int tile = grab_tile(&st->tile_next[1]);
+  __shared__ int tq_slot[2];
+  TileQueue tq{&st->tile_next[1], tq_slot};
+  for (int tile = tq.first();; tile = tq.advance()) {
     if (tile * 64 >= L.n) break;
+    tq.request();
     gam2[0] = gam2[1] = 0.0;
     const int idx = tile * 64 + grp * 32 + lane;
     const bool valid = idx < L.n;
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(192)
 #pragma unroll
       for (int q = 0; q < 18; ++q) part_s[grp][(part * 18 + q) * 32 + lane] = acc.get(q);
     }
+    tq.publish();
     __syncthreads();
     if (valid) {
       const size_t ob = vbase(idx, 18);

@@ -134,13 +134,32 @@ __device__ __forceinline__ void reduce_partials(const double* partials, double (
 // fixed stride then runs the late CTAs' full shares as a second wave (measured:
 // two lanes at half the throughput of one), while a shared counter lets the
 // resident CTAs take the work.  The last CTA to finish resets the counter.
-__device__ __forceinline__ int grab_tile(uint32_t* next) {
-  __shared__ int s_tile;
-  __syncthreads();  // everyone has read the previous tile
-  if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(next, 1u));
-  __syncthreads();
-  return s_tile;
-}
+// The next grab is kept in flight: thread 0 requests tile i+1 while
+// the CTA gathers tile i (the atomic's L2 round trip overlaps the loads instead
+// of holding every warp at a barrier), publishes it before the tile's mid
+// barrier, and everyone reads it after the end barrier.  Two slots, so a warp
+// still reading tile i+1's id never sees tile i+2's.  Per tile this needs only
+// the kernel's own two barriers (a grab-then-broadcast needs two more).
+struct TileQueue {
+  uint32_t* next;
+  int* slot;  // __shared__ int[2]
+  unsigned pending = 0;
+  int it = 0;
+  __device__ __forceinline__ int first() {
+    if (threadIdx.x == 0) slot[1] = static_cast<int>(atomicAdd(next, 1u));
+    __syncthreads();
+    return slot[1];
+  }
+  __device__ __forceinline__ void request() {
+    if (threadIdx.x == 0) pending = atomicAdd(next, 1u);
+  }
+  __device__ __forceinline__ void publish() {  // before the tile's mid barrier
+    if (threadIdx.x == 0) slot[it & 1] = static_cast<int>(pending);
+  }
+  __device__ __forceinline__ int advance() {  // after the tile's end barrier
+    return slot[(it++) & 1];
+  }
+};
 
 __device__ __forceinline__ void tiles_done(uint32_t* next, uint32_t* done) {
   if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
@@ -671,13 +690,15 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
   const bool dn = st->done[s_] != 0;
   const double bcoef = st->beta[s_];
   __shared__ double red[G][6];
-  // Tiles come from the shared counter (grab_tile); p.q is reduced PER TILE
+  // Tiles come from the shared counter (TileQueue); p.q is reduced PER TILE
   // (warp butterfly, groups in fixed order) into partials[tile][6], and the
   // last CTA sums the tiles in index order: the same bits whichever CTA ran
   // which tile (reproducible C^H under any residency).
-  for (;;) {
-    const int tile = grab_tile(&st->tile_next[0]);
+  __shared__ int tq_slot[2];
+  TileQueue tq{&st->tile_next[0], tq_slot};
+  for (int tile = tq.first();; tile = tq.advance()) {
     if (tile * (32 * G) >= A.n) break;
+    tq.request();
     const int idx = tile * (32 * G) + grp * 32 + lane;
     const bool valid = idx < A.n;
     const int g = valid ? A.node_list[idx] : -1;
@@ -697,6 +718,7 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
 #pragma unroll
         for (int k = 0; k < 3; ++k) part_s[grp][(plane * 18 + c * 6 + 3 * half + k) * 32 + lane] = acc.y[c * 3 + k];
     }
+    tq.publish();
     __syncthreads();
     double pq = 0.0;
     if (valid) {

@@ -4,10 +4,11 @@ rows = list(csv.reader(open(sys.argv[1])))
 h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[h]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+mi = hdr.index("Metric Name")
 scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
 tot, cnt = {}, {}
 for r in rows[h + 1:]:
-    if len(r) <= vi:
+    if len(r) <= vi or r[mi] != "gpu__time_duration.sum":  # other metrics (grid size) are not times
         continue
     name = r[ki].split("(")[0].replace("void ", "")
     v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
