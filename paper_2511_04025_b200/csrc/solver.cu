@@ -1149,9 +1149,13 @@ void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s) {
   }
   if constexpr (sizeof(TV) == 8) {
     static const bool three = std::getenv("SHL_APPLY3") != nullptr;  // A/B: three-warp FP64 variant
-    static const int variant = [] {  // A/B: SHL_APPLY6 = 22 (2 groups, 2 blocks/SM), 13, 14
+    // SHL_APPLY6 = GM: G six-warp groups per CTA, M CTAs per SM (A/B).  With the
+    // prefetched tile queue 14 (one group: its barriers hold 6 warps, not 12)
+    // measures 305 vs 311 us for 22 at the same 80 registers; 13 / 15 / 16:
+    // 411 / 344 / 376 us (occupancy, or spills under the tighter register caps).
+    static const int variant = [] {
       const char* e = std::getenv("SHL_APPLY6");
-      return e ? std::atoi(e) : 22;
+      return e ? std::atoi(e) : 14;
     }();
     if (!three) {
       // one CTA per resident slot: the grid-stride loop then has no tail wave
