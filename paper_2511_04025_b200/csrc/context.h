@@ -114,6 +114,7 @@ struct shl_ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // only ever in capture mode (iteration graph)
+  bool high_priority = false;         // lane 0 of a batch under SHL_LANE_PRIO (A/B)
   std::string err;
   bool profiling = false;
   int64_t launches = 0;
