@@ -171,7 +171,9 @@ int shl_homogenize(shl_ctx* ctx, const shl_design* design, const shl_shell_param
  * stops the batch; per-design failures are reported through status. */
 /* Designs a batch keeps in flight concurrently (default 1): lanes >= 2 run
  * that many designs at once on sub-contexts of ctx (same device, one stream
- * and host thread each); results and per-design stats are unchanged. */
+ * and host thread each); results and per-design stats are unchanged.  ctx's
+ * own streams are recreated at the greatest stream priority on the first
+ * multi-lane batch (lane 0 first, other lanes fill its gaps). */
 int shl_set_batch_lanes(shl_ctx* ctx, int lanes);
 int shl_homogenize_batch(shl_ctx* ctx, int n, const shl_design* designs,
                          const shl_shell_params* sp, const shl_material* mat, int r,
