@@ -1,0 +1,608 @@
+// brick.cu -- level-0 operator kernels on shared-memory-staged bricks (sm_100a).
+//
+// The matrix-free masked operator of the reference's GridSolver::apply
+// (grid_solver.hpp:154-176: y_n = sum_e beta_e K0 u_e, node 0 pinned) applied
+// brick by brick.  Level-0 node ids are numbered brick-major (voxel.cu
+// brick_* kernels): the torus is cut into 8x8x4-node bricks, each active brick
+// owns a contiguous id range [bstart[t], bstart[t+1]).  A CTA takes one brick
+// from the tile queue and
+//   1. stages the node map of the brick + 1-node halo (10x10x6 = 600
+//      positions) and beta of its 9x9x5 elements in shared memory,
+//   2. gathers the 18 components (3 dof x 6 load cases) of the input vector at
+//      every staged position into shared memory ([q][600], converted to the
+//      operator type once per position instead of once per use),
+//   3. gives each active node of the brick one thread, which builds the 27
+//      neighbour blocks S_m = sum_e beta_e K0[a(n,e), b(m,e)] (K0 from the
+//      constant bank, FP64 or FP32) and applies them to all six load cases
+//      from shared memory,
+//   4. runs the caller's epilogue (PCG direction update, smoother or
+//      residual) on the node's own coalesced rows, and reduces its dot
+//      products per brick (fixed order -> reproducible).
+// The dependent map -> vector load chain of a per-node gather becomes two
+// bulk phases per brick; the arithmetic reads shared memory only.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "pcg_common.cuh"
+
+namespace shl {
+
+// this translation unit's copy of K0 (uploaded with the solver's element
+// constants, ElementConstLease in solver.cu)
+__constant__ double c_bK0d[576];
+__constant__ float c_bK0f[576];
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T k0(int i);
+template <>
+__device__ __forceinline__ double k0<double>(int i) {
+  return c_bK0d[i];
+}
+template <>
+__device__ __forceinline__ float k0<float>(int i) {
+  return c_bK0f[i];
+}
+
+constexpr int kBX = 8, kBY = 4, kBZ = 4;  // nodes per brick (must match voxel.cu)
+constexpr int kRX = kBX + 2, kRY = kBY + 2, kRZ = kBZ + 2;
+constexpr int kRegion = kRX * kRY * kRZ;  // 360 staged node positions (brick + 1-node halo)
+constexpr int kEX = kBX + 1, kEY = kBY + 1, kEZ = kBZ + 1;
+constexpr int kERegion = kEX * kEY * kEZ;  // 225 staged elements
+constexpr int kNodes = kBX * kBY * kBZ;    // 128 nodes per brick
+constexpr int kThreads = kNodes;           // one thread per brick node
+constexpr int kWarps = kThreads / 32;
+
+// Staged vector layout: FP64 [q][position]; FP32 [c][load-case pair][position]
+// as float2, so the FP32 arithmetic runs on packed FFMA2 over load-case pairs
+// and reads one 64-bit shared word per pair.
+template <typename TS>
+__device__ __forceinline__ int xs_index(int q, int p) {
+  if constexpr (sizeof(TS) == 4)
+    return (((q / 6) * 3 + (q % 6) / 2) * kRegion + p) * 2 + (q & 1);
+  else
+    return q * kRegion + p;
+}
+
+// v in [-r, 3r) -> [0, r)   (staged coordinates never leave that range for r >= 4)
+__device__ __forceinline__ int wrap3(int v, int r) {
+  v += v < 0 ? r : 0;
+  v -= v >= r ? r : 0;
+  v -= v >= r ? r : 0;
+  return v;
+}
+
+#ifdef SHL_BRICK_TRACE
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ unsigned long long g_trace[4][2][64][2];  // [cta][role][event][k,time]
+__device__ int g_trace_n[4][2];
+#define TRACE(msg, ...)                                                        \
+  if (blockIdx.x < 4) {                                                        \
+    const int role_ = threadIdx.x >= kConsumers;                               \
+    const int n_ = g_trace_n[blockIdx.x][role_]++;                             \
+    if (n_ < 64) {                                                             \
+      g_trace[blockIdx.x][role_][n_][0] = (unsigned long long)(__LINE__);      \
+      g_trace[blockIdx.x][role_][n_][1] = gtime();                             \
+    }                                                                          \
+  }
+__device__ void trace_dump(const char* kern) {
+  if (blockIdx.x < 4 && (threadIdx.x == 0 || threadIdx.x == kConsumers)) {
+    const int role = threadIdx.x >= kConsumers;
+    const int n = min(g_trace_n[blockIdx.x][role], 64);
+    for (int i = 0; i < n; ++i)
+      printf("%s cta %d %s line %llu t %llu\n", kern, blockIdx.x, role ? "P" : "C", g_trace[blockIdx.x][role][i][0],
+             g_trace[blockIdx.x][role][i][1]);
+    g_trace_n[blockIdx.x][role] = 0;
+  }
+}
+#define TRACE_DUMP(k) trace_dump(k)
+#else
+#define TRACE(msg, ...)
+#define TRACE_DUMP(k)
+#endif
+
+// ---- async copies (sm_80+ cp.async, sm_90+ bulk L2 prefetch) --------------------
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_addr(dst)), "l"(src), "n"(BYTES)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// Pull [p, p + bytes) into L2 through the TMA unit (one instruction, no registers).
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+// L2 prefetch of the node rows [first, last) of an nq-component blocked vector.
+template <typename T>
+__device__ __forceinline__ void prefetch_rows(const T* v, int nq, int first, int last) {
+  if (last <= first) return;
+  const int b0 = first >> 5, b1 = (last - 1) >> 5;
+  prefetch_l2(v + static_cast<size_t>(b0) * nq * 32, static_cast<unsigned>((b1 - b0 + 1) * nq * 32 * sizeof(T)));
+}
+
+// Shared memory of one CTA (= one brick): the staged input vector, the
+// element betas, the node map of the region and the brick's node positions.
+template <typename TS>
+struct BrickShared {
+  TS xs[18 * kRegion];        // [q][position], 0 where absent
+  TS bs[kERegion];            // element betas of the region
+  int ms[kRegion];            // node ids of the region (-1 absent)
+  unsigned short pc[kNodes];  // region position of brick node first + i
+  double red[kWarps * 6];
+};
+template <typename TS>
+constexpr size_t brick_smem_bytes() {
+  return sizeof(BrickShared<TS>);
+}
+
+__device__ __forceinline__ void brick_origin(const BrickView& B, int t, int& x0, int& y0, int& z0) {
+  const int b = __ldg(B.bcoord + t);
+  x0 = (b % B.nbx) * kBX;
+  y0 = ((b / B.nbx) % B.nby) * kBY;
+  z0 = (b / (B.nbx * B.nby)) * kBZ;
+}
+
+// Neighbour table of the 27-point node stencil, grouped by how many elements a
+// node shares with the neighbour (centre 8, faces 4, edges 2, corners 1):
+// staged-region offset of the neighbour, and per shared element its offset in
+// the staged beta region and the K0 block base (3a)*24 + 3b (a, b the corners
+// of node and neighbour in that element).  The gather loops over neighbours at
+// run time (uniform indices, K0 from the constant bank) so the kernel body is
+// ~2 KB of code instead of a 90 KB unrolled stencil that thrashed the
+// instruction cache.
+struct NbEntry {
+  int roff;
+  int eoff[8];
+  int kb[8];
+};
+__constant__ NbEntry c_nb[27];
+constexpr int kNbFace = 1, kNbEdge = 7, kNbCorner = 19;  // class starts: centre [0,1), faces, edges, corners
+
+template <int K, typename TS>
+__device__ __forceinline__ void gather_class(TS (&y)[18], const TS* __restrict__ xs, const TS* __restrict__ bs,
+                                             int pc, int ec, int m0, int m1) {
+#pragma unroll 2
+  for (int m = m0; m < m1; ++m) {
+    TS Sm[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) Sm[q] = TS(0);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const TS bej = bs[ec + c_nb[m].eoff[j]];
+      const int kb = c_nb[m].kb[j];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) Sm[c * 3 + d] = fma_t(bej, k0<TS>(kb + c * 24 + d), Sm[c * 3 + d]);
+    }
+    const TS* xn = xs + pc + c_nb[m].roff;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const TS z0 = xn[(0 * 6 + s) * kRegion], z1 = xn[(1 * 6 + s) * kRegion], z2 = xn[(2 * 6 + s) * kRegion];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        TS v = y[c * 6 + s];
+        v = fma_t(Sm[c * 3 + 0], z0, v);
+        v = fma_t(Sm[c * 3 + 1], z1, v);
+        v = fma_t(Sm[c * 3 + 2], z2, v);
+        y[c * 6 + s] = v;
+      }
+    }
+  }
+}
+
+// FP32 operator: the whole 27-point stencil unrolled so the K0 entries are
+// constant-bank operands of the S-build FFMAs, and the application on packed
+// FFMA2 over load-case pairs (one FFMA2 = two load cases).
+__device__ __forceinline__ void brick_gather_f32(float (&y)[18], const float* __restrict__ xs,
+                                                 const float* __restrict__ bs, int pc, int ec) {
+  float2 acc[9];  // [c][load-case pair]
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = make_float2(0.f, 0.f);
+  float be[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
+    be[e] = bs[ec - oz * (kEX * kEY) - oy * kEX - ox];
+  }
+  const float2* __restrict__ x2 = reinterpret_cast<const float2*>(xs);
+#pragma unroll
+  for (int m = 0; m < 27; ++m) {
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+    float Sm[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) Sm[q] = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
+      const int bx = ox + dx, by = oy + dy, bz = oz + dz;
+      if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+      const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) Sm[c * 3 + d] = fmaf(be[e], c_bK0f[(3 * a + c) * 24 + 3 * b + d], Sm[c * 3 + d]);
+    }
+    const float2* xn = x2 + pc + dz * (kRX * kRY) + dy * kRX + dx;
+#pragma unroll
+    for (int sp = 0; sp < 3; ++sp) {
+      const float2 z0 = xn[(0 * 3 + sp) * kRegion], z1 = xn[(1 * 3 + sp) * kRegion], z2 = xn[(2 * 3 + sp) * kRegion];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float2 v = acc[c * 3 + sp];
+        v = __ffma2_rn(make_float2(Sm[c * 3 + 0], Sm[c * 3 + 0]), z0, v);
+        v = __ffma2_rn(make_float2(Sm[c * 3 + 1], Sm[c * 3 + 1]), z1, v);
+        v = __ffma2_rn(make_float2(Sm[c * 3 + 2], Sm[c * 3 + 2]), z2, v);
+        acc[c * 3 + sp] = v;
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int sp = 0; sp < 3; ++sp) {
+      y[c * 6 + 2 * sp] = acc[c * 3 + sp].x;
+      y[c * 6 + 2 * sp + 1] = acc[c * 3 + sp].y;
+    }
+}
+
+// y (18, component-major q = c*6 + s) = sum over the 27 neighbours of S_m x_m,
+// S_m = sum_e beta_e K0[a(n,e), b(m,e)] built from the staged element betas.
+template <typename TS>
+__device__ __forceinline__ void brick_gather(TS (&y)[18], const TS* __restrict__ xs, const TS* __restrict__ bs, int pc,
+                                             int ec) {
+  if constexpr (sizeof(TS) == 4) {
+    brick_gather_f32(y, xs, bs, pc, ec);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < 18; ++q) y[q] = TS(0);
+  gather_class<8, TS>(y, xs, bs, pc, ec, 0, kNbFace);
+  gather_class<4, TS>(y, xs, bs, pc, ec, kNbFace, kNbEdge);
+  gather_class<2, TS>(y, xs, bs, pc, ec, kNbEdge, kNbCorner);
+  gather_class<1, TS>(y, xs, bs, pc, ec, kNbCorner, 27);
+}
+
+// Last CTA: fixed-order sum of the nab per-brick partials.
+__device__ __forceinline__ bool brick_last_sum(uint32_t* counter, const double* partials, int nab, double (&tot)[6],
+                                               double* scratch) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+#pragma unroll
+  for (int q = 0; q < 6; ++q) tot[q] = 0.0;
+  for (int t = threadIdx.x; t < nab; t += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) tot[q] += __ldcg(partials + t * 6 + q);
+  block_sum<6>(tot, scratch);
+  return true;
+}
+
+// Stage brick t: node map and betas of the region (cp.async), then the input
+// vector at every region position (cp.async straight into shared memory; an
+// FP32 vector for an FP64 operator lands in the high half of its FP64 slot
+// and is converted in place), and the brick's own node positions.
+template <typename TS, typename TG>
+__device__ __forceinline__ void stage_brick(BrickShared<TS>& S, const BrickView& B, int t, int r, int first,
+                                            int last, const int* __restrict__ nmap, const TS* __restrict__ beta,
+                                            const TG* __restrict__ v) {
+  int x0, y0, z0;
+  brick_origin(B, t, x0, y0, z0);
+  constexpr int kPer = (kRegion + kThreads - 1) / kThreads;  // 3
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int p = threadIdx.x + j * kThreads;
+    if (p < kRegion) {
+      const int lx = p % kRX, ly = (p / kRX) % kRY, lz = p / (kRX * kRY);
+      const int gx = wrap3(x0 + lx - 1, r), gy = wrap3(y0 + ly - 1, r), gz = wrap3(z0 + lz - 1, r);
+      cp_async<4>(&S.ms[p], nmap + (static_cast<size_t>(gz) * r + gy) * r + gx);
+    }
+  }
+  cp_async_commit();
+  for (int e = threadIdx.x; e < kERegion; e += kThreads) {
+    const int lx = e % kEX, ly = (e / kEX) % kEY, lz = e / (kEX * kEY);
+    const int gx = wrap3(x0 + lx - 1, r), gy = wrap3(y0 + ly - 1, r), gz = wrap3(z0 + lz - 1, r);
+    cp_async<sizeof(TS)>(&S.bs[e], beta + (static_cast<size_t>(gz) * r + gy) * r + gx);
+  }
+  cp_async_commit();
+  cp_async_wait<1>();  // the map (betas stay in flight)
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int p = threadIdx.x + j * kThreads;
+    if (p >= kRegion) continue;
+    const int id = S.ms[p];
+    const int lx = p % kRX, ly = (p / kRX) % kRY, lz = p / (kRX * kRY);
+    // interior, unwrapped positions carry the brick's own ids
+    const bool inner = lx >= 1 && lx <= kBX && ly >= 1 && ly <= kBY && lz >= 1 && lz <= kBZ && x0 + lx - 1 < r &&
+                       y0 + ly - 1 < r && z0 + lz - 1 < r;
+    if (inner && id >= first && id < last) S.pc[id - first] = static_cast<unsigned short>(p);
+    if (id >= 0) {
+      const TG* src = v + vbase(id, 18);
+#pragma unroll
+      for (int q = 0; q < 18; ++q) {
+        if constexpr (sizeof(TS) == sizeof(TG))
+          cp_async<sizeof(TS)>(&S.xs[xs_index<TS>(q, p)], src + q * 32);
+        else
+          cp_async<sizeof(TG)>(reinterpret_cast<TG*>(&S.xs[xs_index<TS>(q, p)]) + 1, src + q * 32);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 18; ++q) S.xs[xs_index<TS>(q, p)] = TS(0);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  if constexpr (sizeof(TS) != sizeof(TG)) {
+    static_assert(sizeof(TS) == 2 * sizeof(TG), "FP32 -> FP64 staging");
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int p = threadIdx.x + j * kThreads;
+      if (p >= kRegion || S.ms[p] < 0) continue;
+#pragma unroll
+      for (int q = 0; q < 18; ++q) {
+        TS* slot = &S.xs[q * kRegion + p];
+        *slot = static_cast<TS>(reinterpret_cast<const TG*>(slot)[1]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Per-brick fixed-order sum of six doubles into partials[t*6 + s].
+__device__ __forceinline__ void brick_reduce6(double (&v)[6], double* red, double* partials, int t) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[s] += __shfl_xor_sync(0xffffffffu, v[s], o);
+    if (lane == 0) red[w * 6 + s] = v[s];
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double tot = 0.0;
+#pragma unroll
+    for (int u = 0; u < kWarps; ++u) tot += red[u * 6 + threadIdx.x];
+    partials[t * 6 + threadIdx.x] = tot;
+  }
+}
+
+// ---- K4 on bricks: w = A z, p = z + beta p, q = w + beta q, p.q ----------------
+// One CTA per active brick (the hardware scheduler balances; several bricks'
+// CTAs per SM overlap each other's staging and arithmetic).
+template <typename TV, typename TZ, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const ApplyArgs<TV, TZ> A) {
+  extern __shared__ __align__(16) unsigned char brick_raw[];
+  __shared__ double scratch[32 * 6];
+  PcgState* st = A.state;
+  if (st->stop) return;
+  BrickShared<TV>& S = *reinterpret_cast<BrickShared<TV>*>(brick_raw);
+  const BrickView& B = A.bricks;
+  const int t = blockIdx.x;
+  const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
+  const int idx = first + threadIdx.x;
+  const bool valid = idx < last;
+  // own rows first: they land while the brick stages and computes
+  TV pv[18], qv[18];
+  const size_t ob = vbase(valid ? idx : 0, 18);
+  if (valid) {
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {
+      pv[q] = A.p[ob + q * 32];
+      qv[q] = A.q[ob + q * 32];
+    }
+  }
+  stage_brick<TV, TZ>(S, B, t, A.r, first, last, A.node_map, A.beta, A.z);
+  double pq[6] = {0, 0, 0, 0, 0, 0};
+  if (valid) {
+    const TV ridge = static_cast<TV>(st->ridge);
+    const int pc = S.pc[threadIdx.x];
+    const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
+    TV y[18];
+    brick_gather<TV>(y, S.xs, S.bs, pc, lz * (kEX * kEY) + ly * kEX + lx);
+    TV* __restrict__ pg = A.p + ob;
+    TV* __restrict__ qg = A.q + ob;
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {
+      const int s = q % 6;
+      const TV zq = S.xs[xs_index<TV>(q, pc)];
+      const TV w = idx == 0 ? TV(0) : fma_t(ridge, zq, y[q]);  // node 0 (id 0) pinned
+      TV pn = TV(0), qn = TV(0);
+      if (!st->done[s]) {
+        const TV bc = static_cast<TV>(st->beta[s]);
+        pn = fma_t(bc, pv[q], zq);
+        qn = fma_t(bc, qv[q], w);
+      }
+      pg[q * 32] = pn;
+      qg[q * 32] = qn;
+      pq[s] += static_cast<double>(pn) * static_cast<double>(qn);
+    }
+  }
+  brick_reduce6(pq, S.red, A.partials, t);
+  double tot[6];
+  if (!brick_last_sum(&st->counter_apply, A.partials, B.nab, tot, scratch)) return;
+  if (threadIdx.x == 0) {
+    if (A.defer) {
+      for (int s = 0; s < 6; ++s) A.totals[s] = tot[s];
+    } else {
+      finalize_apply_state(st, tot);
+    }
+    st->counter_apply = 0;
+  }
+}
+
+// ---- level-0 V-cycle sweep on bricks ---------------------------------------------
+// mode 0: xout = xin + w Dinv (b - A xin)
+//      1: xout = b - A xin
+//      2: as 0, plus gamma = b.xout (the V-cycle output z = M r; updates beta)
+template <typename TB, typename TV, typename TO, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    brick_sweep_kernel(const GmgLevelView<TV> L, const TB* __restrict__ b, const TV* __restrict__ xin,
+                       TO* __restrict__ xout, TV omega, int mode, PcgState* st, double* partials, int init) {
+  extern __shared__ __align__(16) unsigned char brick_raw[];
+  __shared__ double scratch[32 * 6];
+  if (st->stop) return;
+  BrickShared<TV>& S = *reinterpret_cast<BrickShared<TV>*>(brick_raw);
+  const BrickView& B = L.bricks;
+  const int t = blockIdx.x;
+  const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
+  const int idx = first + threadIdx.x;
+  const bool valid = idx < last;
+  const size_t ob = vbase(valid ? idx : 0, 18);
+  TV D[6];
+  TB bv[18];
+  if (valid) {
+    if (mode != 1) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
+    }
+#pragma unroll
+    for (int q = 0; q < 18; ++q) bv[q] = b[ob + q * 32];
+  }
+  stage_brick<TV, TV>(S, B, t, L.r, first, last, L.node_map, L.beta, xin);
+  double gam[6] = {0, 0, 0, 0, 0, 0};
+  if (valid) {
+    const int pc = S.pc[threadIdx.x];
+    const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
+    TV y[18];
+    brick_gather<TV>(y, S.xs, S.bs, pc, lz * (kEX * kEY) + ly * kEX + lx);
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      TV res[3], xo[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int q = c * 6 + s;
+        const TV xi = S.xs[xs_index<TV>(q, pc)];
+        const TV wv = idx == 0 ? TV(0) : fma_t(L.ridge, xi, y[q]);  // node 0 (id 0) pinned
+        res[c] = static_cast<TV>(bv[q]) - wv;
+        xo[c] = xi;
+      }
+      if (mode == 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s) * 32] = static_cast<TO>(idx == 0 ? TV(0) : res[c]);
+        continue;
+      }
+      const TV z0v = D[0] * res[0] + D[1] * res[1] + D[2] * res[2];
+      const TV z1v = D[1] * res[0] + D[3] * res[1] + D[4] * res[2];
+      const TV z2v = D[2] * res[0] + D[4] * res[1] + D[5] * res[2];
+      xo[0] = fma_t(omega, z0v, xo[0]);
+      xo[1] = fma_t(omega, z1v, xo[1]);
+      xo[2] = fma_t(omega, z2v, xo[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xout[ob + (c * 6 + s) * 32] = static_cast<TO>(xo[c]);
+        if (mode == 2) gam[s] += static_cast<double>(bv[c * 6 + s]) * static_cast<double>(xo[c]);
+      }
+    }
+  }
+  if (mode != 2) return;
+  brick_reduce6(gam, S.red, partials, t);
+  double tot[6];
+  if (!brick_last_sum(&st->counter_misc, partials, B.nab, tot, scratch)) return;
+  if (threadIdx.x == 0) {
+    if (L.totals) {
+      for (int q = 0; q < 6; ++q) L.totals[q] = tot[q];
+    } else {
+      finalize_gamma_state(st, tot, init);
+    }
+    st->counter_misc = 0;
+  }
+}
+
+// Opt a brick kernel into its dynamic shared memory (> 48 KB for FP64).
+template <typename K>
+bool brick_configure(K kernel, size_t smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  return true;
+}
+
+
+}  // namespace
+
+static void build_nb_table(NbEntry (&t)[27]) {
+  int n = 0;
+  for (int k : {8, 4, 2, 1}) {
+    for (int m = 0; m < 27; ++m) {
+      const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+      const int shared = (2 - (dx != 0)) * (2 - (dy != 0)) * (2 - (dz != 0));
+      if (shared != k) continue;
+      NbEntry& e = t[n++];
+      e.roff = dz * (kRX * kRY) + dy * kRX + dx;
+      int j = 0;
+      for (int el = 0; el < 8; ++el) {
+        const int ox = el & 1, oy = (el >> 1) & 1, oz = (el >> 2) & 1;  // node's corner in the element
+        const int bx = ox + dx, by = oy + dy, bz = oz + dz;
+        if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+        e.eoff[j] = -(oz * (kEX * kEY) + oy * kEX + ox);
+        e.kb[j] = 3 * corner_id(ox, oy, oz) * 24 + 3 * corner_id(bx, by, bz);
+        ++j;
+      }
+      for (; j < 8; ++j) e.eoff[j] = e.kb[j] = 0;
+    }
+  }
+}
+
+void brick_upload_constants(const double* K0d, const float* K0f, cudaStream_t s) {
+  static NbEntry table[27];
+  static const bool built = (build_nb_table(table), true);
+  (void)built;
+  cudaMemcpyToSymbolAsync(c_nb, table, sizeof(table), 0, cudaMemcpyHostToDevice, s);
+  cudaMemcpyToSymbolAsync(c_bK0d, K0d, sizeof(double) * 576, 0, cudaMemcpyHostToDevice, s);
+  cudaMemcpyToSymbolAsync(c_bK0f, K0f, sizeof(float) * 576, 0, cudaMemcpyHostToDevice, s);
+}
+
+// Staged brick apply: one resident CTA per slot, bricks from the tile queue.
+template <typename TV, typename TZ>
+void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s) {
+  constexpr size_t smem = brick_smem_bytes<TV>();
+  constexpr int kMinB = sizeof(TV) == 8 ? 3 : 5;
+  static const bool configured = brick_configure(brick_apply_kernel<TV, TZ, kMinB>, smem);
+  (void)configured;
+  brick_apply_kernel<TV, TZ, kMinB><<<a.bricks.nab, kThreads, smem, s>>>(a);
+}
+
+// Staged brick sweep of level 0, one resident CTA per slot.
+template <typename TB, typename TV, typename TO>
+void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, TO* xout, TV omega, int mode,
+                        PcgState* st, double* partials, int init, cudaStream_t s) {
+  constexpr size_t smem = brick_smem_bytes<TV>();
+  constexpr int kMinB = sizeof(TV) == 8 ? 3 : 5;
+  static const bool configured = brick_configure(brick_sweep_kernel<TB, TV, TO, kMinB>, smem);
+  (void)configured;
+  brick_sweep_kernel<TB, TV, TO, kMinB><<<L.bricks.nab, kThreads, smem, s>>>(
+      L, b, xin, xout, omega, mode, st, partials, init);
+}
+
+template void launch_brick_apply<double, float>(const ApplyArgs<double, float>&, cudaStream_t);
+template void launch_brick_apply<double, double>(const ApplyArgs<double, double>&, cudaStream_t);
+template void launch_brick_apply<float, float>(const ApplyArgs<float, float>&, cudaStream_t);
+template void launch_brick_sweep<double, float, float>(const GmgLevelView<float>&, const double*, const float*,
+                                                       float*, float, int, PcgState*, double*, int, cudaStream_t);
+template void launch_brick_sweep<double, float, double>(const GmgLevelView<float>&, const double*, const float*,
+                                                        double*, float, int, PcgState*, double*, int, cudaStream_t);
+template void launch_brick_sweep<float, float, float>(const GmgLevelView<float>&, const float*, const float*,
+                                                      float*, float, int, PcgState*, double*, int, cudaStream_t);
+template void launch_brick_sweep<double, double, double>(const GmgLevelView<double>&, const double*,
+                                                         const double*, double*, double, int, PcgState*, double*,
+                                                         int, cudaStream_t);
+
+}  // namespace shl

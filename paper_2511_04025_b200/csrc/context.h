@@ -96,7 +96,7 @@ struct Misc {
   int touches;
   int n_nodes;
   int n_elem;
-  int pad0;
+  int n_bricks;  // active level-0 bricks (brick numbering)
   int node0_active;
   double beta_sum;
   double pad[4];
@@ -128,6 +128,20 @@ struct shl_ctx {
   // mesh + topology
   DevBuf occ0, occ1, beta64, beta32, elem_flag, node_flag, off, node_map, node_list, elem_list,
       scan_tmp, beta_partials;
+  // brick-major level-0 numbering (brick.cuh): padded flags / offsets, brick
+  // activity / index, active brick table
+  DevBuf bflag, boff, bact, bidx, bcoord, bstart;
+  int n_bricks = 0;
+  shl::BrickView brick_view() const {
+    shl::BrickView v;
+    const shl::BrickDims d = shl::brick_dims(r);
+    v.bcoord = bcoord.as<int>();
+    v.bstart = bstart.as<int>();
+    v.nab = n_bricks;
+    v.nbx = d.nbx;
+    v.nby = d.nby;
+    return v;
+  }
   int64_t n_surface = 0, n_elem = 0;
   int n_nodes = 0, full_fallback = 0, node0_active = 0;
   double volume_ratio = 0.0, beta_sum = 0.0;

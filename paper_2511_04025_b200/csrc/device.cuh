@@ -62,6 +62,17 @@ void launch_scatter_compact(const int* flag, const int* offset, int n, int* map_
                             int* list, cudaStream_t s);
 void launch_fill_int(int* p, int v, size_t n, cudaStream_t s);
 size_t scan_temp_bytes(int n);
+// brick-major level-0 numbering (8x4x4-node bricks, brick.cu): node_map /
+// node_list in brick order, active brick table (bcoord, bstart[nab+1]) and
+// nab written to *nab_out.  Scan temp must hold scan_temp_bytes(np).
+struct BrickDims {
+  int nbx = 0, nby = 0, nbz = 0, nb = 0;
+  long long np = 0;  // padded positions = nb * 256
+};
+BrickDims brick_dims(int r);
+void launch_brick_numbering(const int* node_flag, int r, int* bflag, int* boff, int* bact, int* bidx,
+                            void* temp, size_t temp_bytes, int* node_map, int* node_list, int* bcoord,
+                            int* bstart, int* nab_out, cudaStream_t s);
 void launch_exclusive_scan(const int* in, int* out, int n, void* temp, size_t temp_bytes,
                            cudaStream_t s);
 

@@ -992,6 +992,10 @@ template <typename TB, typename TV>
 void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const TV* xin, TV* xout,
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s) {
+  if (fine && L.bricks.nab > 0) {
+    launch_brick_sweep<TB, TV, TV>(L, b, xin, xout, omega, mode, st, partials, init, s);
+    return;
+  }
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
   static const bool one = std::getenv("SHL_APPLY1") != nullptr;  // A/B: thread-per-node kernels
   if (fine && one) {
@@ -1031,6 +1035,10 @@ bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xout, TV omega,
 template <typename TB, typename TV, typename TO>
 void launch_level_sweep_out(const GmgLevelView<TV>& L, const TB* b, const TV* xin, TO* xout, TV omega,
                             PcgState* st, double* partials, int init, int grid, cudaStream_t s) {
+  if (L.bricks.nab > 0) {
+    launch_brick_sweep<TB, TV, TO>(L, b, xin, xout, omega, 2, st, partials, init, s);
+    return;
+  }
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
   level_sweep3_kernel<TB, TV, true, TO><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, 2, st, partials, init);
 }

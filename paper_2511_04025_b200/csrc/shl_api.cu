@@ -157,15 +157,28 @@ void build_topology(shl_ctx* c) {
   c->node_map.ensure(static_cast<size_t>(n3) * sizeof(int));
   c->node_list.ensure(static_cast<size_t>(n3) * sizeof(int));
   c->elem_list.ensure(static_cast<size_t>(n3) * sizeof(int));
-  const size_t tb = shl::scan_temp_bytes(n3);
+  const shl::BrickDims bd = shl::brick_dims(r);
+  const size_t tb = shl::scan_temp_bytes(static_cast<int>(std::max<long long>(n3, bd.np)));
   c->scan_tmp.ensure(tb);
+  c->bflag.ensure(static_cast<size_t>(bd.np) * sizeof(int));
+  c->boff.ensure(static_cast<size_t>(bd.np) * sizeof(int));
+  c->bact.ensure(static_cast<size_t>(bd.nb) * sizeof(int));
+  c->bidx.ensure(static_cast<size_t>(bd.nb) * sizeof(int));
+  c->bcoord.ensure(static_cast<size_t>(bd.nb) * sizeof(int));
+  c->bstart.ensure(static_cast<size_t>(bd.nb + 1) * sizeof(int));
   int* off_n = c->off.as<int>();
   int* off_e = off_n + n3;
   shl::launch_node_flags(c->elem_flag.as<int>(), r, c->node_flag.as<int>(), c->stream);
+  // grid-order offsets (node counts; the z-slab plans number their slabs from them)
   shl::launch_exclusive_scan(c->node_flag.as<int>(), off_n, n3, c->scan_tmp.p, c->scan_tmp.cap,
                              c->stream);
-  shl::launch_scatter_compact(c->node_flag.as<int>(), off_n, n3, c->node_map.as<int>(),
-                              c->node_list.as<int>(), c->stream);
+  // level-0 node ids in brick-major order: each active 8x8x4 brick owns a
+  // contiguous id range, so the staged brick kernels read their own nodes'
+  // rows coalesced (brick.cuh)
+  shl::launch_brick_numbering(c->node_flag.as<int>(), r, c->bflag.as<int>(), c->boff.as<int>(),
+                              c->bact.as<int>(), c->bidx.as<int>(), c->scan_tmp.p, c->scan_tmp.cap,
+                              c->node_map.as<int>(), c->node_list.as<int>(), c->bcoord.as<int>(),
+                              c->bstart.as<int>(), &c->misc.as<Misc>()->n_bricks, c->stream);
   shl::launch_exclusive_scan(c->elem_flag.as<int>(), off_e, n3, c->scan_tmp.p, c->scan_tmp.cap,
                              c->stream);
   shl::launch_scatter_compact(c->elem_flag.as<int>(), off_e, n3, nullptr, c->elem_list.as<int>(),
@@ -174,7 +187,7 @@ void build_topology(shl_ctx* c) {
   finalize_counts_kernel<<<1, 256, 0, c->stream>>>(c->misc.as<Misc>(), c->node_flag.as<int>(),
                                                    off_n, c->elem_flag.as<int>(), off_e, n3,
                                                    c->beta_partials.as<double>(), nbp);
-  c->launches += 1 + 2 * 2 + 2 + 1;
+  c->launches += 1 + 2 + 2 + 6 + 1;
   CK(cudaGetLastError());
   c->d2h += sizeof(Misc);
   CK(cudaMemcpyAsync(c->hmisc, c->misc.p, sizeof(Misc), cudaMemcpyDeviceToHost, c->stream));
@@ -182,6 +195,7 @@ void build_topology(shl_ctx* c) {
   c->n_nodes = c->hmisc->n_nodes;
   c->n_elem = c->hmisc->n_elem;
   c->node0_active = c->hmisc->node0_active;
+  c->n_bricks = c->hmisc->n_bricks;
   c->beta_sum = c->hmisc->beta_sum;
   c->volume_ratio = c->beta_sum / (double(r) * r * r);
 }
@@ -274,7 +288,8 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
                      std::max<size_t>({static_cast<size_t>(std::max(grid_a, 6 * c->num_sms)) * 6,
                                        static_cast<size_t>((n + 31) / 32) * 6,  // per-tile p.q / r.z
                                        static_cast<size_t>(grid_u) * 2,
-                                       static_cast<size_t>(grid_c) * 21, 64}));
+                                       static_cast<size_t>(grid_c) * 21,
+                                       static_cast<size_t>(c->n_bricks) * 6, 64}));
   c->state.ensure(sizeof(shl::PcgState));
   c->cout.ensure(36 * sizeof(double));
 
@@ -315,6 +330,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
                                        : reinterpret_cast<const TZ*>(c->beta32.p);
     vc.view.push_back({c->node_list.as<int>(), c->node_map.as<int>(), beta_v, nullptr, dinv, r, n, n,
                        static_cast<TZ>(ridge)});
+    vc.view.back().bricks = c->brick_view();
     TZ* g0 = c->gmg0.as<TZ>();
     vc.b.push_back(nullptr);
     vc.xa.push_back(g0);
@@ -350,6 +366,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
                                 static_cast<TZ>(vc.gp.omega)};
   shl::ApplyArgs<TV, TZ> aa{c->node_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p, q,
                         c->partials.as<double>(), dst, r, n, ld, n, 0, r, nullptr, 0};
+  aa.bricks = c->brick_view();
   vc.st = dst;
   // z = M r: block Jacobi inside the update kernel, or the V-cycle
   auto precondition = [&](int init) {

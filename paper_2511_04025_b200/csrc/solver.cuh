@@ -10,6 +10,17 @@
 
 namespace shl {
 
+// Level-0 brick tables (brick.cu): active bricks of 8x4x4 nodes in
+// brick-major order, each owning the contiguous node ids
+// [bstart[t], bstart[t+1]).  nab == 0: no brick numbering (z-slab levels), the
+// per-node gather kernels run instead.
+struct BrickView {
+  const int* bcoord = nullptr;  // active brick t -> brick id bx + nbx*(by + nby*bz)
+  const int* bstart = nullptr;  // nab + 1 entries
+  int nab = 0;
+  int nbx = 0, nby = 0;
+};
+
 // TV: Krylov vectors p, q and the operator arithmetic; TZ: the preconditioned
 // residual z (the multigrid V-cycle's type).  Mixed multigrid runs TV = double
 // with TZ = float: w = A z is accumulated in FP64 from the FP32 z, so p^T A p
@@ -32,6 +43,7 @@ struct ApplyArgs {
   int nzl;        // node-map planes (r when not slabbed)
   double* totals; // defer != 0: write the 6 reduced sums here, leave state alone
   int defer;
+  BrickView bricks;  // nab > 0: staged brick kernel (brick.cuh)
 };
 
 template <typename TX, typename TV, typename TZ = TV>
@@ -96,6 +108,7 @@ struct GmgLevelView {
   TV ridge;
   int zbase = 0;             // level 0 of a z-slab: global z of local node-map plane 0
   double* totals = nullptr;  // non-null: the last sweep writes its 6 r.z sums here (slabs)
+  BrickView bricks{};        // level 0 with brick numbering: staged brick sweeps
 };
 
 void launch_coarse_flags(const int* map_f, int r_f, int r_c, int* flag_c, cudaStream_t s);
@@ -158,6 +171,13 @@ void launch_setup(const int* node_list, int n_nodes, int ld, int r, const double
                   double ridge, TX* rvec, TV* dinv, cudaStream_t s);
 template <typename TV, typename TZ>
 void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s);
+// Staged brick kernels of level 0 (brick.cu); used when a.bricks.nab > 0.
+template <typename TV, typename TZ>
+void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s);
+template <typename TB, typename TV, typename TO>
+void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, TO* xout, TV omega, int mode,
+                        PcgState* st, double* partials, int init, cudaStream_t s);
+void brick_upload_constants(const double* K0d, const float* K0f, cudaStream_t s);
 // Grid (block count) launch_apply / launch_level_sweep use for n nodes; the
 // caller sizes its partials buffer as 6 doubles per block.
 int apply_grid(int n, int num_sms);

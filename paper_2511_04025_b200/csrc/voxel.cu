@@ -192,6 +192,66 @@ __global__ void scatter_kernel(const int* __restrict__ flag, const int* __restri
   if (f) list[off[i]] = i;
 }
 
+// ---- brick-major level-0 node numbering (brick.cuh) -------------------------
+// Padded brick-major index p = brick * 256 + (lz*8 + ly)*8 + lx over
+// ceil(r/8) x ceil(r/8) x ceil(r/4) bricks of 8x8x4 nodes; positions outside
+// the torus (ragged last bricks) are never active.
+constexpr int kBrickX = 8, kBrickY = 4, kBrickZ = 4, kBrickN = kBrickX * kBrickY * kBrickZ;
+
+__device__ __forceinline__ long long brick_to_grid(long long p, int r, int nbx, int nby) {
+  const long long b = p / kBrickN;
+  const int w = static_cast<int>(p % kBrickN);
+  const int x = static_cast<int>(b % nbx) * kBrickX + w % kBrickX;
+  const int y = static_cast<int>((b / nbx) % nby) * kBrickY + (w / kBrickX) % kBrickY;
+  const int z = static_cast<int>(b / (static_cast<long long>(nbx) * nby)) * kBrickZ + w / (kBrickX * kBrickY);
+  if (x >= r || y >= r || z >= r) return -1;
+  return (static_cast<long long>(z) * r + y) * r + x;
+}
+
+__global__ void brick_flag_kernel(const int* __restrict__ node_flag, int r, int nbx, int nby, long long np,
+                                  int* __restrict__ bflag) {
+  const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (p >= np) return;
+  const long long g = brick_to_grid(p, r, nbx, nby);
+  bflag[p] = g >= 0 ? node_flag[g] : 0;
+}
+
+__global__ void brick_scatter_kernel(const int* __restrict__ bflag, const int* __restrict__ boff, int r, int nbx,
+                                     int nby, long long np, int* __restrict__ map, int* __restrict__ list) {
+  const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (p >= np) return;
+  const long long g = brick_to_grid(p, r, nbx, nby);
+  if (g < 0) return;
+  const int f = bflag[p];
+  map[g] = f ? boff[p] : -1;
+  if (f) list[boff[p]] = static_cast<int>(g);
+}
+
+__global__ void brick_active_kernel(const int* __restrict__ bflag, const int* __restrict__ boff, int nb,
+                                    int* __restrict__ bact) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const long long first = static_cast<long long>(b) * kBrickN, last = first + kBrickN - 1;
+  bact[b] = (boff[last] + bflag[last] - boff[first]) > 0;
+}
+
+__global__ void brick_table_kernel(const int* __restrict__ bact, const int* __restrict__ bidx,
+                                   const int* __restrict__ boff, const int* __restrict__ bflag, int nb,
+                                   int* __restrict__ bcoord, int* __restrict__ bstart, int* __restrict__ nab_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  if (bact[b]) {
+    bcoord[bidx[b]] = b;
+    bstart[bidx[b]] = boff[static_cast<long long>(b) * kBrickN];
+  }
+  if (b == nb - 1) {
+    const int nab = bidx[b] + bact[b];
+    const long long lastp = static_cast<long long>(nb) * kBrickN - 1;
+    bstart[nab] = boff[lastp] + bflag[lastp];
+    *nab_out = nab;
+  }
+}
+
 __global__ void fill_int_kernel(int* p, int v, size_t n) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   if (i < n) p[i] = v;
@@ -252,6 +312,29 @@ void launch_scatter_compact(const int* flag, const int* off, int n, int* map, in
 
 void launch_fill_int(int* p, int v, size_t n, cudaStream_t s) {
   if (n) fill_int_kernel<<<blocks(n, 256), 256, 0, s>>>(p, v, n);
+}
+
+BrickDims brick_dims(int r) {
+  BrickDims d;
+  d.nbx = (r + kBrickX - 1) / kBrickX;
+  d.nby = (r + kBrickY - 1) / kBrickY;
+  d.nbz = (r + kBrickZ - 1) / kBrickZ;
+  d.nb = d.nbx * d.nby * d.nbz;
+  d.np = static_cast<long long>(d.nb) * kBrickN;
+  return d;
+}
+
+void launch_brick_numbering(const int* node_flag, int r, int* bflag, int* boff, int* bact, int* bidx,
+                            void* temp, size_t temp_bytes, int* node_map, int* node_list, int* bcoord,
+                            int* bstart, int* nab_out, cudaStream_t s) {
+  const BrickDims d = brick_dims(r);
+  brick_flag_kernel<<<blocks(d.np, 256), 256, 0, s>>>(node_flag, r, d.nbx, d.nby, d.np, bflag);
+  cub::DeviceScan::ExclusiveSum(temp, temp_bytes, bflag, boff, static_cast<int>(d.np), s);
+  brick_scatter_kernel<<<blocks(d.np, 256), 256, 0, s>>>(bflag, boff, r, d.nbx, d.nby, d.np, node_map,
+                                                         node_list);
+  brick_active_kernel<<<blocks(d.nb, 256), 256, 0, s>>>(bflag, boff, d.nb, bact);
+  cub::DeviceScan::ExclusiveSum(temp, temp_bytes, bact, bidx, d.nb, s);
+  brick_table_kernel<<<blocks(d.nb, 256), 256, 0, s>>>(bact, bidx, boff, bflag, d.nb, bcoord, bstart, nab_out);
 }
 
 size_t scan_temp_bytes(int n) {
