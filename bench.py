@@ -15,8 +15,12 @@ Under torchrun each rank drives its own GPU with its own designs (weak
 scaling: independent designs, no data-path collective); rank 0 prints one
 JSON line.  --impl reference times the reference CPU path (the reference's
 own field/voxel code via oracle/_ref + the oracle's restatement of its PCG)
-on the host cores, on a bounded sample (field + mesh in full, a few PCG
-iterations, solve extrapolated by the design's lockstep iteration count).
+on the host cores, on a bounded sample: field + mesh in full, a few PCG
+iterations timed, the 128^3 solve extrapolated by the design's lockstep
+iteration count of the reference algorithm (marked "extrapolated": true), and
+one complete, non-extrapolated C1 (32^3) homogenization; with all host
+threads and with threads=1 (the reference's homogenize default,
+pipeline.hpp:16).
 """
 from __future__ import annotations
 
@@ -35,10 +39,11 @@ sys.path.insert(0, ROOT)
 METRIC = "C^H homogenizations/sec at 128^3 (ms/design: field, solve) at 1/2/4/8 B200"
 UNIT = "designs/s"
 
-# Lockstep (max over the 6 columns) PCG iteration counts of the bench designs at
-# r=128, rtol 1e-5, measured by full solves (tools/probe.py; FP64 and mixed agree
-# to +-1; GPU run of 2026-10-18, profiles/README.md).  Used only to extrapolate
-# the bounded CPU-reference sample.
+# Lockstep (max over the 6 columns) iteration counts of the reference algorithm
+# (block-Jacobi PCG, grid_solver.hpp:37-96, FP64) for the bench designs at
+# r=128, rtol 1e-5, from full GPU solves (tools/probe.py, round 1).  The GPU arm
+# re-measures the count of its cpu_baseline seed in the same run; the
+# reference arm (which runs no GPU code) extrapolates with this table.
 ITERS_128 = {1: 1117, 2: 1106, 3: 1524, 4: 1164, 5: 1181, 6: 950, 7: 916, 8: 1069,
              9: 1128, 10: 1072}
 
@@ -48,8 +53,9 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=16)
     p.add_argument("--warmup", type=int, default=4)
-    p.add_argument("--lanes", type=int, default=2,
-                   help="designs in flight at once per GPU (shl_set_batch_lanes)")
+    p.add_argument("--lanes", type=int, default=1,
+                   help="designs in flight at once per GPU (shl_set_batch_lanes); 1 = reproducible "
+                        "(2 lanes can fall into a contended mode, DESIGN.md 4.2)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--r", type=int, default=128)
     p.add_argument("--tol", type=float, default=1e-5)
@@ -172,15 +178,25 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------------------ CPU reference sample
-def cpu_reference_design(seed, args, threads):
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_reference_design(seed, args, threads, iters, cpu_iters=None):
     """The reference CPU path on one 128^3 design, bounded: field + mesh in full
     (the reference's own field.hpp / voxel.hpp through oracle/_ref when built,
     else the oracle restatement), `cpu_iters` masked PCG iterations
-    (grid_solver.hpp restated), the rest of the solve extrapolated."""
-    import numpy as np
-
+    (grid_solver.hpp restated) timed, the solve extrapolated to `iters`."""
     import oracle as O
     use_ref = O.have_ref()
+    n_it = cpu_iters if cpu_iters is not None else args.cpu_iters
     d = O.random_design("cubic_octant", 8, 2, -1.0, 1.0, seed)
     t0 = time.perf_counter()
     g = O.sample_grid(d, args.r, threads=threads, use_ref=use_ref)
@@ -188,40 +204,78 @@ def cpu_reference_design(seed, args, threads):
     m = O.build_reduced_mesh(g)
     t2 = time.perf_counter()
     K0 = O.element_stiffness(1.0, 0.3, 1.0 / args.r)
-    res = O.grid_solve(m.beta, K0, tol=args.tol, max_iter=args.cpu_iters, threads=threads,
-                       allow_unconverged=True)
+    res = O.grid_solve(m.beta, K0, tol=args.tol, max_iter=n_it, threads=threads, allow_unconverged=True)
     t3 = time.perf_counter()
-    it_full = ITERS_128.get(seed, 1115) if args.r == 128 else None
-    per_it = res.t_solve_ms / max(args.cpu_iters, 1) / 1e3
-    solve_s = per_it * (it_full if it_full else args.cpu_iters)
+    per_it = res.t_solve_ms / max(n_it, 1) / 1e3
+    solve_s = per_it * iters
     total = (t1 - t0) + (t2 - t1) + res.t_rhs_ms / 1e3 + solve_s + res.t_reduce_ms / 1e3
-    return {"t_field_s": t1 - t0, "t_mesh_s": t2 - t1, "per_iter_s": per_it, "iters": it_full,
+    return {"t_field_s": t1 - t0, "t_mesh_s": t2 - t1, "per_iter_s": per_it, "iters": iters,
             "total_s": total, "field_from": "reference field.hpp (oracle/_ref)" if use_ref else "oracle port",
-            "sample_s": t3 - t0}
+            "sample_s": t3 - t0, "threads": threads}
+
+
+def cpu_c1_full(threads):
+    """One complete C1 homogenization (32^3, CubicOctant 2 pre -> 16 charges, seed 1,
+    rtol 1e-5) through the oracle pipeline: measured end to end, not extrapolated."""
+    import oracle as O
+    d = O.random_design("cubic_octant", 2, 2, -1.0, 1.0, 1)
+    t0 = time.perf_counter()
+    res = O.homogenize(d, 32, tol=1e-5, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"config": "C1 32^3 seed 1, rtol 1e-5, full pipeline", "threads": threads, "seconds": dt,
+            "designs_per_s": 1.0 / dt, "iterations": [int(v) for v in res.iterations]}
+
+
+def cpu_baseline_block(seed, args, iters, iters_source, nproc):
+    """cpu_baseline object: all threads (the headline value) and threads=1, both
+    extrapolated at 128^3, plus the measured C1 full solve."""
+    full = cpu_reference_design(seed, args, nproc, iters)
+    one = cpu_reference_design(seed, args, 1, iters, cpu_iters=1)
+    c1 = cpu_c1_full(nproc)
+    return {"value": 1.0 / full["total_s"], "unit": UNIT, "cores": nproc, "kind": "port",
+            "extrapolated": True, "cpu_model": cpu_model(),
+            "sample": f"seed {seed} at {args.r}^3: field+mesh in full ({full['field_from']}), "
+                      f"{args.cpu_iters} masked block-Jacobi PCG iterations timed "
+                      f"({full['per_iter_s']*1e3:.0f} ms each on {nproc} threads), solve extrapolated to "
+                      f"{iters} lockstep iterations ({iters_source}); {full['sample_s']:.1f} s of CPU work",
+            "iters": iters, "iters_source": iters_source,
+            "threads_1": {"value": 1.0 / one["total_s"], "unit": UNIT, "cores": 1, "extrapolated": True,
+                          "per_iter_s": one["per_iter_s"], "t_field_s": one["t_field_s"]},
+            "c1_full_measured": c1}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
+    nproc = os.cpu_count() or 1
     warm, timed = seeds_for(0, args.steps, 0)
-    timed = timed[:12]  # ~12 s of CPU work per design: keep the whole arm within a few minutes
+    timed = timed[:3]  # bounded: ~15 s of CPU work per design, the whole arm within a few minutes
     times, samples = [], []
     for s in timed:
-        r = cpu_reference_design(s, args, threads)
+        it = ITERS_128.get(s, 1115) if args.r == 128 else args.cpu_iters
+        r = cpu_reference_design(s, args, nproc, it)
         times.append(r["total_s"])
         samples.append(r)
+    one = cpu_reference_design(timed[0], args, 1, samples[0]["iters"], cpu_iters=1)
+    c1 = cpu_c1_full(nproc)
+    c1_one = cpu_c1_full(1)
     per = statistics.mean(times)
     val = 1.0 / per
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference", "config": config(args, 1),
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+            "impl": "reference", "config": config(args, 1), "extrapolated": True,
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": nproc, "kind": "port", "extrapolated": True,
+                             "cpu_model": cpu_model(),
                              "sample": f"{len(timed)} designs at {args.r}^3: field+mesh in full "
                                        f"({samples[0]['field_from']}), {args.cpu_iters} masked PCG "
-                                       f"iterations timed, solve extrapolated to the design's "
-                                       f"lockstep count (~{samples[0]['iters']})"},
+                                       f"iterations timed, solve extrapolated to the design's lockstep "
+                                       f"count of the reference algorithm ({[x['iters'] for x in samples]}, "
+                                       f"FP64 block-Jacobi PCG, bench.py ITERS_128)",
+                             "threads_1": {"value": 1.0 / one["total_s"], "unit": UNIT, "cores": 1,
+                                           "extrapolated": True, "per_iter_s": one["per_iter_s"],
+                                           "t_field_s": one["t_field_s"]},
+                             "c1_full_measured": {"all_threads": c1, "threads_1": c1_one}},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "detail": {"t_field_s": statistics.mean(x["t_field_s"] for x in samples),
                        "t_mesh_s": statistics.mean(x["t_mesh_s"] for x in samples),
@@ -337,8 +391,10 @@ def run_ours(args, rank, world, local):
     line = {"metric": METRIC, "value": total_designs / dev_max, "unit": UNIT, "n_gpus": world,
             "steps": len(designs), "warmup": args.warmup, "ms_per_step": dev_max / len(designs) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": {"mixed": "f64 field/C^H, f32 apply + f64 x/r", "fp32": "f64 field/C^H, f32 PCG",
-                      "fp64": "f64"}[args.precision],
+            "dtype": ({"mixed": "f64 (field, C^H, Krylov x/r/p/q and the A.z operator); f32 multigrid V-cycle and z",
+                       "fp32": "f64 field/C^H, f32 PCG", "fp64": "f64"}[args.precision] if gmg else
+                      {"mixed": "f64 field/C^H and x/r; f32 operator, p/q, z (block-Jacobi PCG)",
+                       "fp32": "f64 field/C^H, f32 PCG", "fp64": "f64"}[args.precision]),
             "data": "synthetic (seeded random_design, no checkpoint/dataset)",
             "config": config(args, world),
             "e2e": {"value": total_designs / wall_max, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -369,14 +425,18 @@ def run_ours(args, rank, world, local):
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_design(timed[0], args, os.cpu_count() or 1)
-            line["cpu_baseline"] = {"value": 1.0 / cb["total_s"], "unit": UNIT,
-                                    "cores": os.cpu_count() or 1, "kind": "port",
-                                    "sample": f"seed {timed[0]} at {args.r}^3: field+mesh in full "
-                                              f"({cb['field_from']}), {args.cpu_iters} masked PCG "
-                                              f"iterations timed ({cb['per_iter_s']*1e3:.0f} ms each), "
-                                              f"solve extrapolated to {cb['iters']} iterations; "
-                                              f"{cb['sample_s']:.1f} s of CPU work"}
+            # the reference algorithm's iteration count for this seed, measured in
+            # this run: FP64 block-Jacobi PCG on the GPU (untimed)
+            seed0 = timed[0]
+            iters_source = "FP64 block-Jacobi PCG of the same design on the GPU, this run"
+            try:
+                jopt = S.HomogenizeOptions(residual_tol=args.tol, precision="fp64", preconditioner="jacobi")
+                jr = S.homogenize(designs[0], sp, mat, args.r, jopt, ctx=ctx)
+                iters = int(max(jr.iterations))
+            except Exception as e:  # pragma: no cover - fall back to the committed table
+                iters = ITERS_128.get(seed0, 1115)
+                iters_source = f"bench.py ITERS_128 (GPU check failed: {e})"
+            line["cpu_baseline"] = cpu_baseline_block(seed0, args, iters, iters_source, os.cpu_count() or 1)
         except Exception as e:  # the baseline must never block the GPU line
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1,
                                     "kind": "port", "sample": f"failed: {e}"}

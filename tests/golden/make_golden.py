@@ -38,7 +38,11 @@ def cases():
     out.append(("c1_seed1", lambda: O.random_design("cubic_octant", 2, 2, -1, 1, 1, use_ref=True), (16,), (32,)))
     out.append(("none64_seed7", lambda: O.random_design("none", 64, 2, -1, 1, 7, use_ref=True), (8,), (32,)))
     out.append(("tetra_seed5", lambda: O.random_design("tetrahedral", 2, 2, -1, 1, 5, use_ref=True), (8,), (16,)))
-    out.append(("c3_seed1", lambda: O.random_design("cubic_octant", 8, 2, -1, 1, 1, use_ref=True), (), (64,)))
+    # bench configuration C3 (BASELINE.json configs[2]: 128^3, CubicOctant 8 pre -> 64 charges):
+    # the first timed bench seeds; and C5 (256^3, seed 1)
+    for seed in (1, 2, 3):
+        out.append((f"c3_seed{seed}", lambda s=seed: O.random_design("cubic_octant", 8, 2, -1, 1, s, use_ref=True),
+                    (), ((64, 128, 256) if seed == 1 else (128,))))
     out.append(("gyroid", O.gyroid_design, (16,), (32, 64)))
     out.append(("plane_z", lambda: O.plane_design_z(0.5 / 32), (16,), (32,)))
     return out
@@ -73,6 +77,13 @@ def main() -> None:
                                               info["corner_group_size"]], np.int64)
             manifest[key] = dict(centres=sha(g.samples), corners=sha(g.corners), elements=sha(el),
                                  beta=sha(be))
+            if r >= 128:
+                # beta is compared to 1e-12 relative on the device (exp differs), so
+                # large grids keep a deterministic sample of it instead of the digest
+                idx = np.linspace(0, len(el) - 1, 4096).astype(np.int64)
+                arrays[f"{key}/beta_sample_idx"] = idx
+                arrays[f"{key}/beta_sample"] = be[idx]
+                arrays[f"{key}/beta_sum"] = np.array([be.sum()])
     vs = np.linspace(-0.3, 0.3, 121)
     for sharp, fl in ((500.0, 1e-3), (140.0, 0.01), (100.0, 1e-3)):
         arrays[f"step/{sharp}_{fl}"] = np.array([O.step_function(v, sharp, fl, use_ref=True) for v in vs])
