@@ -5,7 +5,9 @@
 // the device through one shl_homogenize call.  Errors carry the reference's
 // stage prefixes ("field: ", "mesh: ", "solve: ").  solver_used reports the
 // device solver ("device_pcg_mixed" / "device_pcg_fp64" / ...) instead of
-// "grid_cg" / "direct_ldlt" (solver-name contract).
+// "grid_cg" / "direct_ldlt" (solver-name contract).  Like the
+// reference, the result carries the sampled grid and the reduced mesh (with
+// its lattice topology); return_fields = false skips those readbacks.
 #pragma once
 
 #include <sstream>
@@ -19,19 +21,19 @@ enum class SolverKind { Auto, Direct, GridCG };
 
 struct HomogenizeOptions {
   int threads = 1;                      // accepted, unused (device path)
-  SolverKind solver = SolverKind::Auto;  // every kind maps to the device PCG
+  SolverKind solver = SolverKind::Auto;  // the device PCG; GridCG keeps the reference's full-grid check
   double residual_tol = 1e-9;
   int corner_gauge = 0;                 // any gauge gives the same tensor
   int precision = SHL_PREC_AUTO;        // device arithmetic (shellular_cuda.h)
   int max_iter = 0;
   int preconditioner = SHL_PRECOND_AUTO;  // multigrid V-cycle when r allows (shellular_cuda.h)
-  bool return_fields = false;           // copy the grid + element list back
+  bool return_fields = true;            // fill res.grid / res.mesh as the reference does (pipeline.hpp:70,74)
 };
 
 struct HomogenizationResult {
   ElasticTensor tensor;
-  FieldGrid grid;   // filled when opt.return_fields
-  VoxelMesh mesh;   // resolution / full_fallback always; elements when return_fields
+  FieldGrid grid;   // samples when opt.return_fields (default)
+  VoxelMesh mesh;   // resolution / full_fallback always; elements, beta, topology when return_fields
   StageTimings timings;
   double volume_ratio = 0.0;
   double element_fraction = 0.0;
@@ -62,6 +64,9 @@ inline HomogenizationResult homogenize(const DesignParams& params, const ShellPa
   double C[36];
   shl_ctx* ctx = detail::context();
   detail::check(shl_homogenize(ctx, &a.d, &spa, &ma, r, &o, C, &res.stats), ctx);
+  // pipeline.hpp:81-88: the grid solver only accepts the full-grid fallback mesh
+  if (opt.solver == SolverKind::GridCG && res.stats.full_fallback == 0)
+    throw SolverError("solve: grid solver requires the full-grid fallback mesh");
   for (int i = 0; i < 6; ++i)
     for (int j = 0; j < 6; ++j) res.tensor.c(i, j) = C[i * 6 + j];
   const shl_stats& st = res.stats;

@@ -3,13 +3,18 @@
 // ShellParams (:18-34), step_function (:38-41), classify_surface_elements
 // (:118-141) and build_reduced_mesh (:235-313) with the reference's
 // semantics; the element selection and beta run on the device (identical
-// element sets, beta within 1e-12 relative).  The node bookkeeping of
-// build_topology (:147-228) is implicit on the device (active torus nodes);
-// VoxelMesh therefore carries the element list, beta and counts but does not
-// materialize node_coords / periodic_groups.
+// element sets, beta within 1e-12 relative).  The device solver needs no
+// lattice topology (active torus nodes are implicit), but the drop-in
+// VoxelMesh carries the reference's: element_nodes, node_coords, node_class,
+// periodic_groups and corner_group with build_topology's (:147-228) numbering,
+// built on the host from the returned element list (detail::build_topology).
 #pragma once
 
+#include <algorithm>
+#include <chrono>
 #include <fstream>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "field.hpp"
@@ -38,14 +43,29 @@ inline double step_function(double v, const ShellParams& sp) {
   return 1.0 + 0.5 * v0 - v0 / (1.0 + std::exp(-sp.sharpness * v * v));
 }
 
+enum class NodeClass : std::uint8_t { Interior, Face, Edge, Corner };
+
+struct PeriodicGroup {
+  std::uint32_t master = 0;                             // node with all offsets zero
+  std::vector<std::pair<std::uint32_t, Vec3i>> slaves;  // (node, lattice offset in {0,1}^3)
+};
+
 struct VoxelMesh {
   int resolution = 0;
   std::vector<std::uint32_t> elements;  // sorted linear ids (k*r + j)*r + i
   std::vector<double> beta;             // per element
+  std::vector<std::uint32_t> element_nodes;  // 8 per element (voxel.hpp:147-228 numbering)
+  std::vector<Vec3i> node_coords;            // lattice ints in [0, r]
+  std::vector<NodeClass> node_class;
+  std::vector<PeriodicGroup> periodic_groups;
+  int corner_group = -1;  // index into periodic_groups, -1 if absent
   bool full_fallback = false;
+  double t_select_ms = 0.0;    // element selection + beta (device)
+  double t_topology_ms = 0.0;  // node numbering + periodic groups (host)
   std::int64_t active_nodes = 0;  // torus nodes touched by an element (device count)
 
   size_t num_elements() const { return elements.size(); }
+  size_t num_nodes() const { return node_coords.size(); }
   double element_fraction() const {
     return double(elements.size()) / (double(resolution) * resolution * resolution);
   }
@@ -79,6 +99,79 @@ struct VoxelMesh {
 };
 
 namespace detail {
+// The reference's lattice topology (voxel.hpp:147-228): nodes numbered in order
+// of first use over the sorted element list (hex corner order of
+// element_stiffness), boundary nodes grouped by lattice position mod r, groups
+// in increasing key order, each group's members in node order; the same group
+// checks and error messages.  A dense (r+1)^3 lattice index replaces the
+// reference's hash maps (same result, linear time).
+inline void build_topology(VoxelMesh& m) {
+  const int r = m.resolution;
+  const size_t r1 = static_cast<size_t>(r) + 1;
+  static const int off[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
+                                {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+  std::vector<std::int32_t> id(r1 * r1 * r1, -1);
+  m.element_nodes.assign(m.elements.size() * 8, 0);
+  m.node_coords.clear();
+  m.node_coords.reserve(m.elements.size() + m.elements.size() / 4);
+  for (size_t e = 0; e < m.elements.size(); ++e) {
+    const Vec3i c = VoxelMesh::element_coords(m.elements[e], r);
+    for (int n = 0; n < 8; ++n) {
+      const int i = c[0] + off[n][0], j = c[1] + off[n][1], k = c[2] + off[n][2];
+      std::int32_t& slot = id[(static_cast<size_t>(k) * r1 + j) * r1 + i];
+      if (slot < 0) {
+        slot = static_cast<std::int32_t>(m.node_coords.size());
+        m.node_coords.emplace_back(i, j, k);
+      }
+      m.element_nodes[e * 8 + n] = static_cast<std::uint32_t>(slot);
+    }
+  }
+  const size_t nn = m.node_coords.size();
+  m.node_class.assign(nn, NodeClass::Interior);
+  std::vector<std::pair<std::uint64_t, std::uint32_t>> boundary;  // (key mod r, node)
+  for (size_t n = 0; n < nn; ++n) {
+    const Vec3i& c = m.node_coords[n];
+    int b = 0;
+    for (int a = 0; a < 3; ++a) b += (c[a] == 0 || c[a] == r);
+    m.node_class[n] = static_cast<NodeClass>(b);
+    if (b == 0) continue;
+    const std::uint64_t key =
+        (static_cast<std::uint64_t>(c[2] % r) * r1 + static_cast<std::uint64_t>(c[1] % r)) * r1 + (c[0] % r);
+    boundary.emplace_back(key, static_cast<std::uint32_t>(n));
+  }
+  std::sort(boundary.begin(), boundary.end());  // by key, members in node order
+  m.periodic_groups.clear();
+  m.corner_group = -1;
+  for (size_t a = 0; a < boundary.size();) {
+    size_t b = a;
+    while (b < boundary.size() && boundary[b].first == boundary[a].first) ++b;
+    PeriodicGroup g;
+    bool found_master = false;
+    for (size_t q = a; q < b; ++q) {
+      const std::uint32_t n = boundary[q].second;
+      const Vec3i& c = m.node_coords[n];
+      const Vec3i delta(c[0] == r, c[1] == r, c[2] == r);
+      if (delta == Vec3i::Zero()) {
+        g.master = n;
+        found_master = true;
+      } else {
+        g.slaves.emplace_back(n, delta);
+      }
+    }
+    if (!found_master)
+      throw SolverError("periodic group without master node: mesh is not periodically complete");
+    int axes = 0;
+    for (int d = 0; d < 3; ++d) axes += (m.node_coords[g.master][d] % r == 0);
+    const size_t expect = size_t(1) << axes;
+    if (b - a != expect)
+      throw SolverError("periodic group has " + std::to_string(b - a) + " members, expected " +
+                        std::to_string(expect));
+    if (axes == 3) m.corner_group = static_cast<int>(m.periodic_groups.size());
+    m.periodic_groups.push_back(std::move(g));
+    a = b;
+  }
+}
+
 inline shl_ctx* load_grid(const FieldGrid& grid) {
   shl_ctx* ctx = context();
   check(shl_load_grid(ctx, grid.resolution, grid.samples.data(), grid.corner_samples.data(), grid.norm),
@@ -109,10 +202,15 @@ inline VoxelMesh build_reduced_mesh(const FieldGrid& grid, const ShellParams& sp
   std::int64_t n = 0;
   std::int32_t ff = 0;
   const shl_shell_params p = sp.abi();
+  const auto t0 = std::chrono::steady_clock::now();
   detail::check(shl_build_reduced_mesh(ctx, &p, m.elements.data(), m.beta.data(), &n, &ff), ctx);
+  const auto t1 = std::chrono::steady_clock::now();
   m.elements.resize(static_cast<size_t>(n));
   m.beta.resize(static_cast<size_t>(n));
   m.full_fallback = ff != 0;
+  detail::build_topology(m);
+  m.t_select_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  m.t_topology_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
   return m;
 }
 
@@ -125,6 +223,7 @@ inline VoxelMesh full_solid_mesh(int r, double beta_value = 1.0) {
   m.beta.assign(total, beta_value);
   m.full_fallback = true;
   m.active_nodes = static_cast<std::int64_t>(total);
+  detail::build_topology(m);
   return m;
 }
 

@@ -90,6 +90,15 @@ enum {
   SHL_PRECOND_AUTO = 2    /* GMG when r is even and r/2 >= 8, else block Jacobi */
 };
 
+/* Solver options.  Ridge: the reference regularizes a singular system with
+ * 1e-11 * mean|diag A| when a component floats or the factorization fails
+ * (fem.hpp:337-350).  Floating components are the common case for shell
+ * meshes and hinge modes are not detected up front, so the device
+ * PCG always adds that ridge to its Krylov operator when it is FP64 (C^H moves
+ * by O(1e-11), tested against the unridged direct solve at 1e-8); FP32-storage
+ * operators and preconditioners use 1e-8 * mean|diag A| (tested against the
+ * FP64 solve at 1e-6).  stats.n_floating reports whether the reference would
+ * have ridged (expect_singular). */
 typedef struct {
   double tol;         /* per-column ||r|| <= tol*||b|| (grid_solver.hpp:68) */
   int max_iter;       /* 0 = 20r+2000 (grid_solver.hpp:38) */
@@ -121,6 +130,10 @@ typedef struct {
   int32_t gmg_levels;      /* multigrid levels incl. the fine one (0 = block Jacobi) */
   int32_t precond_fallback; /* 1: AUTO multigrid broke down, solved with block Jacobi;
                                2: mixed multigrid redone with the FP64-accumulated operator */
+  int32_t n_components;     /* mechanically connected element components: elements sharing a
+                               torus node are coupled (fem.hpp:288-317 union-find criterion) */
+  int32_t n_floating;       /* components without an element at torus node 0: their rigid
+                               motions are null modes (the reference's expect_singular) */
 } shl_stats;
 
 int shl_ctx_create(int device, shl_ctx** out);

@@ -47,7 +47,8 @@ class shl_stats(C.Structure):
                 ("apply_ms", C.c_double), ("update_ms", C.c_double),
                 ("apply_launches", C.c_int64), ("kernel_launches", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("gmg_levels", C.c_int32), ("precond_fallback", C.c_int32)]
+                ("gmg_levels", C.c_int32), ("precond_fallback", C.c_int32),
+                ("n_components", C.c_int32), ("n_floating", C.c_int32)]
 
 
 # every symbol include/shellular_cuda.h declares (checked by tests/test_abi.py)

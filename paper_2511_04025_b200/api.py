@@ -462,6 +462,8 @@ class SolveStats:
     gmg_levels: int = 0
     precond_fallback: int = 0  # 1: block-Jacobi redo, 2: FP64-operator redo (shellular_cuda.h)
     lane: int = 0              # batch lane (homogenize_batch(lanes=...))
+    n_components: int = 0      # mechanically connected element components (fem.hpp:288-317)
+    n_floating: int = 0        # ... without an element at torus node 0 (expect_singular)
 
     @classmethod
     def from_abi(cls, s: L.shl_stats) -> "SolveStats":
@@ -470,7 +472,7 @@ class SolveStats:
                    s.n_elements, s.n_nodes, s.n_tiles, s.norm, s.volume_ratio,
                    bool(s.full_fallback), s.apply_ms, s.update_ms, s.apply_launches,
                    s.kernel_launches, s.h2d_bytes, s.d2h_bytes, s.gmg_levels, s.precond_fallback,
-                   s.lane)
+                   s.lane, s.n_components, s.n_floating)
 
 
 class GridSolver:

@@ -99,7 +99,9 @@ struct Misc {
   int n_bricks;  // active level-0 bricks (brick numbering)
   int node0_active;
   double beta_sum;
-  double pad[4];
+  int n_components;  // mechanical components of the element set (fem.hpp:288-317)
+  int n_floating;    // ... without an element at torus node 0
+  double pad[3];
 };
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -132,6 +134,8 @@ struct shl_ctx {
   // activity / index, active brick table
   DevBuf bflag, boff, bact, bidx, bcoord, bstart;
   int n_bricks = 0;
+  DevBuf cc_parent, cc_corner;  // union-find workspaces (launch_components)
+  int n_components = 0, n_floating = 0;
   shl::BrickView brick_view() const {
     shl::BrickView v;
     const shl::BrickDims d = shl::brick_dims(r);
@@ -160,7 +164,7 @@ struct shl_ctx {
   int* hlevels = nullptr;  // pinned: per multigrid level (last scan offset, last flag)
   shl::PcgState* hstate = nullptr;
   double* hC = nullptr;
-  cudaEvent_t ev[12] = {};
+  cudaEvent_t ev[12] = {};  // 0 field | 1 mesh select | 7 topology | 2 solve: 3 AS | 8 RHS | 9 AS | 4 | 5 C | 6
   void* nccl = nullptr;  // z-slab communicator (slab.cu), created on demand
   void (*nccl_deleter)(void*) = nullptr;
   std::vector<cudaEvent_t> prof_ev;

@@ -62,6 +62,12 @@ void launch_scatter_compact(const int* flag, const int* offset, int n, int* map_
                             int* list, cudaStream_t s);
 void launch_fill_int(int* p, int v, size_t n, cudaStream_t s);
 size_t scan_temp_bytes(int n);
+// Connected components of the active elements under the reference's coupling
+// (shared torus node, fem.hpp:288-317): *n_comp += components, *n_float +=
+// components without an element at torus node 0 (floating: rigid null modes).
+// parent / corner: r^3 int workspaces.
+void launch_components(const int* elem_flag, int r, int* parent, int* corner, int* n_comp, int* n_float,
+                       cudaStream_t s);
 // brick-major level-0 numbering (8x4x4-node bricks, brick.cu): node_map /
 // node_list in brick order, active brick table (bcoord, bstart[nab+1]) and
 // nab written to *nab_out.  Scan temp must hold scan_temp_bytes(np).

@@ -241,8 +241,17 @@ void run_mesh(shl_ctx* c, const shl_shell_params& sp) {
     // keep the final occupancy in occ0
     CK(cudaMemcpyAsync(c->occ0.p, a, n3, cudaMemcpyDeviceToDevice, c->stream));
   }
+  CK(cudaEventRecord(c->ev[7], c->stream));  // t_mesh | t_PBC boundary (voxel.hpp t_select / t_topology)
+  c->cc_parent.ensure(n3 * sizeof(int));
+  c->cc_corner.ensure(n3 * sizeof(int));
+  CK(cudaMemsetAsync(&dm->n_components, 0, sizeof(int) * 2, c->stream));
+  shl::launch_components(c->elem_flag.as<int>(), r, c->cc_parent.as<int>(), c->cc_corner.as<int>(),
+                         &dm->n_components, &dm->n_floating, c->stream);
+  c->launches += 4;
   build_topology(c);
   c->n_surface = c->hmisc->n_surface;
+  c->n_components = c->hmisc->n_components;
+  c->n_floating = c->hmisc->n_floating;
   if (c->n_surface == 0)
     throw ShlError(SHL_DEGENERATE, "field has no zero crossing: no surface to mesh");
   c->full_fallback = c->n_elem == static_cast<int64_t>(n3);
@@ -315,8 +324,10 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   CK(cudaMemsetAsync(x, 0, nX * sizeof(TX), c->stream));
   CK(cudaMemsetAsync(p, 0, 2 * nV * sizeof(TV), c->stream));
   CK(cudaMemsetAsync(z, 0, nV * sizeof(TZ), c->stream));
+  CK(cudaEventRecord(c->ev[8], c->stream));
   shl::launch_setup<TX, TZ>(c->node_list.as<int>(), n, ld, r, c->beta64.as<double>(), ridge, rv,
                             dinv, c->stream);
+  CK(cudaEventRecord(c->ev[9], c->stream));
   Vcycle<TX, TZ, TZ> vc{c, gmg_params()};
   vc.zout = z;
   vc.s = c->stream;
@@ -568,8 +579,11 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   std::memcpy(C_out, c->hC, 36 * sizeof(double));
   c->launches += launches;
   if (st) {
-    st->t_AS = c->ms(3, 4);
-    st->t_RHS = 0.0;
+    // t_RHS: right-hand sides + block-Jacobi inverse (setup kernel); t_AS: the
+    // rest of the setup (element constants, workspaces, multigrid Galerkin
+    // hierarchy) -- the matrix-free solve assembles no global matrix
+    st->t_RHS = c->ms(8, 9);
+    st->t_AS = c->ms(3, 4) - st->t_RHS;
     st->t_solve = c->ms(4, 5);
     st->t_C = c->ms(5, 6);
     for (int s = 0; s < 6; ++s) st->iterations[s] = fin.iters[s];
@@ -647,6 +661,8 @@ void fill_mesh_stats(shl_ctx* c, shl_stats* st) {
   st->n_nodes = c->n_nodes;
   st->n_tiles = 0;
   st->full_fallback = c->full_fallback;
+  st->n_components = c->n_components;
+  st->n_floating = c->n_floating;
   st->norm = c->norm;
   st->volume_ratio = c->volume_ratio;
 }
@@ -706,8 +722,8 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
   c->sync();
   if (st) {
     st->t_field = c->ms(0, 1);
-    st->t_mesh = c->ms(1, 2);
-    st->t_PBC = 0.0;  // node pairing is the ordered compaction inside t_mesh
+    st->t_mesh = c->ms(1, 7);  // classify, dilation, completion, corners, beta
+    st->t_PBC = c->ms(7, 2);   // components + node numbering (the periodic pairing is implicit on the torus)
     st->t_fwd = c->ms(0, 6);
     fill_mesh_stats(c, st);
     st->kernel_launches = c->launches - l0;

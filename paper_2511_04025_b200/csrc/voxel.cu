@@ -252,6 +252,85 @@ __global__ void brick_table_kernel(const int* __restrict__ bact, const int* __re
   }
 }
 
+// ---- mechanical connectivity (fem.hpp:288-317) ---------------------------------
+// Elements are coupled when they share a torus node (the reference's canonical
+// (mod r) node key), i.e. they are 26-neighbours on the periodic element grid.
+// Lock-free union-find on the dense r^3 element grid: parents only ever point
+// to smaller ids (a root is hooked under the smaller root by CAS), so path
+// halving races are benign.
+__device__ __forceinline__ int uf_find(int* p, int x) {
+  int cur = p[x];
+  if (cur == x) return x;
+  int prev = x, next;
+  while (cur > (next = p[cur])) {
+    p[prev] = next;
+    prev = cur;
+    cur = next;
+  }
+  return cur;
+}
+
+__device__ __forceinline__ void uf_union(int* p, int a, int b) {
+  for (;;) {
+    a = uf_find(p, a);
+    b = uf_find(p, b);
+    if (a == b) return;
+    if (a < b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    if (atomicCAS(&p[a], a, b) == a) return;  // a still a root: hooked under b
+  }
+}
+
+__global__ void cc_init_kernel(const int* __restrict__ ef, int n3, int* __restrict__ parent, int* __restrict__ corner) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n3) return;
+  parent[e] = ef[e] ? e : -1;
+  corner[e] = 0;
+}
+
+__global__ void cc_union_kernel(const int* __restrict__ ef, int r, int* __restrict__ parent) {
+  const int n3 = r * r * r;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n3 || !ef[e]) return;
+  const int i = e % r, j = (e / r) % r, k = e / (r * r);
+  // the 13 "forward" neighbours of the 26 (each pair is united once)
+  for (int d = 14; d < 27; ++d) {
+    const int di = d % 3 - 1, dj = (d / 3) % 3 - 1, dk = d / 9 - 1;
+    const int f = (wrapi(k + dk, r) * r + wrapi(j + dj, r)) * r + wrapi(i + di, r);
+    if (f != e && ef[f]) uf_union(parent, e, f);
+  }
+}
+
+// every element's root; roots of components holding an element at torus node 0
+__global__ void cc_mark_kernel(const int* __restrict__ ef, int r, int* __restrict__ parent, int* __restrict__ corner) {
+  const int n3 = r * r * r;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n3 || !ef[e]) return;
+  const int root = uf_find(parent, e);
+  const int i = e % r, j = (e / r) % r, k = e / (r * r);
+  const bool at0 = (i == 0 || i == r - 1) && (j == 0 || j == r - 1) && (k == 0 || k == r - 1);
+  if (at0) corner[root] = 1;
+}
+
+__global__ void cc_count_kernel(const int* __restrict__ parent, const int* __restrict__ corner, int n3,
+                                int* __restrict__ n_comp, int* __restrict__ n_float) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  int c = 0, f = 0;
+  if (e < n3 && parent[e] == e) {
+    c = 1;
+    f = corner[e] == 0;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  f = __reduce_add_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && c) {
+    atomicAdd(n_comp, c);
+    if (f) atomicAdd(n_float, f);
+  }
+}
+
 __global__ void fill_int_kernel(int* p, int v, size_t n) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   if (i < n) p[i] = v;
@@ -335,6 +414,15 @@ void launch_brick_numbering(const int* node_flag, int r, int* bflag, int* boff, 
   brick_active_kernel<<<blocks(d.nb, 256), 256, 0, s>>>(bflag, boff, d.nb, bact);
   cub::DeviceScan::ExclusiveSum(temp, temp_bytes, bact, bidx, d.nb, s);
   brick_table_kernel<<<blocks(d.nb, 256), 256, 0, s>>>(bact, bidx, boff, bflag, d.nb, bcoord, bstart, nab_out);
+}
+
+void launch_components(const int* elem_flag, int r, int* parent, int* corner, int* n_comp, int* n_float,
+                       cudaStream_t s) {
+  const int n3 = r * r * r;
+  cc_init_kernel<<<blocks(n3, 256), 256, 0, s>>>(elem_flag, n3, parent, corner);
+  cc_union_kernel<<<blocks(n3, 256), 256, 0, s>>>(elem_flag, r, parent);
+  cc_mark_kernel<<<blocks(n3, 256), 256, 0, s>>>(elem_flag, r, parent, corner);
+  cc_count_kernel<<<blocks(n3, 256), 256, 0, s>>>(parent, corner, n3, n_comp, n_float);
 }
 
 size_t scan_temp_bytes(int n) {

@@ -591,6 +591,38 @@ DEVICE_CASE(homogenize_composition, "homogenize composes the stages and reports 
   CHECK_THROWS_AS(homogenize(seeded_design(5), ShellParams{}, BaseMaterial{}, 3), ValidationError);
 }
 
+DEVICE_CASE(reduced_mesh_topology, "reduced mesh topology matches the reference's build_topology") {
+  // node / periodic-group counts of the reference's own build_topology
+  // (voxel.hpp:147-228) for these designs: tests/golden/reference_fixtures.npz
+  // ("<name>/r<r>/info", written from oracle/_ref by make_golden.py)
+  struct Want {
+    std::uint64_t seed;
+    int r;
+    size_t nodes, groups;
+  };
+  for (const Want& w : {Want{3, 16, 3862, 544}, Want{12, 16, 3640, 416}}) {
+    VoxelMesh m = build_reduced_mesh(sample_grid(seeded_design(w.seed), w.r), ShellParams{});
+    CHECK(m.num_nodes() == w.nodes);
+    CHECK(m.periodic_groups.size() == w.groups);
+    CHECK(m.corner_group == 0 && m.periodic_groups[0].slaves.size() == 7);
+    CHECK(m.element_nodes.size() == 8 * m.num_elements());
+    for (size_t e = 0; e < m.num_elements(); ++e) {
+      const Vec3i c = VoxelMesh::element_coords(m.elements[e], w.r);
+      CHECK(m.node_coords[m.element_nodes[e * 8]] == c);
+      CHECK(m.node_coords[m.element_nodes[e * 8 + 6]] == Vec3i(c[0] + 1, c[1] + 1, c[2] + 1));
+    }
+  }
+  // the drop-in homogenize fills the grid and mesh like the reference (pipeline.hpp:70,74)
+  HomogenizationResult res = homogenize(seeded_design(3), ShellParams{}, BaseMaterial{}, 16);
+  CHECK(res.grid.samples.size() == size_t(16 * 16 * 16) && res.mesh.num_nodes() == 3862);
+  CHECK(res.mesh.element_fraction() == res.element_fraction);
+  // GridCG on a reduced mesh: the reference's SolverError (pipeline.hpp:86-88)
+  HomogenizeOptions o;
+  o.solver = SolverKind::GridCG;
+  CHECK_THROWS_AS(homogenize(seeded_design(3), ShellParams{}, BaseMaterial{}, 16, o), SolverError);
+  CHECK(res.stats.n_components >= 1 && res.stats.n_floating >= 0);
+}
+
 DEVICE_CASE(orthotropic, "plane design homogenizes to an orthotropic tensor") {
   DesignParams p = plane_design(2, 0.0);
   ShellParams sp;

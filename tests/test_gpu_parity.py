@@ -427,3 +427,20 @@ def test_bench_config_chom_vs_oracle(S, lanes):
         assert stats[i].n_nodes == gold["n_nodes"][i]
         assert stats[i].gmg_levels > 0
         assert err < 1e-4, (s, err)
+
+
+@pytest.mark.parametrize("seed,r", [(3, 16), (12, 16), (21, 16), (1, 32), (5, 32)])
+def test_floating_components_vs_reference_criterion(S, O, seed, r):
+    """shl_stats.n_components / n_floating: the union-find connectivity scan of
+    build_periodic_system (fem.hpp:288-317: elements sharing a torus node are
+    coupled; a component with no element at torus node 0 floats), on the
+    device, against the oracle's restatement (oracle/direct.py)."""
+    from oracle import direct as D
+    sd, od = pair(S, O, "cubic_octant", seed, 4)
+    res = S.homogenize(sd, S.ShellParams(), S.BaseMaterial(), r,
+                       S.HomogenizeOptions(residual_tol=1e-5, precision="mixed"))
+    om = O.build_reduced_mesh(O.sample_grid(od, r))
+    mesh = D.build_topology(r, om.elements, om.beta.reshape(-1)[om.elements])
+    sys_ = D.build_periodic_system(mesh, O.element_stiffness(1.0, 0.3, 1.0 / r))
+    assert res.stats.n_components == sys_.n_components
+    assert (res.stats.n_floating > 0) == sys_.expect_singular
