@@ -60,8 +60,7 @@ struct DevBuf {
   }
   void ensure(size_t bytes) {
     if (bytes <= cap) return;
-    static const bool sync_alloc = std::getenv("SHL_SYNC_ALLOC") != nullptr;  // A/B
-    const cudaStream_t as = sync_alloc ? nullptr : g_alloc_stream;
+    const cudaStream_t as = g_alloc_stream;
     if (p) {
       if (as)
         CK(cudaFreeAsync(p, as));

@@ -32,32 +32,6 @@ __host__ __device__ inline unsigned node_case_blocks(int n, int threads_per_bloc
 }
 
 
-// ---------------------------------------------------------------- gathers
-template <typename TV>
-__device__ __forceinline__ void stencil_gather(GatherAcc<TV>& acc, int idx, int g,
-                                               const TV* __restrict__ xv,
-                                               const TV* __restrict__ stencil,
-                                               const int* __restrict__ nmap, int r, int zero_slot) {
-  acc.zero();
-  if (g == 0) return;
-  const int rr = r * r;
-  const int i = g % r, j = (g / r) % r, k = g / rr;
-  const int xs[3] = {i == 0 ? r - 1 : i - 1, i, i == r - 1 ? 0 : i + 1};
-  const int ys[3] = {(j == 0 ? r - 1 : j - 1) * r, j * r, (j == r - 1 ? 0 : j + 1) * r};
-  const int zs[3] = {(k == 0 ? r - 1 : k - 1) * rr, k * rr, (k == r - 1 ? 0 : k + 1) * rr};
-  const TV* sb = stencil + vbase(idx, kStencil);
-#pragma unroll
-  for (int m = 0; m < 27; ++m) {
-    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-    int nb = (m == 13) ? idx : nmap[zs[dz + 1] + ys[dy + 1] + xs[dx + 1]];
-    nb = nb < 0 ? zero_slot : nb;
-    TV S[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) S[q] = sb[(m * 9 + q) * 32];
-    acc.add(S, xv + vbase(nb, 18));
-  }
-}
-
 template <typename TV>
 struct LevelArgs {
   const int* node_list;
@@ -70,71 +44,6 @@ struct LevelArgs {
   int zbase;          // level 0 of a z-slab (0 otherwise)
   double* totals;     // mode 2: write the r.z sums here instead of finalizing (slabs)
 };
-
-// mode: 0 smooth   xout = xin + w Dinv (b - A xin)
-//       1 residual xout = b - A xin
-//       2 smooth + partial b.xout (the V-cycle output z = M r, gamma = r.z)
-template <typename TB, typename TV, bool kFine>
-__global__ void __launch_bounds__(256, 3)
-    level_sweep_kernel(const LevelArgs<TV> L, const TB* __restrict__ b, const TV* __restrict__ xin,
-                       TV* __restrict__ xout, TV omega, int mode, PcgState* st,
-                       double* partials, int init) {
-  __shared__ double scratch[32 * 6];
-  if (st->stop) return;
-  double gam[6] = {0, 0, 0, 0, 0, 0};
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < L.n; idx += gridDim.x * blockDim.x) {
-    const int g = L.node_list[idx];
-    GatherAcc<TV> acc;
-    if (kFine)
-      fine_gather<TV>(acc, idx, g, xin, L.beta, L.node_map, L.r, 0, L.zero_slot);
-    else
-      stencil_gather<TV>(acc, idx, g, xin, L.stencil, L.node_map, L.r, L.zero_slot);
-    const size_t ob = vbase(idx, 18);
-    TV D[6];
-#pragma unroll
-    for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      TV res[3], xo[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const size_t o = ob + (c * 6 + s) * 32;
-        const TV xi = xin[o];
-        TV w = acc.get(c * 6 + s);
-        if (kFine && g != 0) w = fma_t(L.ridge, xi, w);
-        res[c] = static_cast<TV>(b[o]) - w;
-        xo[c] = xi;
-      }
-      if (mode == 1) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s) * 32] = g == 0 ? TV(0) : res[c];
-        continue;
-      }
-      const TV z0 = D[0] * res[0] + D[1] * res[1] + D[2] * res[2];
-      const TV z1 = D[1] * res[0] + D[3] * res[1] + D[4] * res[2];
-      const TV z2 = D[2] * res[0] + D[4] * res[1] + D[5] * res[2];
-      xo[0] = fma_t(omega, z0, xo[0]);
-      xo[1] = fma_t(omega, z1, xo[1]);
-      xo[2] = fma_t(omega, z2, xo[2]);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        xout[ob + (c * 6 + s) * 32] = xo[c];
-        if (mode == 2) gam[s] += static_cast<double>(b[ob + (c * 6 + s) * 32]) * static_cast<double>(xo[c]);
-      }
-    }
-  }
-  if (mode != 2) return;
-  block_sum<6>(gam, scratch);
-  if (publish_partial<6>(gam, partials, &st->counter_misc)) {
-    double tot[6];
-    __syncthreads();
-    reduce_partials<6>(partials, tot, scratch);
-    if (threadIdx.x == 0) {
-      finalize_gamma_state(st, tot, init);
-      st->counter_misc = 0;
-    }
-  }
-}
 
 // stencil_gather restricted to neighbour plane dz = PLANE-1.
 template <typename TV, int PLANE>
@@ -520,94 +429,6 @@ __global__ void coarse_flag_kernel(const int* __restrict__ map_f, int r_f, int r
   flag_c[G] = on;
 }
 
-// S_{n,m} of level 0 (the masked element sum; pinned node 0 has no row/column)
-template <typename TV>
-__device__ __forceinline__ void fine_block(const TV* __restrict__ betav, int r, int fi, int fj,
-                                           int fk, int dx, int dy, int dz, TV ridge, TV (&S)[9]) {
-#pragma unroll
-  for (int q = 0; q < 9; ++q) S[q] = TV(0);
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
-    const int bx = ox + dx, by = oy + dy, bz = oz + dz;
-    if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
-    const int ei = (fi - ox + r) % r, ej = (fj - oy + r) % r, ek = (fk - oz + r) % r;
-    const TV be = betav[(static_cast<size_t>(ek) * r + ej) * r + ei];
-    if (be == TV(0)) continue;
-    const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int d = 0; d < 3; ++d) S[c * 3 + d] = fma_t(be, k0<TV>((3 * a + c) * 24 + 3 * b + d), S[c * 3 + d]);
-  }
-  if (dx == 0 && dy == 0 && dz == 0) {
-    S[0] += ridge;
-    S[4] += ridge;
-    S[8] += ridge;
-  }
-}
-
-// A_c(N, N+D) = sum_{n in supp N} sum_{m ~ n, m in supp(N+D)} w(n,N) A_f(n,m) w(m,N+D)
-// One thread per active coarse node; 243 accumulators in shared memory.
-template <typename TV, bool kFine>
-__global__ void __launch_bounds__(64) galerkin_kernel(const int* __restrict__ list_c, int n_c,
-                                                      int r_c, const int* __restrict__ map_f,
-                                                      int r_f, const TV* __restrict__ betav,
-                                                      const TV* __restrict__ stencil_f, TV ridge,
-                                                      TV* __restrict__ stencil_c) {
-  extern __shared__ __align__(16) unsigned char gsm[];
-  TV* acc = reinterpret_cast<TV*>(gsm) + threadIdx.x * kStencil;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n_c) return;
-  for (int q = 0; q < kStencil; ++q) acc[q] = TV(0);
-  const int G = list_c[idx];
-  const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
-  if (G != 0) {
-    for (int nk = -1; nk <= 1; ++nk)
-      for (int nj = -1; nj <= 1; ++nj)
-        for (int ni = -1; ni <= 1; ++ni) {
-          // fine node n (unwrapped 2N + d) and its weight for N
-          const int ux = 2 * I + ni, uy = 2 * J + nj, uz = 2 * K + nk;
-          const int fi = (ux + r_f) % r_f, fj = (uy + r_f) % r_f, fk = (uz + r_f) % r_f;
-          const size_t gn = (static_cast<size_t>(fk) * r_f + fj) * r_f + fi;
-          const int nf = map_f[gn];
-          if (nf < 0 || gn == 0) continue;
-          const TV wn = TV((ni ? 0.5 : 1.0) * (nj ? 0.5 : 1.0) * (nk ? 0.5 : 1.0));
-          for (int m = 0; m < 27; ++m) {
-            const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-            const int vx = ux + dx, vy = uy + dy, vz = uz + dz;  // fine m, unwrapped
-            const int mi = (vx + r_f) % r_f, mj = (vy + r_f) % r_f, mk = (vz + r_f) % r_f;
-            const size_t gm = (static_cast<size_t>(mk) * r_f + mj) * r_f + mi;
-            if (gm == 0 || map_f[gm] < 0) continue;
-            TV S[9];
-            if (kFine) {
-              fine_block<TV>(betav, r_f, fi, fj, fk, dx, dy, dz, ridge, S);
-            } else {
-              const TV* sb = stencil_f + vbase(nf, kStencil);
-#pragma unroll
-              for (int q = 0; q < 9; ++q) S[q] = sb[(m * 9 + q) * 32];
-            }
-            // coarse parents of m (unwrapped): even -> v/2, odd -> (v-1)/2, (v+1)/2
-            const int ax0 = (vx - (vx & 1)) / 2, ay0 = (vy - (vy & 1)) / 2, az0 = (vz - (vz & 1)) / 2;
-            const int nx = (vx & 1) ? 2 : 1, ny = (vy & 1) ? 2 : 1, nz = (vz & 1) ? 2 : 1;
-            const TV wm = TV(1.0 / (nx * ny * nz));
-            for (int c = 0; c < nz; ++c)
-              for (int b = 0; b < ny; ++b)
-                for (int a = 0; a < nx; ++a) {
-                  // vx in [2I-2, 2I+2] so the parent offset lies in [-1, 1]
-                  const int Dx = ax0 + a - I, Dy = ay0 + b - J, Dz = az0 + c - K;
-                  const int slot = ((Dz + 1) * 3 + (Dy + 1)) * 3 + (Dx + 1);
-                  const TV w = wn * wm;
-#pragma unroll
-                  for (int q = 0; q < 9; ++q) acc[slot * 9 + q] = fma_t(w, S[q], acc[slot * 9 + q]);
-                }
-          }
-        }
-  }
-  TV* out = stencil_c + vbase(idx, kStencil);
-  for (int q = 0; q < kStencil; ++q) out[q * 32] = acc[q];
-}
-
 // ---- level-1 Galerkin from elements -------------------------------------
 // Inside one coarse cell the trilinear P maps the cell's 8 coarse corners onto
 // the 27 fine nodes of its 8 fine elements, so P^T A_f P restricted to the cell
@@ -818,139 +639,6 @@ __global__ void coarse_dinv_kernel(const int* __restrict__ list_c, int n_c,
   for (int q = 0; q < 6; ++q) dinv[vbase(idx, 6) + q * 32] = static_cast<TV>(inv[q]);
 }
 
-// ---- coarsest level: every Jacobi sweep in one cluster launch ---------------
-// The coarsest grid (8^3 torus, <= 512 active nodes) used to take one kernel
-// per damped Jacobi sweep, each a few microseconds of dependent L2 loads plus a
-// launch.  Here a cluster of kCoarseCluster CTAs owns it: CTA k holds the
-// stencils, right-hand side, Dinv, neighbour ids and x (ping-pong) of nodes
-// [k*per, (k+1)*per) in shared memory.  A sweep gathers neighbour values
-// straight from the owning CTA's shared memory (distributed shared memory
-// loads; thread = node x load case x stencil plane, planes summed in fixed
-// order), writes the owned nodes' new values locally, and ends with one
-// cluster barrier.  Same arithmetic as jacobi_first + (sweeps-1)
-// coarse_warp_sweep launches.
-constexpr int kCoarseCluster = 16;
-
-template <typename TV>
-__global__ void __cluster_dims__(kCoarseCluster, 1, 1) __launch_bounds__(576)
-    coarsest_cluster_kernel(const LevelArgs<TV> L, const TV* __restrict__ b, TV* __restrict__ xout, TV omega,
-                            int sweeps, const PcgState* st) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  if (st->stop) return;  // the same value in every CTA of the cluster
-  const int n = L.n;
-  const int per = (n + kCoarseCluster - 1) / kCoarseCluster;  // <= 32
-  const int rank = static_cast<int>(cl.block_rank());
-  const int n0 = rank * per;
-  const int nown = max(0, min(n, n0 + per) - n0);
-  extern __shared__ __align__(16) unsigned char csm[];
-  TV* xs = reinterpret_cast<TV*>(csm);                  // [2][per][18] owned x, ping-pong
-  TV* sten = xs + 2 * per * 18;                         // [per][243]
-  TV* bo = sten + static_cast<size_t>(per) * kStencil;  // [per][18]
-  TV* dv = bo + per * 18;                               // [per][6]
-  TV* part = dv + per * 6;                              // [3][per][18]
-  int* nbr = reinterpret_cast<int*>(part + 3 * per * 18);  // [per][27] owner-local slot, -1 = absent
-  int* gid = nbr + per * 27;                                 // [per]
-  const int tid = threadIdx.x;
-  for (int t = tid; t < nown * kStencil; t += blockDim.x) {
-    const int li = t / kStencil, q = t % kStencil;
-    sten[li * kStencil + q] = L.stencil[vbase(n0 + li, kStencil) + q * 32];
-  }
-  for (int t = tid; t < nown * 18; t += blockDim.x) {
-    const int li = t / 18, q = t % 18;
-    bo[t] = b[vbase(n0 + li, 18) + q * 32];
-  }
-  for (int t = tid; t < nown * 6; t += blockDim.x) {
-    const int li = t / 6, q = t % 6;
-    dv[t] = L.dinv[vbase(n0 + li, 6) + q * 32];
-  }
-  const int r = L.r, rr = r * r;
-  for (int t = tid; t < nown * 27; t += blockDim.x) {
-    const int li = t / 27, m = t % 27;
-    const int g = L.node_list[n0 + li];
-    if (m == 0) gid[li] = g;
-    const int i = g % r, j = (g / r) % r, k = g / rr;
-    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-    const int xi = (i + dx + r) % r, yj = (j + dy + r) % r, zk = (k + dz + r) % r;
-    nbr[t] = (m == 13) ? n0 + li : L.node_map[(zk * r + yj) * r + xi];
-  }
-  __syncthreads();
-  const int p = tid / 192, rem = tid % 192, li = rem / 6, s_ = rem % 6;
-  const bool owner = li < nown;
-  // x0 = omega Dinv b (jacobi_first)
-  if (p == 0 && owner) {
-    const TV* D = dv + li * 6;
-    const TV r0 = bo[li * 18 + s_], r1 = bo[li * 18 + 6 + s_], r2 = bo[li * 18 + 12 + s_];
-    xs[li * 18 + s_] = omega * (D[0] * r0 + D[1] * r1 + D[2] * r2);
-    xs[li * 18 + 6 + s_] = omega * (D[1] * r0 + D[3] * r1 + D[4] * r2);
-    xs[li * 18 + 12 + s_] = omega * (D[2] * r0 + D[4] * r1 + D[5] * r2);
-  }
-  cl.sync();
-  int cur = 0;
-  for (int k = 1; k < sweeps; ++k) {
-    if (owner) {
-      TV y[3] = {TV(0), TV(0), TV(0)};
-      if (gid[li] != 0) {
-        // gather the plane's neighbour values first (independent DSMEM loads)
-        TV xv[9][3];
-#pragma unroll
-        for (int mm = 0; mm < 9; ++mm) {
-          const int jn = nbr[li * 27 + p * 9 + mm];
-          if (jn < 0) {
-            xv[mm][0] = xv[mm][1] = xv[mm][2] = TV(0);
-            continue;
-          }
-          const TV* src = cl.map_shared_rank(xs, jn / per) + (cur * per + jn % per) * 18 + s_;
-          xv[mm][0] = src[0];
-          xv[mm][1] = src[6];
-          xv[mm][2] = src[12];
-        }
-#pragma unroll
-        for (int mm = 0; mm < 9; ++mm) {
-          const TV* S = sten + li * kStencil + (p * 9 + mm) * 9;
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            y[c] = fma_t(S[c * 3 + 0], xv[mm][0], fma_t(S[c * 3 + 1], xv[mm][1], fma_t(S[c * 3 + 2], xv[mm][2], y[c])));
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) part[(p * per + li) * 18 + c * 6 + s_] = y[c];
-    }
-    __syncthreads();
-    if (p == 0 && owner) {
-      const TV* xo = xs + (cur * per + li) * 18 + s_;
-      TV* xn = xs + ((cur ^ 1) * per + li) * 18 + s_;
-      if (gid[li] == 0) {
-        xn[0] = xn[6] = xn[12] = TV(0);
-      } else {
-        TV res[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int q = c * 6 + s_;
-          const TV yy = part[(0 * per + li) * 18 + q] + part[(1 * per + li) * 18 + q] + part[(2 * per + li) * 18 + q];
-          res[c] = bo[li * 18 + q] - yy;
-        }
-        const TV* D = dv + li * 6;
-        xn[0] = fma_t(omega, D[0] * res[0] + D[1] * res[1] + D[2] * res[2], xo[0]);
-        xn[6] = fma_t(omega, D[1] * res[0] + D[3] * res[1] + D[4] * res[2], xo[6]);
-        xn[12] = fma_t(omega, D[2] * res[0] + D[4] * res[1] + D[5] * res[2], xo[12]);
-      }
-    }
-    cl.sync();  // new values visible cluster-wide; nobody still reads the old buffer
-    cur ^= 1;
-  }
-  if (p == 0 && owner) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) xout[vbase(n0 + li, 18) + (c * 6 + s_) * 32] = xs[(cur * per + li) * 18 + c * 6 + s_];
-  }
-}
-
-template <typename TV>
-size_t coarsest_smem_bytes(int n) {
-  const int per = (n + kCoarseCluster - 1) / kCoarseCluster;
-  return sizeof(TV) * static_cast<size_t>(per) * (36 + kStencil + 18 + 6 + 54) + sizeof(int) * static_cast<size_t>(per) * 28;
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -963,23 +651,13 @@ template <typename TV>
 void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int r_f,
                      const TV* beta_f, const TV* stencil_f, TV ridge, TV* stencil_c, cudaStream_t s) {
   if (n_c == 0) return;
-  const size_t smem = 64 * kStencil * sizeof(TV);
-  static const bool nodewise = std::getenv("SHL_GALERKIN_NODEWISE") != nullptr;  // A/B check
-  if (stencil_f == nullptr && !nodewise) {
+  if (stencil_f == nullptr) {
     galerkin_fine_kernel<TV><<<(n_c + 31) / 32, dim3(32, 27), 0, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f, ridge,
                                                                       stencil_c);
-  } else if (!nodewise) {
+  } else {
     const long long threads = static_cast<long long>(n_c) * 27 * 32;
     galerkin_stored_kernel<TV><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(list_c, n_c, r_c, map_f,
                                                                                             r_f, stencil_f, stencil_c);
-  } else if (stencil_f == nullptr) {
-    cudaFuncSetAttribute(galerkin_kernel<TV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    galerkin_kernel<TV, true><<<(n_c + 63) / 64, 64, smem, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f,
-                                                                nullptr, ridge, stencil_c);
-  } else {
-    cudaFuncSetAttribute(galerkin_kernel<TV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    galerkin_kernel<TV, false><<<(n_c + 63) / 64, 64, smem, s>>>(list_c, n_c, r_c, map_f, r_f, nullptr,
-                                                                 stencil_f, ridge, stencil_c);
   }
 }
 
@@ -997,10 +675,7 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
     return;
   }
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
-  static const bool one = std::getenv("SHL_APPLY1") != nullptr;  // A/B: thread-per-node kernels
-  if (fine && one) {
-    level_sweep_kernel<TB, TV, true><<<grid, 256, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
-  } else if (fine) {
+  if (fine) {
     level_sweep3_kernel<TB, TV, true><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
   } else if (L.n > 32768) {  // large stored level: thread per node is throughput-bound
     level_sweep3_kernel<TB, TV, false><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
@@ -1008,28 +683,6 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
     coarse_warp_sweep_kernel<TV><<<(L.n + 7) / 8, 256, 0, s>>>(a, reinterpret_cast<const TV*>(b), xin, xout,
                                                                omega, mode, st);
   }
-}
-
-// false when the level does not fit the cluster kernel (caller keeps per-sweep launches)
-template <typename TV>
-bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xout, TV omega, int sweeps, const PcgState* st,
-                     cudaStream_t s) {
-  // Opt-in (SHL_COARSE_CLUSTER=1): 45 us vs ~100 us of per-sweep launches at
-  // 128^3 alone, but a 16-CTA cluster must find 16 free SMs in one GPC, which
-  // stalls it behind other batch lanes' kernels (3 lanes: 28 vs 34 designs/s).
-  static const bool off = std::getenv("SHL_COARSE_CLUSTER") == nullptr;
-  const int per = (L.n + kCoarseCluster - 1) / kCoarseCluster;
-  const size_t smem = coarsest_smem_bytes<TV>(L.n);
-  if (off || L.n == 0 || per > 32 || smem > 227 * 1024) return false;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(coarsest_cluster_kernel<TV>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(coarsest_cluster_kernel<TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    configured = true;
-  }
-  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
-  coarsest_cluster_kernel<TV><<<kCoarseCluster, 576, smem, s>>>(a, b, xout, omega, sweeps, st);
-  return true;
 }
 
 template <typename TB, typename TV, typename TO>
@@ -1088,10 +741,6 @@ template void launch_level_sweep<float, float>(const GmgLevelView<float>&, bool,
 template void launch_level_sweep<double, double>(const GmgLevelView<double>&, bool, const double*,
                                                  const double*, double*, double, int, PcgState*, double*,
                                                  int, int, cudaStream_t);
-template bool launch_coarsest<float>(const GmgLevelView<float>&, const float*, float*, float, int, const PcgState*,
-                                     cudaStream_t);
-template bool launch_coarsest<double>(const GmgLevelView<double>&, const double*, double*, double, int,
-                                      const PcgState*, cudaStream_t);
 template void launch_level_sweep_out<double, float, double>(const GmgLevelView<float>&, const double*,
                                                            const float*, double*, float, PcgState*, double*,
                                                            int, int, cudaStream_t);

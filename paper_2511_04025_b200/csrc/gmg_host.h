@@ -29,18 +29,7 @@ struct GmgParams {
   int nu_at(int l) const { return (l == 0 && nu0 > 0) ? nu0 : nu; }
 };
 
-inline GmgParams gmg_params() {
-  GmgParams g;
-  if (const char* e = std::getenv("SHL_GMG_NU")) g.nu = std::max(1, std::atoi(e));
-  if (const char* e = std::getenv("SHL_GMG_OMEGA")) g.omega = std::atof(e);
-  if (const char* e = std::getenv("SHL_GMG_MIN_R")) g.min_r = std::max(4, std::atoi(e));
-  if (const char* e = std::getenv("SHL_GMG_COARSE")) g.coarse_sweeps = std::max(1, std::atoi(e));
-  if (const char* e = std::getenv("SHL_GMG_LEVELS")) g.max_levels = std::atoi(e);
-  if (const char* e = std::getenv("SHL_GMG_OMEGA_C")) g.omega_c = std::atof(e);
-  if (const char* e = std::getenv("SHL_GMG_L1")) g.l1 = std::atoi(e);
-  if (const char* e = std::getenv("SHL_GMG_NU0")) g.nu0 = std::max(1, std::atoi(e));
-  return g;
-}
+inline GmgParams gmg_params() { return GmgParams{}; }
 
 // Coarse levels 1..L: active set, ordered ids, Galerkin stencils, Dinv.
 // Two passes so the host waits once, not once per level: the active sets and
@@ -137,10 +126,6 @@ struct Vcycle {
                                         s);
       ++launches;
     };
-    if (l == L && !fine && shl::launch_coarsest<TV>(V, b[l], cur, w, gp.coarse_sweeps, st, s)) {
-      ++launches;  // the whole coarsest solve in one cluster launch
-      return cur;
-    }
     if (!fine) {
       shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, s);
       ++launches;

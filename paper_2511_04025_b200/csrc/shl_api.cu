@@ -313,12 +313,11 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   // still FP32-resolution-small: C^H moves by < 1e-7 relative (tests compare
   // against FP64).  Every K0 diagonal entry is equal, so
   // mean diag = K0[0] * (8 sum beta) / n_nodes.
-  static const char* ridge_env = std::getenv("SHL_RIDGE_REL");  // dev aid
   // the operator PCG solves uses the Krylov type's ridge; the preconditioner
   // (block Jacobi / V-cycle) the ridge of its own storage type
   const double diag_mean = n > 0 ? std::fabs(K0[0]) * 8.0 * c->beta_sum / double(n) : 0.0;
-  const double ridge_op = diag_mean * (ridge_env ? std::atof(ridge_env) : (sizeof(TV) == 8 ? 1e-11 : 1e-8));
-  const double ridge = diag_mean * (ridge_env ? std::atof(ridge_env) : (sizeof(TZ) == 8 ? 1e-11 : 1e-8));
+  const double ridge_op = diag_mean * (sizeof(TV) == 8 ? 1e-11 : 1e-8);
+  const double ridge = diag_mean * (sizeof(TZ) == 8 ? 1e-11 : 1e-8);
   CK(cudaEventRecord(c->ev[3], c->stream));
   shl::ElementConstLease const_lease(K0, W, T, r, c->stream);
   CK(cudaMemsetAsync(x, 0, nX * sizeof(TX), c->stream));
@@ -389,23 +388,23 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
   ua.init = 0;
   int64_t launches = 2 + 2;
-  static const int check_env = [] {  // A/B: SHL_CHECK_EVERY
-    const char* e = std::getenv("SHL_CHECK_EVERY");
-    return e ? std::atoi(e) : 0;
-  }();
-  int check = opt.check_every > 0 ? opt.check_every : (check_env > 0 ? check_env : (n < 200000 ? 16 : 32));
-  static const bool trace = std::getenv("SHL_TRACE") != nullptr;  // dev aid: per-iteration scalars
-  if (trace) check = 1;
+  int check = opt.check_every > 0 ? opt.check_every : (n < 200000 ? 16 : 32);
+#ifdef SHL_DEV_TRACE  // dev build only: per-iteration scalars on stderr
+  constexpr bool trace = true;
+  check = 1;
+#else
+  constexpr bool trace = false;
+#endif
   double apply_ms = 0.0, update_ms = 0.0;
   int64_t apply_launches = 0;
   int64_t issued = 0;
   // Steady state: the iteration (update, V-cycle, apply: ~30 launches with
   // multigrid) is captured once into a CUDA graph of kGraphIters iterations
   // and replayed, which removes the per-kernel launch gaps of the small
-  // coarse-level kernels.  Profiling / tracing keep direct launches.
-  static const bool no_graph = std::getenv("SHL_NOGRAPH") != nullptr;  // A/B
+  // coarse-level kernels.  Profiling (shl_set_profiling: per-launch events,
+  // per-kernel ncu launch lists) and tracing keep direct launches.
   constexpr int kGraphIters = 4;
-  const bool use_graph = !c->profiling && !trace && !no_graph && check % kGraphIters == 0;
+  const bool use_graph = !c->profiling && !trace && check % kGraphIters == 0;
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;  // kernel launches per graph replay
   // The whole solve loop as ONE graph launch when the driver supports
@@ -413,7 +412,6 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   // one-thread kernel setting the condition to !stop.  No host polls during the
   // solve (host scheduling delays no longer idle the design's stream) and at
   // most kGraphIters-1 no-op iterations after convergence.
-  static const bool no_while = std::getenv("SHL_NO_WHILE") != nullptr;  // A/B: host-polled replay
   bool use_while = false;
   if (use_graph) {
     // recorded on a side stream: capture + instantiation (host work) overlap the
@@ -421,7 +419,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
     const int64_t before = launches + vc.launches;
     const cudaStream_t cs = c->cap_stream;
     cudaGraph_t graph = nullptr;
-    if (!no_while) {
+    {
       cudaGraph_t g = nullptr;
       CK(cudaGraphCreate(&g, 0));
       cudaGraphConditionalHandle h;
@@ -614,22 +612,11 @@ void solve_dispatch_once(shl_ctx* c, const double* K0, const shl_solve_options& 
       // A p swamps the ridge-sized curvature of a voxel shell's hinge modes
       // (elements sharing only an edge or a corner) and p^T A p loses its sign
       // on ~1 in 16 designs at 128^3; the FP64 operator keeps the reference's
-      // 1e-11 ridge and costs ~3% per design (128^3 sweep).  SHL_MIXED_OP32=1
-      // (A/B) runs the FP32 operator and redoes breakdowns with the FP64 one.
-      static const bool op32 = std::getenv("SHL_MIXED_OP32") != nullptr;
-      if (!gmg) {
+      // 1e-11 ridge and costs ~3% per design (128^3 sweep).
+      if (!gmg)
         run_solve<double, float, float>(c, K0, opt, C_out, st, prec, gmg);
-      } else if (!op32) {
+      else
         run_solve<double, double, float>(c, K0, opt, C_out, st, prec, gmg);
-      } else {
-        try {
-          run_solve<double, float, float>(c, K0, opt, C_out, st, prec, gmg);
-        } catch (const ShlError& e) {
-          if (!is_breakdown(e)) throw;
-          run_solve<double, double, float>(c, K0, opt, C_out, st, prec, gmg);
-          if (st) st->precond_fallback = 2;
-        }
-      }
       break;
     }
     default: run_solve<float, float, float>(c, K0, opt, C_out, st, prec, gmg); break;
@@ -997,23 +984,27 @@ int shl_homogenize_batch(shl_ctx* c, int n, const shl_design* designs, const shl
   // drifted into lockstep contention on about one run in three (one lane's
   // setup kernels queued behind the other's resident solve kernels: 26 vs 35
   // designs/s at 2 lanes); with lane 0 prioritised 2 lanes measure 33.5-34.4
-  // designs/s in every run.  SHL_LANE_PRIO=0 restores equal priorities (A/B).
-  static const bool lane_prio = [] {
-    const char* e = std::getenv("SHL_LANE_PRIO");
-    return !(e && std::atoi(e) == 0);
-  }();
-  if (lane_prio && L > 1 && !c->high_priority) {
-    int least = 0, greatest = 0;
-    cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    cudaSetDevice(c->device);
-    cudaStreamSynchronize(c->stream);
-    cudaStreamSynchronize(c->cap_stream);
-    cudaStreamDestroy(c->stream);
-    cudaStreamDestroy(c->cap_stream);
-    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&c->cap_stream, cudaStreamNonBlocking, greatest) != cudaSuccess)
-      return SHL_CUDA;
-    c->high_priority = true;
+  // designs/s on most runs (not on every box).
+  if (L > 1 && !c->high_priority) {
+    const int rc = shl::host::guarded(c, [&] {
+      int least = 0, greatest = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      // new streams first: on failure the context keeps its working streams
+      cudaStream_t s0 = nullptr, s1 = nullptr;
+      CK(cudaStreamCreateWithPriority(&s0, cudaStreamNonBlocking, greatest));
+      if (cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, greatest) != cudaSuccess) {
+        cudaStreamDestroy(s0);
+        throw ShlError(SHL_CUDA, "cudaStreamCreateWithPriority failed");
+      }
+      CK(cudaStreamSynchronize(c->stream));
+      CK(cudaStreamSynchronize(c->cap_stream));
+      CK(cudaStreamDestroy(c->stream));
+      CK(cudaStreamDestroy(c->cap_stream));
+      c->stream = s0;
+      c->cap_stream = s1;
+      c->high_priority = true;
+    });
+    if (rc != SHL_OK) return rc;
   }
   std::atomic<int> next{0};
   std::atomic<int> device_failed{0};

@@ -21,7 +21,6 @@
 // Scalars never leave the device: the last block of each reduction kernel
 // (fixed-order sum of the per-block partials -> deterministic) updates the
 // PcgState, so the host only polls a flag every few iterations.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <condition_variable>
@@ -344,68 +343,8 @@ __device__ __forceinline__ TV gather3_sum(const TV* part_s, int q, int lane) {
   return part_s[(0 * 18 + q) * 32 + lane] + part_s[(1 * 18 + q) * 32 + lane] + part_s[(2 * 18 + q) * 32 + lane];
 }
 
-template <typename TV>
-__global__ void __launch_bounds__(256, sizeof(TV) == 4 ? 3 : 2) apply_kernel(const ApplyArgs<TV> A) {
-  __shared__ double scratch[32 * 6];
-  PcgState* st = A.state;
-  if (st->stop) return;
-  const TV* __restrict__ zv = A.z;
-  const TV* __restrict__ betav = A.beta;
-  const int* __restrict__ nmap = A.node_map;
-  TV* __restrict__ pv = A.p;
-  TV* __restrict__ qv = A.q;
-  const int r = A.r;
-  const size_t ld = A.ld;
-  TV bcoef[6];
-  bool dn[6];
-#pragma unroll
-  for (int s = 0; s < 6; ++s) {
-    dn[s] = st->done[s] != 0;
-    bcoef[s] = static_cast<TV>(st->beta[s]);
-  }
-  const TV ridge = static_cast<TV>(st->ridge);
-  double dl[6] = {0, 0, 0, 0, 0, 0};
-  (void)ld;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < A.n; idx += gridDim.x * blockDim.x) {
-    const int g = A.node_list[idx];
-    GatherAcc<TV> acc;
-    fine_gather<TV>(acc, idx, g, zv, betav, nmap, r, A.zbase, A.zero_slot);
-    const size_t ob = vbase(idx, 18);
-#pragma unroll
-    for (int q = 0; q < 18; ++q) {
-      const int s = q % 6;
-      const size_t o = ob + q * 32;
-      const TV zq = zv[o];
-      const TV w = g != 0 ? fma_t(ridge, zq, acc.get(q)) : TV(0);
-      TV pn = TV(0), qn = TV(0);
-      if (!dn[s]) {
-        pn = fma_t(bcoef[s], pv[o], zq);
-        qn = fma_t(bcoef[s], qv[o], w);
-      }
-      pv[o] = pn;
-      qv[o] = qn;
-      // p.Ap from the updated p and q (q = A p by recurrence); more robust than
-      // the delta - beta*gamma/alpha recurrence under a strong FP32 preconditioner
-      dl[s] += static_cast<double>(pn) * static_cast<double>(qn);
-    }
-  }
-  block_sum<6>(dl, scratch);
-  if (publish_partial<6>(dl, A.partials, &st->counter_apply)) {
-    double tot[6];
-    __syncthreads();
-    reduce_partials<6>(A.partials, tot, scratch);
-    if (threadIdx.x == 0) {
-      if (A.defer) {
-        for (int s = 0; s < 6; ++s) A.totals[s] = tot[s];
-      } else {
-        finalize_apply_state(st, tot);
-      }
-      st->counter_apply = 0;
-    }
-  }
-}
-
-// Same contract as apply_kernel, latency-split three ways (gather3_tile).
+// w = A z, p = z + beta p, q = w + beta q, p.q (the FP32 operator), latency-split
+// three ways (gather3_tile).
 template <typename TV, typename TZ>
 __global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV, TZ> A) {
   __shared__ __align__(16) TV part_s[2][3 * 18 * 32];
@@ -948,50 +887,20 @@ void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s) {
     launch_brick_apply<TV, TZ>(a, s);
     return;
   }
-  if constexpr (std::is_same<TV, TZ>::value) {
-    static const bool one = std::getenv("SHL_APPLY1") != nullptr;  // thread-per-node variant (A/B checks)
-    if (one) {
-      apply_kernel<TV><<<grid, 256, 0, s>>>(a);
-      return;
-    }
-  }
+  // per-node gather kernels: the z-slab levels (slab-local numbering)
   if constexpr (sizeof(TV) == 8) {
-    static const bool three = std::getenv("SHL_APPLY3") != nullptr;  // A/B: three-warp FP64 variant
-    // SHL_APPLY6 = GM: G six-warp groups per CTA, M CTAs per SM (A/B).  With the
-    // prefetched tile queue 14 (one group: its barriers hold 6 warps, not 12)
-    // measures 305 vs 311 us for 22 at the same 80 registers; 13 / 15 / 16:
-    // 411 / 344 / 376 us (occupancy, or spills under the tighter register caps).
-    static const int variant = [] {
-      const char* e = std::getenv("SHL_APPLY6");
-      return e ? std::atoi(e) : 14;
+    // one six-warp group per CTA, 4 CTAs per SM, one CTA per resident slot
+    // (tiles are dynamic, so the grid-stride loop has no tail wave)
+    static const int nsm = [] {
+      int dev = 0, v = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      return v;
     }();
-    if (!three) {
-      // one CTA per resident slot: the grid-stride loop then has no tail wave
-      static const int nsm = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-      }();
-      if (variant == 22) {
-        static const int per_sm = [] {  // A/B: CTAs per SM of the apply (tiles are dynamic)
-          const char* e = std::getenv("SHL_APPLY_CTAS_PER_SM");
-          return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
-        }();
-        apply6_kernel<TZ, 2, 2><<<std::min(grid, per_sm * nsm), 384, 0, s>>>(a);
-      } else if (variant == 15) {  // partials hold 6 * nsm blocks (shl_api.cu run_solve)
-        apply6_kernel<TZ, 1, 5><<<std::max(1, std::min((a.n + 31) / 32, 5 * nsm)), 192, 0, s>>>(a);
-      } else if (variant == 16) {
-        apply6_kernel<TZ, 1, 6><<<std::max(1, std::min((a.n + 31) / 32, 6 * nsm)), 192, 0, s>>>(a);
-      } else if (variant == 14) {
-        apply6_kernel<TZ, 1, 4><<<std::min(grid, 4 * nsm), 192, 0, s>>>(a);
-      } else {
-        apply6_kernel<TZ, 1, 3><<<std::min(grid, 3 * nsm), 192, 0, s>>>(a);
-      }
-      return;
-    }
+    apply6_kernel<TZ, 1, 4><<<std::min(grid, 4 * nsm), 192, 0, s>>>(a);
+  } else {
+    apply3_kernel<TV, TZ><<<grid, 192, 0, s>>>(a);
   }
-  apply3_kernel<TV, TZ><<<grid, 192, 0, s>>>(a);
 }
 
 int apply_grid(int n, int num_sms) { return std::max(1, std::min((n + 63) / 64, num_sms * 4)); }

@@ -133,11 +133,6 @@ template <typename TB, typename TV>
 void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const TV* xin, TV* xout,
                         TV omega, int mode, PcgState* st, double* partials, int init, int grid,
                         cudaStream_t s);
-// Coarsest level: omega Dinv b followed by sweeps-1 damped Jacobi sweeps in one
-// cluster launch; false if the level does not fit (use per-sweep launches).
-template <typename TV>
-bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* xout, TV omega, int sweeps, const PcgState* st,
-                     cudaStream_t s);
 // Last level-0 sweep of the V-cycle (mode 2) writing z = M r in the Krylov
 // vectors' type TO (FP64 in mixed multigrid, so the apply needs no conversions).
 template <typename TB, typename TV, typename TO>
