@@ -31,6 +31,7 @@
 #ifndef SHELLULAR_CUDA_H
 #define SHELLULAR_CUDA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -210,6 +211,26 @@ int shl_homogenize_zslab(shl_ctx* ctx, const uint8_t* nccl_id, int rank, int nra
                          const shl_design* design, const shl_shell_params* sp,
                          const shl_material* mat, int r, const shl_solve_options* opt,
                          double* C_out, shl_stats* stats);
+
+/* Host-staged transport for the per-rank z-slab solve: the caller's
+ * communicator (e.g. torch.distributed over gloo) moves host buffers; the
+ * library syncs its stream and stages device data through pinned memory
+ * around each call.  Counts are in values (double if f64, else float).
+ * Callbacks return 0 on success. */
+typedef struct {
+  void* user;
+  /* element-wise sum over all ranks, in place */
+  int (*allreduce_sum)(void* user, void* buf, size_t n, int f64);
+  /* periodic ring: send send_hi to rank+1 and send_lo to rank-1; receive
+   * recv_lo from rank-1 and recv_hi from rank+1 */
+  int (*ring_exchange)(void* user, const void* send_hi, size_t n_send_hi, const void* send_lo,
+                       size_t n_send_lo, void* recv_lo, size_t n_recv_lo, void* recv_hi,
+                       size_t n_recv_hi, int f64);
+} shl_slab_transport;
+int shl_homogenize_zslab_host(shl_ctx* ctx, const shl_slab_transport* transport, int rank,
+                              int nranks, const shl_design* design, const shl_shell_params* sp,
+                              const shl_material* mat, int r, const shl_solve_options* opt,
+                              double* C_out, shl_stats* stats);
 
 /* Marching cubes on the resident grid's corner samples: the zero level set
  * with linear edge interpolation, vertices/triangles in exactly the

@@ -51,13 +51,23 @@ class shl_stats(C.Structure):
                 ("n_components", C.c_int32), ("n_floating", C.c_int32)]
 
 
+# shl_slab_transport (host-staged z-slab transport callbacks)
+SLAB_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int)
+SLAB_EXCHANGE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
+                            C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int)
+
+
+class shl_slab_transport(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum", SLAB_ALLREDUCE), ("ring_exchange", SLAB_EXCHANGE)]
+
+
 # every symbol include/shellular_cuda.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "shl_ctx_create", "shl_ctx_destroy", "shl_last_error", "shl_set_profiling",
     "shl_sample_grid", "shl_load_grid", "shl_classify_surface", "shl_build_reduced_mesh",
     "shl_grid_solve", "shl_solve_mesh", "shl_homogenize", "shl_homogenize_batch",
     "shl_element_stiffness", "shl_random_design", "shl_expand_symmetry",
-    "shl_homogenize_slabs", "shl_nccl_unique_id", "shl_homogenize_zslab",
+    "shl_homogenize_slabs", "shl_nccl_unique_id", "shl_homogenize_zslab", "shl_homogenize_zslab_host",
     "shl_extract_isosurface", "shl_voxel_raw", "shl_set_batch_lanes",
 )
 
@@ -105,6 +115,9 @@ def lib() -> C.CDLL:
     L.shl_homogenize_zslab.argtypes = [vp, vp, C.c_int, C.c_int, P(shl_design),
                                        P(shl_shell_params), P(shl_material), C.c_int,
                                        P(shl_solve_options), vp, P(shl_stats)]
+    L.shl_homogenize_zslab_host.argtypes = [vp, P(shl_slab_transport), C.c_int, C.c_int, P(shl_design),
+                                            P(shl_shell_params), P(shl_material), C.c_int,
+                                            P(shl_solve_options), vp, P(shl_stats)]
     L.shl_extract_isosurface.argtypes = [vp, vp, C.c_int64, vp, C.c_int64, P(C.c_int64),
                                          P(C.c_int64)]
     L.shl_voxel_raw.argtypes = [vp, vp]

@@ -610,6 +610,57 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def homogenize_zslab_host(params: DesignParams, sp: ShellParams, mat: BaseMaterial, r: int,
+                          rank: int, nranks: int, transport,
+                          opt: HomogenizeOptions = HomogenizeOptions(),
+                          ctx: Context | None = None) -> HomogenizationResult:
+    """One z-slab per rank over a host-staged transport (shl_homogenize_zslab_host):
+    `transport.allreduce_sum(buf)` sums a host numpy array over the ranks in
+    place; `transport.ring_exchange(send_hi, send_lo, recv_lo, recv_hi)` sends
+    to rank+1 / rank-1 and receives from rank-1 / rank+1 (numpy views of the
+    library's pinned staging buffers).  See zslab.TorchSlabTransport."""
+    ctx = ctx or default_context()
+    d, keep = params._abi()
+    spa, ma, oa = sp._abi(), mat._abi(), opt._abi()
+
+    def view(ptr, n, f64):
+        if n == 0:
+            return np.zeros(0, np.float64 if f64 else np.float32)
+        ct = (C.c_double if f64 else C.c_float) * n
+        return np.ctypeslib.as_array(ct.from_address(ptr))
+
+    def allreduce(user, buf, n, f64):
+        try:
+            transport.allreduce_sum(view(buf, n, f64))
+            return 0
+        except Exception:  # noqa: BLE001 - no exception may cross the C ABI
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def exchange(user, shi, nshi, slo, nslo, rlo, nrlo, rhi, nrhi, f64):
+        try:
+            transport.ring_exchange(view(shi, nshi, f64), view(slo, nslo, f64), view(rlo, nrlo, f64),
+                                    view(rhi, nrhi, f64))
+            return 0
+        except Exception:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    cbs = (L.SLAB_ALLREDUCE(allreduce), L.SLAB_EXCHANGE(exchange))  # kept alive for the call
+    tr = L.shl_slab_transport(None, cbs[0], cbs[1])
+    Cm = np.zeros(36)
+    st = L.shl_stats()
+    _check(L.lib().shl_homogenize_zslab_host(ctx.handle, C.byref(tr), int(rank), int(nranks), C.byref(d),
+                                             C.byref(spa), C.byref(ma), int(r), C.byref(oa),
+                                             Cm.ctypes.data, C.byref(st)), ctx)
+    s = SolveStats.from_abi(st)
+    return HomogenizationResult(Cm.reshape(6, 6), int(r), s.timings, s.volume_ratio,
+                                s.n_elements / float(r) ** 3, f"device_pcg_{s.precision}_zslab_host",
+                                s.iterations, s)
+
+
 def homogenize_zslab(params: DesignParams, sp: ShellParams, mat: BaseMaterial, r: int,
                      nccl_id: bytes, rank: int, nranks: int,
                      opt: HomogenizeOptions = HomogenizeOptions(),

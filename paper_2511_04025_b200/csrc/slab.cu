@@ -89,6 +89,94 @@ struct NcclComm {
   }
 };
 
+// ---------------------------------------------------------------- transports
+// What a rank's slab solve needs from the other ranks: an in-place sum of a
+// few device values (PCG scalars, C^H, the level-1 multigrid right-hand side)
+// and the periodic-ring ghost-plane exchange.  Two backends:
+//   NcclTransport -- ncclAllReduce / ncclSend+Recv on the stream (NVLink)
+//   HostTransport -- stream sync, D2H into pinned buffers, the caller's
+//                    callbacks (shl_slab_transport: e.g. torch.distributed
+//                    gloo over TCP), H2D.  No kernel ever waits for another
+//                    rank, so ranks may even share one GPU (tests).
+struct SlabTransport {
+  int rank = 0, nranks = 1;
+  virtual ~SlabTransport() = default;
+  virtual void allreduce(void* dev, size_t n, bool f64, cudaStream_t s) = 0;
+  // send send_hi to rank+1 and send_lo to rank-1; receive recv_lo from rank-1
+  // and recv_hi from rank+1 (counts in values)
+  virtual void exchange(const void* send_hi, size_t n_send_hi, const void* send_lo, size_t n_send_lo,
+                        void* recv_lo, size_t n_recv_lo, void* recv_hi, size_t n_recv_hi, bool f64,
+                        cudaStream_t s) = 0;
+};
+
+struct NcclTransport : SlabTransport {
+  NcclComm* comm;
+  explicit NcclTransport(NcclComm* c) : comm(c) {
+    rank = c->rank;
+    nranks = c->nranks;
+  }
+  void allreduce(void* dev, size_t n, bool f64, cudaStream_t s) override {
+    NK(nccl().AllReduce(dev, dev, n, f64 ? ncclFloat64 : ncclFloat32, ncclSum, comm->comm, s));
+  }
+  void exchange(const void* send_hi, size_t n_send_hi, const void* send_lo, size_t n_send_lo, void* recv_lo,
+                size_t n_recv_lo, void* recv_hi, size_t n_recv_hi, bool f64, cudaStream_t s) override {
+    const ncclDataType_t dt = f64 ? ncclFloat64 : ncclFloat32;
+    const int lo = (rank - 1 + nranks) % nranks, hi = (rank + 1) % nranks;
+    NK(nccl().GroupStart());
+    NK(nccl().Send(send_hi, n_send_hi, dt, hi, comm->comm, s));
+    NK(nccl().Send(send_lo, n_send_lo, dt, lo, comm->comm, s));
+    NK(nccl().Recv(recv_lo, n_recv_lo, dt, lo, comm->comm, s));
+    NK(nccl().Recv(recv_hi, n_recv_hi, dt, hi, comm->comm, s));
+    NK(nccl().GroupEnd());
+  }
+};
+
+struct HostTransport : SlabTransport {
+  shl_slab_transport cb;
+  unsigned char* host = nullptr;  // pinned staging
+  size_t cap = 0;
+  HostTransport(const shl_slab_transport& t, int r, int n) : cb(t) {
+    rank = r;
+    nranks = n;
+  }
+  ~HostTransport() override {
+    if (host) cudaFreeHost(host);
+  }
+  unsigned char* staging(size_t bytes) {
+    if (bytes > cap) {
+      if (host) cudaFreeHost(host);
+      host = nullptr;
+      cap = bytes + bytes / 4;
+      CK(cudaMallocHost(&host, cap));
+    }
+    return host;
+  }
+  void allreduce(void* dev, size_t n, bool f64, cudaStream_t s) override {
+    const size_t bytes = n * (f64 ? 8 : 4);
+    unsigned char* h = staging(bytes);
+    CK(cudaMemcpyAsync(h, dev, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (cb.allreduce_sum(cb.user, h, n, f64 ? 1 : 0) != 0)
+      throw ShlError(SHL_IO, "z-slab transport: allreduce_sum callback failed");
+    CK(cudaMemcpyAsync(dev, h, bytes, cudaMemcpyHostToDevice, s));
+  }
+  void exchange(const void* send_hi, size_t n_send_hi, const void* send_lo, size_t n_send_lo, void* recv_lo,
+                size_t n_recv_lo, void* recv_hi, size_t n_recv_hi, bool f64, cudaStream_t s) override {
+    const size_t w = f64 ? 8 : 4;
+    unsigned char* h = staging(w * (n_send_hi + n_send_lo + n_recv_lo + n_recv_hi));
+    unsigned char *hs_hi = h, *hs_lo = hs_hi + w * n_send_hi, *hr_lo = hs_lo + w * n_send_lo,
+                  *hr_hi = hr_lo + w * n_recv_lo;
+    if (n_send_hi) CK(cudaMemcpyAsync(hs_hi, send_hi, w * n_send_hi, cudaMemcpyDeviceToHost, s));
+    if (n_send_lo) CK(cudaMemcpyAsync(hs_lo, send_lo, w * n_send_lo, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (cb.ring_exchange(cb.user, hs_hi, n_send_hi, hs_lo, n_send_lo, hr_lo, n_recv_lo, hr_hi, n_recv_hi,
+                         f64 ? 1 : 0) != 0)
+      throw ShlError(SHL_IO, "z-slab transport: ring_exchange callback failed");
+    if (n_recv_lo) CK(cudaMemcpyAsync(recv_lo, hr_lo, w * n_recv_lo, cudaMemcpyHostToDevice, s));
+    if (n_recv_hi) CK(cudaMemcpyAsync(recv_hi, hr_hi, w * n_recv_hi, cudaMemcpyHostToDevice, s));
+  }
+};
+
 // ---------------------------------------------------------------- slab plan
 struct SlabPlan {
   int z0 = 0, z1 = 0;       // owned planes [z0, z1)
@@ -208,7 +296,7 @@ void build_slabs(shl_ctx* c, int G, int first, int count, std::vector<Slab>& sla
 // process holds; their vectors are small next to level 0).
 template <typename TX, typename TV, typename TZ>
 void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
-                     shl_stats* st, int prec, int G, NcclComm* comm, bool use_gmg) {
+                     shl_stats* st, int prec, int G, SlabTransport* comm, bool use_gmg) {
   const int r = c->r;
   if (!c->node0_active)
     throw ShlError(SHL_SOLVER, "mesh has no corner node group: cannot prescribe the strain gauge");
@@ -302,7 +390,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
   // cross-slab sum: in-process slabs are summed by the finalize kernel; ranks
   // all-reduce their one total first
   auto reduce = [&](int k) {
-    if (dist) NK(nccl().AllReduce(totals, totals, k, ncclFloat64, ncclSum, comm->comm, c->stream));
+    if (dist) comm->allreduce(totals, k, true, c->stream);
   };
   // ghost exchange of an 18-component vector (z each iteration, x for C^H)
   auto exchange = [&](auto vec_of) {
@@ -321,18 +409,13 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
       return;
     }
     Slab& me = slabs[0];
-    const int lo = (comm->rank - 1 + comm->nranks) % comm->nranks, hi = (comm->rank + 1) % comm->nranks;
     const size_t stride = 18 * static_cast<size_t>(std::max(max_plane, 1));
     T *send_hi = buf, *send_lo = buf + stride, *recv_lo = buf + 2 * stride, *recv_hi = buf + 3 * stride;
-    const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
     launch_pack<T>(vec_of(me), me.P.n_owned - me.P.cnt_last, me.P.cnt_last, send_hi, c->stream);
     launch_pack<T>(vec_of(me), 0, me.P.cnt_first, send_lo, c->stream);
-    NK(nccl().GroupStart());
-    NK(nccl().Send(send_hi, 18 * static_cast<size_t>(me.P.cnt_last), dt, hi, comm->comm, c->stream));
-    NK(nccl().Send(send_lo, 18 * static_cast<size_t>(me.P.cnt_first), dt, lo, comm->comm, c->stream));
-    NK(nccl().Recv(recv_lo, 18 * static_cast<size_t>(me.P.n_glo), dt, lo, comm->comm, c->stream));
-    NK(nccl().Recv(recv_hi, 18 * static_cast<size_t>(me.P.n_ghi), dt, hi, comm->comm, c->stream));
-    NK(nccl().GroupEnd());
+    comm->exchange(send_hi, 18 * static_cast<size_t>(me.P.cnt_last), send_lo, 18 * static_cast<size_t>(me.P.cnt_first),
+                   recv_lo, 18 * static_cast<size_t>(me.P.n_glo), recv_hi, 18 * static_cast<size_t>(me.P.n_ghi),
+                   sizeof(T) == 8, c->stream);
     launch_unpack<T>(vec_of(me), me.P.n_owned, me.P.n_glo, recv_lo, c->stream);
     launch_unpack<T>(vec_of(me), me.P.n_owned + me.P.n_glo, me.P.n_ghi, recv_hi, c->stream);
   };
@@ -390,9 +473,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
       launch_restrict_slab<TZ>(C1, S.map.as<int>(), S.P.zbase, S.P.nzl, S.P.z0, S.P.z1, r, RES(S), b1, dst,
                                c->stream);
     }
-    if (dist)
-      NK(nccl().AllReduce(b1, b1, 18 * static_cast<size_t>(c->gmg[0].ld), sizeof(TZ) == 8 ? ncclFloat64 : ncclFloat32,
-                          ncclSum, comm->comm, c->stream));
+    if (dist) comm->allreduce(b1, 18 * static_cast<size_t>(c->gmg[0].ld), sizeof(TZ) == 8, c->stream);
     TZ* x1 = vc.level(1, nullptr, init);  // coarse levels, replicated
     for (int s = 0; s < nloc; ++s) {
       Slab& S = slabs[s];
@@ -486,7 +567,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
   }
 }
 
-void homogenize_slabs(shl_ctx* c, int G, NcclComm* comm, const shl_design* design,
+void homogenize_slabs(shl_ctx* c, int G, SlabTransport* comm, const shl_design* design,
                       const shl_shell_params* sp, const shl_material* mat, int r,
                       const shl_solve_options* o, double* C_out, shl_stats* st) {
   if (!C_out) throw ShlError(SHL_VALIDATION, "null argument");
@@ -591,7 +672,21 @@ int shl_homogenize_zslab(shl_ctx* c, const uint8_t* nccl_id, int rank, int nrank
       c->nccl = comm;
       c->nccl_deleter = [](void* p) { delete static_cast<NcclComm*>(p); };
     }
-    homogenize_slabs(c, nranks, comm, design, sp, mat, r, opt, C_out, st);
+    NcclTransport t(comm);
+    homogenize_slabs(c, nranks, &t, design, sp, mat, r, opt, C_out, st);
+  });
+}
+
+int shl_homogenize_zslab_host(shl_ctx* c, const shl_slab_transport* transport, int rank, int nranks,
+                              const shl_design* design, const shl_shell_params* sp, const shl_material* mat,
+                              int r, const shl_solve_options* opt, double* C_out, shl_stats* st) {
+  if (!c || !transport || !transport->allreduce_sum || !transport->ring_exchange || nranks < 2 || rank < 0 ||
+      rank >= nranks)
+    return SHL_VALIDATION;
+  if (st) std::memset(st, 0, sizeof(*st));
+  return guarded(c, [&] {
+    HostTransport t(*transport, rank, nranks);
+    homogenize_slabs(c, nranks, &t, design, sp, mat, r, opt, C_out, st);
   });
 }
 

@@ -6,7 +6,9 @@
 Rank 0 creates the NCCL unique id through the library (shl_nccl_unique_id),
 torch.distributed (gloo) broadcasts the 128 bytes, and every rank calls
 shl_homogenize_zslab for its slab; C^H is identical on every rank.  With one
-process the same slab code runs emulated (`--emulate G`).  The default
+process the same slab code runs emulated (`--emulate G`).  `--transport host`
+runs the per-rank path over torch.distributed (gloo) through the host-staged
+transport (TorchSlabTransport) instead of NCCL.  The default
 preconditioner is multigrid: level 0 on the slabs (ghost exchange before every
 sweep, restriction all-reduced), coarse levels replicated on every rank.
 """
@@ -19,6 +21,41 @@ import os
 import numpy as np
 
 
+class TorchSlabTransport:
+    """Host-staged z-slab transport over torch.distributed (any backend that
+    moves CPU tensors, e.g. gloo): the callbacks of shl_homogenize_zslab_host.
+    Ring neighbours: rank-1 (lo) and rank+1 (hi), periodic; tag 1 carries the
+    plane sent upward, tag 2 the plane sent downward, so two ranks (lo == hi)
+    still pair every message."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allreduce_sum(self, buf: np.ndarray) -> None:
+        import torch
+        t = torch.from_numpy(buf)  # shares memory with the staging buffer
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def ring_exchange(self, send_hi, send_lo, recv_lo, recv_hi) -> None:
+        import torch
+        lo, hi = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        reqs = []
+        if send_hi.size:
+            reqs.append(self.dist.isend(torch.from_numpy(send_hi), hi, group=self.group, tag=1))
+        if send_lo.size:
+            reqs.append(self.dist.isend(torch.from_numpy(send_lo), lo, group=self.group, tag=2))
+        if recv_lo.size:
+            reqs.append(self.dist.irecv(torch.from_numpy(recv_lo), lo, group=self.group, tag=1))
+        if recv_hi.size:
+            reqs.append(self.dist.irecv(torch.from_numpy(recv_hi), hi, group=self.group, tag=2))
+        for q in reqs:
+            q.wait()
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--r", type=int, default=256)
@@ -27,6 +64,7 @@ def main(argv=None):
     ap.add_argument("--precision", default="mixed")
     ap.add_argument("--emulate", type=int, default=0, help="G slabs on one device")
     ap.add_argument("--preconditioner", default="auto", choices=["auto", "gmg", "jacobi"])
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"])
     a = ap.parse_args(argv)
     from . import api as S
     rank = int(os.environ.get("RANK", 0))
@@ -45,10 +83,14 @@ def main(argv=None):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("gloo")
-        obj = [S.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        res = S.homogenize_zslab(d, S.ShellParams(), S.BaseMaterial(), a.r, obj[0], rank, world,
-                                 opt, ctx)
+        if a.transport == "host":
+            res = S.homogenize_zslab_host(d, S.ShellParams(), S.BaseMaterial(), a.r, rank, world,
+                                          TorchSlabTransport(), opt, ctx)
+        else:
+            obj = [S.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            res = S.homogenize_zslab(d, S.ShellParams(), S.BaseMaterial(), a.r, obj[0], rank, world,
+                                     opt, ctx)
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:

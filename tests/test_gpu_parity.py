@@ -444,3 +444,30 @@ def test_floating_components_vs_reference_criterion(S, O, seed, r):
     sys_ = D.build_periodic_system(mesh, O.element_stiffness(1.0, 0.3, 1.0 / r))
     assert res.stats.n_components == sys_.n_components
     assert (res.stats.n_floating > 0) == sys_.expect_singular
+
+
+def test_repeat_runs_bitwise_identical(S):
+    """Race check without a sanitizer (compute-sanitizer is closed on this GPU
+    pool): the same 64^3 design solved repeatedly, alone and interleaved with
+    other designs on 1 and 3 batch lanes, gives bitwise identical C^H and
+    iteration counts -- every reduction (per-brick partials, last-CTA sums,
+    tile queues, union-find component count) is order-deterministic, so any
+    data race on them would show up as a changed bit."""
+    spec = S.RandomDesignSpec("cubic_octant", 8, 2, -1.0, 1.0)
+    sp, mat = S.ShellParams(), S.BaseMaterial()
+    opt = S.HomogenizeOptions(residual_tol=1e-6, precision="mixed")
+    d = S.random_design(spec, 7)
+    ctx = S.Context(0)
+    ref = S.homogenize(d, sp, mat, 64, opt, ctx=ctx)
+    for _ in range(3):
+        res = S.homogenize(d, sp, mat, 64, opt, ctx=ctx)
+        assert np.array_equal(res.tensor, ref.tensor)
+        assert np.array_equal(res.iterations, ref.iterations)
+        assert res.stats.n_components == ref.stats.n_components
+    others = [S.random_design(spec, s) for s in (8, 9, 10, 11, 12)]
+    for lanes in (1, 3):
+        C, status, st = S.homogenize_batch(others[:3] + [d] + others[3:], sp, mat, 64, opt, ctx=ctx, lanes=lanes)
+        assert np.all(status == 0)
+        assert np.array_equal(C[3], ref.tensor)
+        assert np.array_equal(st[3].iterations, ref.iterations)
+    ctx.close()
