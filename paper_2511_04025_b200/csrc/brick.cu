@@ -23,9 +23,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 
+#include "internal.h"
 #include "pcg_common.cuh"
+#include "stencil_patterns.h"
 
 namespace shl {
 
@@ -33,6 +36,8 @@ namespace shl {
 // constants, ElementConstLease in solver.cu)
 __constant__ double c_bK0d[576];
 __constant__ float c_bK0f[576];
+// FP32 stencil coefficients coef_m(c,d) = K0[3 a0(m) + c][3 b0(m) + d] (stencil_patterns.h)
+__constant__ float c_bcoeff[243];
 
 namespace {
 
@@ -59,9 +64,9 @@ constexpr int kWarps = kThreads / 32;
 // Staged vector layout: FP64 [q][position]; FP32 [c][load-case pair][position]
 // as float2, so the FP32 arithmetic runs on packed FFMA2 over load-case pairs
 // and reads one 64-bit shared word per pair.
-template <typename TS>
+template <typename TS, bool kPairs = (sizeof(TS) == 4)>
 __device__ __forceinline__ int xs_index(int q, int p) {
-  if constexpr (sizeof(TS) == 4)
+  if constexpr (kPairs)
     return (((q / 6) * 3 + (q % 6) / 2) * kRegion + p) * 2 + (q & 1);
   else
     return q * kRegion + p;
@@ -136,17 +141,17 @@ __device__ __forceinline__ void prefetch_rows(const T* v, int nq, int first, int
 
 // Shared memory of one CTA (= one brick): the staged input vector, the
 // element betas, the node map of the region and the brick's node positions.
-template <typename TS>
+template <typename TS, typename TB = TS>
 struct BrickShared {
   TS xs[18 * kRegion];        // [q][position], 0 where absent
-  TS bs[kERegion];            // element betas of the region
+  TB bs[kERegion];            // element betas of the region
   int ms[kRegion];            // node ids of the region (-1 absent)
   unsigned short pc[kNodes];  // region position of brick node first + i
   double red[kWarps * 6];
 };
-template <typename TS>
+template <typename TS, typename TB = TS>
 constexpr size_t brick_smem_bytes() {
-  return sizeof(BrickShared<TS>);
+  return sizeof(BrickShared<TS, TB>);
 }
 
 __device__ __forceinline__ void brick_origin(const BrickView& B, int t, int& x0, int& y0, int& z0) {
@@ -172,8 +177,8 @@ struct NbEntry {
 __constant__ NbEntry c_nb[27];
 constexpr int kNbFace = 1, kNbEdge = 7, kNbCorner = 19;  // class starts: centre [0,1), faces, edges, corners
 
-template <int K, typename TS>
-__device__ __forceinline__ void gather_class(TS (&y)[18], const TS* __restrict__ xs, const TS* __restrict__ bs,
+template <int K, typename TS, typename TX = TS>
+__device__ __forceinline__ void gather_class(TS (&y)[18], const TX* __restrict__ xs, const TS* __restrict__ bs,
                                              int pc, int ec, int m0, int m1) {
 #pragma unroll 2
   for (int m = m0; m < m1; ++m) {
@@ -189,10 +194,11 @@ __device__ __forceinline__ void gather_class(TS (&y)[18], const TS* __restrict__
 #pragma unroll
         for (int d = 0; d < 3; ++d) Sm[c * 3 + d] = fma_t(bej, k0<TS>(kb + c * 24 + d), Sm[c * 3 + d]);
     }
-    const TS* xn = xs + pc + c_nb[m].roff;
+    const TX* xn = xs + pc + c_nb[m].roff;
 #pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      const TS z0 = xn[(0 * 6 + s) * kRegion], z1 = xn[(1 * 6 + s) * kRegion], z2 = xn[(2 * 6 + s) * kRegion];
+    for (int s = 0; s < 6; ++s) {  // (an FP32-staged vector widens exactly)
+      const TS z0 = static_cast<TS>(xn[(0 * 6 + s) * kRegion]), z1 = static_cast<TS>(xn[(1 * 6 + s) * kRegion]),
+               z2 = static_cast<TS>(xn[(2 * 6 + s) * kRegion]);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         TS v = y[c * 6 + s];
@@ -205,9 +211,29 @@ __device__ __forceinline__ void gather_class(TS (&y)[18], const TS* __restrict__
   }
 }
 
-// FP32 operator: the whole 27-point stencil unrolled so the K0 entries are
-// constant-bank operands of the S-build FFMAs, and the application on packed
-// FFMA2 over load-case pairs (one FFMA2 = two load cases).
+// The S-build through the stencil's sign structure (stencil_patterns.h): per
+// neighbour the distinct signed beta sums (60 per node, 124 adds) times the
+// 243 stencil coefficients, instead of 576 beta*K0 FMAs with 576 constants.
+// Every index is a compile-time constant after unrolling.
+__device__ __forceinline__ void stencil_block_f32(int m, const float (&be)[8], float (&Sm)[9]) {
+  float P[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    if (p >= pat::npat(m)) break;
+    float acc = be[pat::elem(m, 0)];  // the first sign of every pattern is +1
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+      if (j >= pat::shared(m)) break;
+      acc = pat::sign(m, p, j) > 0 ? acc + be[pat::elem(m, j)] : acc - be[pat::elem(m, j)];
+    }
+    P[p] = acc;
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) Sm[q] = c_bcoeff[m * 9 + q] * P[pat::pat_of(m, q)];
+}
+
+// FP32 operator: the stencil unrolled with the structured S-build and the
+// application on packed FFMA2 over load-case pairs (one FFMA2 = two load cases).
 __device__ __forceinline__ void brick_gather_f32(float (&y)[18], const float* __restrict__ xs,
                                                  const float* __restrict__ bs, int pc, int ec) {
   float2 acc[9];  // [c][load-case pair]
@@ -224,19 +250,7 @@ __device__ __forceinline__ void brick_gather_f32(float (&y)[18], const float* __
   for (int m = 0; m < 27; ++m) {
     const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
     float Sm[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) Sm[q] = 0.f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
-      const int bx = ox + dx, by = oy + dy, bz = oz + dz;
-      if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
-      const int a = corner_id(ox, oy, oz), b = corner_id(bx, by, bz);
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) Sm[c * 3 + d] = fmaf(be[e], c_bK0f[(3 * a + c) * 24 + 3 * b + d], Sm[c * 3 + d]);
-    }
+    stencil_block_f32(m, be, Sm);
     const float2* xn = x2 + pc + dz * (kRX * kRY) + dy * kRX + dx;
 #pragma unroll
     for (int sp = 0; sp < 3; ++sp) {
@@ -262,8 +276,8 @@ __device__ __forceinline__ void brick_gather_f32(float (&y)[18], const float* __
 
 // y (18, component-major q = c*6 + s) = sum over the 27 neighbours of S_m x_m,
 // S_m = sum_e beta_e K0[a(n,e), b(m,e)] built from the staged element betas.
-template <typename TS>
-__device__ __forceinline__ void brick_gather(TS (&y)[18], const TS* __restrict__ xs, const TS* __restrict__ bs, int pc,
+template <typename TS, typename TX = TS>
+__device__ __forceinline__ void brick_gather(TS (&y)[18], const TX* __restrict__ xs, const TS* __restrict__ bs, int pc,
                                              int ec) {
   if constexpr (sizeof(TS) == 4) {
     brick_gather_f32(y, xs, bs, pc, ec);
@@ -271,10 +285,10 @@ __device__ __forceinline__ void brick_gather(TS (&y)[18], const TS* __restrict__
   }
 #pragma unroll
   for (int q = 0; q < 18; ++q) y[q] = TS(0);
-  gather_class<8, TS>(y, xs, bs, pc, ec, 0, kNbFace);
-  gather_class<4, TS>(y, xs, bs, pc, ec, kNbFace, kNbEdge);
-  gather_class<2, TS>(y, xs, bs, pc, ec, kNbEdge, kNbCorner);
-  gather_class<1, TS>(y, xs, bs, pc, ec, kNbCorner, 27);
+  gather_class<8, TS, TX>(y, xs, bs, pc, ec, 0, kNbFace);
+  gather_class<4, TS, TX>(y, xs, bs, pc, ec, kNbFace, kNbEdge);
+  gather_class<2, TS, TX>(y, xs, bs, pc, ec, kNbEdge, kNbCorner);
+  gather_class<1, TS, TX>(y, xs, bs, pc, ec, kNbCorner, 27);
 }
 
 // Last CTA: fixed-order sum of the nab per-brick partials.
@@ -301,10 +315,13 @@ __device__ __forceinline__ bool brick_last_sum(uint32_t* counter, const double* 
 // vector at every region position (cp.async straight into shared memory; an
 // FP32 vector for an FP64 operator lands in the high half of its FP64 slot
 // and is converted in place), and the brick's own node positions.
-template <typename TS, typename TG>
-__device__ __forceinline__ void stage_brick(BrickShared<TS>& S, const BrickView& B, int t, int r, int first,
-                                            int last, const int* __restrict__ nmap, const TS* __restrict__ beta,
+template <typename TS, typename TG, typename TB = TS>
+__device__ __forceinline__ void stage_brick(BrickShared<TS, TB>& S, const BrickView& B, int t, int r, int first,
+                                            int last, const int* __restrict__ nmap, const TB* __restrict__ beta,
                                             const TG* __restrict__ v) {
+  // FP32 arithmetic reads load-case pairs; an FP32 vector for the FP64
+  // operator keeps the [q][position] layout of its scalar widening loads
+  constexpr bool kPairs = sizeof(TS) == 4 && sizeof(TB) == 4;
   int x0, y0, z0;
   brick_origin(B, t, x0, y0, z0);
   constexpr int kPer = (kRegion + kThreads - 1) / kThreads;  // 3
@@ -321,7 +338,7 @@ __device__ __forceinline__ void stage_brick(BrickShared<TS>& S, const BrickView&
   for (int e = threadIdx.x; e < kERegion; e += kThreads) {
     const int lx = e % kEX, ly = (e / kEX) % kEY, lz = e / (kEX * kEY);
     const int gx = wrap3(x0 + lx - 1, r), gy = wrap3(y0 + ly - 1, r), gz = wrap3(z0 + lz - 1, r);
-    cp_async<sizeof(TS)>(&S.bs[e], beta + (static_cast<size_t>(gz) * r + gy) * r + gx);
+    cp_async<sizeof(TB)>(&S.bs[e], beta + (static_cast<size_t>(gz) * r + gy) * r + gx);
   }
   cp_async_commit();
   cp_async_wait<1>();  // the map (betas stay in flight)
@@ -341,13 +358,13 @@ __device__ __forceinline__ void stage_brick(BrickShared<TS>& S, const BrickView&
 #pragma unroll
       for (int q = 0; q < 18; ++q) {
         if constexpr (sizeof(TS) == sizeof(TG))
-          cp_async<sizeof(TS)>(&S.xs[xs_index<TS>(q, p)], src + q * 32);
+          cp_async<sizeof(TS)>(&S.xs[xs_index<TS, kPairs>(q, p)], src + q * 32);
         else
-          cp_async<sizeof(TG)>(reinterpret_cast<TG*>(&S.xs[xs_index<TS>(q, p)]) + 1, src + q * 32);
+          cp_async<sizeof(TG)>(reinterpret_cast<TG*>(&S.xs[xs_index<TS, kPairs>(q, p)]) + 1, src + q * 32);
       }
     } else {
 #pragma unroll
-      for (int q = 0; q < 18; ++q) S.xs[xs_index<TS>(q, p)] = TS(0);
+      for (int q = 0; q < 18; ++q) S.xs[xs_index<TS, kPairs>(q, p)] = TS(0);
     }
   }
   cp_async_commit();
@@ -395,36 +412,35 @@ __global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const Apply
   __shared__ double scratch[32 * 6];
   PcgState* st = A.state;
   if (st->stop) return;
-  BrickShared<TV>& S = *reinterpret_cast<BrickShared<TV>*>(brick_raw);
+  // z staged in its storage type (FP32 in mixed multigrid: half the shared
+  // memory of an FP64 copy, so more bricks per SM), widened exactly on use
+  BrickShared<TZ, TV>& S = *reinterpret_cast<BrickShared<TZ, TV>*>(brick_raw);
   const BrickView& B = A.bricks;
   const int t = blockIdx.x;
   const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
   const int idx = first + threadIdx.x;
   const bool valid = idx < last;
-  // own rows first: they land while the brick stages and computes
-  TV pv[18], qv[18];
   const size_t ob = vbase(valid ? idx : 0, 18);
-  if (valid) {
-#pragma unroll
-    for (int q = 0; q < 18; ++q) {
-      pv[q] = A.p[ob + q * 32];
-      qv[q] = A.q[ob + q * 32];
-    }
-  }
-  stage_brick<TV, TZ>(S, B, t, A.r, first, last, A.node_map, A.beta, A.z);
+  stage_brick<TZ, TZ, TV>(S, B, t, A.r, first, last, A.node_map, A.beta, A.z);
   double pq[6] = {0, 0, 0, 0, 0, 0};
   if (valid) {
     const TV ridge = static_cast<TV>(st->ridge);
     const int pc = S.pc[threadIdx.x];
     const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
     TV y[18];
-    brick_gather<TV>(y, S.xs, S.bs, pc, lz * (kEX * kEY) + ly * kEX + lx);
+    brick_gather<TV, TZ>(y, S.xs, S.bs, pc, lz * (kEX * kEY) + ly * kEX + lx);
     TV* __restrict__ pg = A.p + ob;
     TV* __restrict__ qg = A.q + ob;
+    TV pv[18], qv[18];
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {  // every load in flight before the first store
+      pv[q] = pg[q * 32];
+      qv[q] = qg[q * 32];
+    }
 #pragma unroll
     for (int q = 0; q < 18; ++q) {
       const int s = q % 6;
-      const TV zq = S.xs[xs_index<TV>(q, pc)];
+      const TV zq = static_cast<TV>(S.xs[xs_index<TZ, false>(q, pc)]);
       const TV w = idx == 0 ? TV(0) : fma_t(ridge, zq, y[q]);  // node 0 (id 0) pinned
       TV pn = TV(0), qn = TV(0);
       if (!st->done[s]) {
@@ -562,6 +578,26 @@ static void build_nb_table(NbEntry (&t)[27]) {
 }
 
 void brick_upload_constants(const double* K0d, const float* K0f, cudaStream_t s) {
+  // coef_m(c,d) = K0[3 a0 + c][3 b0 + d]; every other term of the entry must be
+  // +-coef (the isotropic sign structure of stencil_patterns.h)
+  static thread_local float cf[243];
+  double kmax = 0.0;
+  for (int i = 0; i < 576; ++i) kmax = std::max(kmax, std::fabs(K0d[i]));
+  for (int m = 0; m < 27; ++m) {
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+    for (int q = 0; q < 9; ++q) {
+      const int c = q / 3, d = q % 3;
+      const double coef = K0d[(3 * pat::a0(m) + c) * 24 + 3 * pat::b0(m) + d];
+      for (int j = 0; j < pat::shared(m); ++j) {
+        const int e = pat::elem(m, j), ox = e & 1, oy = (e >> 1) & 1, oz = (e >> 2) & 1;
+        const int a = corner_id(ox, oy, oz), b = corner_id(ox + dx, oy + dy, oz + dz);
+        if (std::fabs(K0d[(3 * a + c) * 24 + 3 * b + d] - coef * pat::sign(m, pat::pat_of(m, q), j)) > 1e-12 * kmax)
+          throw ShlError(SHL_VALIDATION, "element stiffness lacks the isotropic stencil sign structure");
+      }
+      cf[m * 9 + q] = static_cast<float>(coef);
+    }
+  }
+  cudaMemcpyToSymbolAsync(c_bcoeff, cf, sizeof(cf), 0, cudaMemcpyHostToDevice, s);
   static NbEntry table[27];
   static const bool built = (build_nb_table(table), true);
   (void)built;
@@ -573,8 +609,8 @@ void brick_upload_constants(const double* K0d, const float* K0f, cudaStream_t s)
 // Staged brick apply: one resident CTA per slot, bricks from the tile queue.
 template <typename TV, typename TZ>
 void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s) {
-  constexpr size_t smem = brick_smem_bytes<TV>();
-  constexpr int kMinB = sizeof(TV) == 8 ? 3 : 5;
+  constexpr size_t smem = brick_smem_bytes<TZ, TV>();
+  constexpr int kMinB = sizeof(TZ) == 8 ? 3 : 4;
   static const bool configured = brick_configure(brick_apply_kernel<TV, TZ, kMinB>, smem);
   (void)configured;
   brick_apply_kernel<TV, TZ, kMinB><<<a.bricks.nab, kThreads, smem, s>>>(a);
