@@ -408,6 +408,7 @@ __device__ __forceinline__ void brick_reduce6(double (&v)[6], double* red, doubl
 // CTAs per SM overlap each other's staging and arithmetic).
 template <typename TV, typename TZ, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const ApplyArgs<TV, TZ> A) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char brick_raw[];
   __shared__ double scratch[32 * 6];
   PcgState* st = A.state;
@@ -440,7 +441,8 @@ __global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const Apply
 #pragma unroll
     for (int q = 0; q < 18; ++q) {
       const int s = q % 6;
-      const TV zq = static_cast<TV>(S.xs[xs_index<TZ, false>(q, pc)]);
+      // (the staged layout of stage_brick: load-case pairs iff all-FP32)
+      const TV zq = static_cast<TV>(S.xs[xs_index<TZ, sizeof(TZ) == 4 && sizeof(TV) == 4>(q, pc)]);
       const TV w = idx == 0 ? TV(0) : fma_t(ridge, zq, y[q]);  // node 0 (id 0) pinned
       TV pn = TV(0), qn = TV(0);
       if (!st->done[s]) {
@@ -474,6 +476,7 @@ template <typename TB, typename TV, typename TO, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
     brick_sweep_kernel(const GmgLevelView<TV> L, const TB* __restrict__ b, const TV* __restrict__ xin,
                        TO* __restrict__ xout, TV omega, int mode, PcgState* st, double* partials, int init) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char brick_raw[];
   __shared__ double scratch[32 * 6];
   if (st->stop) return;
@@ -613,7 +616,7 @@ void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s) {
   constexpr int kMinB = sizeof(TZ) == 8 ? 3 : 4;
   static const bool configured = brick_configure(brick_apply_kernel<TV, TZ, kMinB>, smem);
   (void)configured;
-  brick_apply_kernel<TV, TZ, kMinB><<<a.bricks.nab, kThreads, smem, s>>>(a);
+  launch_pdl(brick_apply_kernel<TV, TZ, kMinB>, a.bricks.nab, kThreads, smem, s, a);
 }
 
 // Staged brick sweep of level 0, one resident CTA per slot.
@@ -624,8 +627,8 @@ void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, T
   constexpr int kMinB = sizeof(TV) == 8 ? 3 : 5;
   static const bool configured = brick_configure(brick_sweep_kernel<TB, TV, TO, kMinB>, smem);
   (void)configured;
-  brick_sweep_kernel<TB, TV, TO, kMinB><<<L.bricks.nab, kThreads, smem, s>>>(
-      L, b, xin, xout, omega, mode, st, partials, init);
+  launch_pdl(brick_sweep_kernel<TB, TV, TO, kMinB>, L.bricks.nab, kThreads, smem, s, L, b, xin, xout, omega, mode,
+             st, partials, init);
 }
 
 template void launch_brick_apply<double, float>(const ApplyArgs<double, float>&, cudaStream_t);

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(192)
     level_sweep3_kernel(const LevelArgs<TV> L, const TB* __restrict__ b, const TV* __restrict__ xin,
                         TO* __restrict__ xout, TV omega, int mode, PcgState* st, double* partials,
                         int init) {
+  pdl_wait();
   __shared__ __align__(16) TV part_s[2][3 * 18 * 32];
   __shared__ double scratch[32 * 6];
   if (st->stop) return;
@@ -276,6 +277,7 @@ template <typename TV>
 __global__ void __launch_bounds__(256) coarse_warp_sweep_kernel(const LevelArgs<TV> L, const TV* __restrict__ b,
                                                                 const TV* __restrict__ xin, TV* __restrict__ xout,
                                                                 TV omega, int mode, const PcgState* st) {
+  pdl_wait();
   if (st->stop) return;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= L.n) return;  // whole warps exit together
@@ -287,6 +289,7 @@ template <typename TB, typename TV>
 __global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV* __restrict__ dinv,
                                     int n, const TB* __restrict__ b, TV* __restrict__ xout, TV omega,
                                     const PcgState* st) {
+  pdl_wait();
   if (st->stop) return;
   int idx, s;
   node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
@@ -308,6 +311,7 @@ template <typename TV>
 __global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c,
                                 const int* __restrict__ map_f, int r_f, const TV* __restrict__ res_f,
                                 TV* __restrict__ b_c, const PcgState* st) {
+  pdl_wait();
   if (st->stop) return;
   int idx, s;
   node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
@@ -382,6 +386,7 @@ template <typename TV>
 __global__ void prolong_kernel(const int* __restrict__ list_f, int n_f, int r_f,
                                const int* __restrict__ map_c, int r_c, const TV* __restrict__ x_c,
                                TV* __restrict__ x_f, const PcgState* st) {
+  pdl_wait();
   if (st->stop) return;
   int idx, s;
   node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
@@ -676,12 +681,12 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
   }
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
   if (fine) {
-    level_sweep3_kernel<TB, TV, true><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+    launch_pdl(level_sweep3_kernel<TB, TV, true>, grid, 192, 0, s, a, b, xin, xout, omega, mode, st, partials, init);
   } else if (L.n > 32768) {  // large stored level: thread per node is throughput-bound
-    level_sweep3_kernel<TB, TV, false><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, mode, st, partials, init);
+    launch_pdl(level_sweep3_kernel<TB, TV, false>, grid, 192, 0, s, a, b, xin, xout, omega, mode, st, partials, init);
   } else {  // small stored level: latency-bound, one warp per node (mode 2 is level-0 only)
-    coarse_warp_sweep_kernel<TV><<<(L.n + 7) / 8, 256, 0, s>>>(a, reinterpret_cast<const TV*>(b), xin, xout,
-                                                               omega, mode, st);
+    launch_pdl(coarse_warp_sweep_kernel<TV>, (L.n + 7) / 8, 256, 0, s, a, reinterpret_cast<const TV*>(b), xin, xout,
+               omega, mode, st);
   }
 }
 
@@ -693,19 +698,23 @@ void launch_level_sweep_out(const GmgLevelView<TV>& L, const TB* b, const TV* xi
     return;
   }
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
-  level_sweep3_kernel<TB, TV, true, TO><<<grid, 192, 0, s>>>(a, b, xin, xout, omega, 2, st, partials, init);
+  launch_pdl(level_sweep3_kernel<TB, TV, true, TO>, grid, 192, 0, s, a, b, xin, xout, omega, 2, st, partials, init);
 }
 
 template <typename TB, typename TV>
 void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
                          cudaStream_t s) {
-  if (L.n) jacobi_first_kernel<TB, TV><<<node_case_blocks(L.n, 192), 192, 0, s>>>(L.node_list, L.dinv, L.n, b, xout, omega, st);
+  if (L.n)
+    launch_pdl(jacobi_first_kernel<TB, TV>, node_case_blocks(L.n, 192), 192, 0, s, L.node_list, L.dinv, L.n, b, xout,
+               omega, st);
 }
 
 template <typename TV>
 void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
                      const PcgState* st, cudaStream_t s) {
-  if (C.n) restrict_kernel<TV><<<node_case_blocks(C.n, 192), 192, 0, s>>>(C.node_list, C.n, C.r, F.node_map, F.r, res_f, b_c, st);
+  if (C.n)
+    launch_pdl(restrict_kernel<TV>, node_case_blocks(C.n, 192), 192, 0, s, C.node_list, C.n, C.r, F.node_map, F.r,
+               res_f, b_c, st);
 }
 
 template <typename TV>
@@ -719,7 +728,9 @@ void launch_restrict_slab(const GmgLevelView<TV>& C, const int* map_s, int zbase
 template <typename TV>
 void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
                     const PcgState* st, cudaStream_t s) {
-  if (F.n) prolong_kernel<TV><<<node_case_blocks(F.n, 192), 192, 0, s>>>(F.node_list, F.n, F.r, C.node_map, C.r, x_c, x_f, st);
+  if (F.n)
+    launch_pdl(prolong_kernel<TV>, node_case_blocks(F.n, 192), 192, 0, s, F.node_list, F.n, F.r, C.node_map, C.r, x_c,
+               x_f, st);
 }
 
 #define SHL_GMG_INST(TV)                                                                               \

@@ -12,6 +12,32 @@
 
 namespace shl {
 
+// ---- programmatic dependent launch -------------------------------------------
+// The solve loop is a chain of ~35 dependent kernels per PCG iteration, most of
+// them small (coarse multigrid levels).  Launched with programmatic stream
+// serialization, a kernel's launch is processed while its predecessor still
+// runs; pdl_wait() (griddepcontrol.wait) then holds it until the predecessor
+// has completed and its writes are visible.  Every kernel launched this way
+// calls pdl_wait() before touching global memory; launched normally it is a
+// no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ float fma_t(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fma_t(double a, double b, double c) { return fma(a, b, c); }
 

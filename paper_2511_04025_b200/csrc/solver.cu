@@ -525,6 +525,7 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
 // of a node block run together and Dinv is re-read from L2, not DRAM.
 template <typename TX, typename TV, typename TZ>
 __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV, TZ> U) {
+  pdl_wait();
   __shared__ double scratch[32 * 2];
   PcgState* st = U.state;
   if (st->stop) return;
@@ -782,10 +783,11 @@ void launch_finalize_update(PcgState* st, const double* totals, int nslab, int i
 // Device-side loop control of the solve graph: keep iterating while the PCG
 // state has not stopped (converged, broken down or out of iterations).
 __global__ void set_while_kernel(cudaGraphConditionalHandle h, const PcgState* st) {
+  pdl_wait();
   cudaGraphSetConditional(h, st->stop ? 0u : 1u);
 }
 void launch_set_while(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s) {
-  set_while_kernel<<<1, 1, 0, s>>>(h, st);
+  launch_pdl(set_while_kernel, 1, 1, 0, s, h, st);
 }
 
 void launch_finalize_update_gmg(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s) {
@@ -907,7 +909,7 @@ int apply_grid(int n, int num_sms) { return std::max(1, std::min((n + 63) / 64, 
 
 template <typename TX, typename TV, typename TZ>
 void launch_update(const UpdateArgs<TX, TV, TZ>& u, int grid, cudaStream_t s) {
-  update_kernel<TX, TV, TZ><<<grid, 256, 0, s>>>(u);
+  launch_pdl(update_kernel<TX, TV, TZ>, grid, 256, 0, s, u);
 }
 
 template <typename TX>
