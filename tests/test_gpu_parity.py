@@ -251,9 +251,10 @@ def test_batch_lanes_match_single(S, r, lanes):
 
 def test_c4_sweep_subset(S):
     """Config C4 (64^3, CubicOctant 8 pre-expansion charges): seeds 0..15 in one
-    batch with 4 designs in flight; seeds 0..3 against the oracle's C^H
-    (tests/golden/c4_chom.npz, masked PCG to rtol 1e-8) at the 1e-4 relative
-    Frobenius bar, all 16 finite, symmetric and positive definite."""
+    batch with 4 designs in flight, every one against the oracle's C^H
+    (tests/golden/c4_chom.npz, masked block-Jacobi PCG to rtol 1e-8; the
+    fixed 16-seed subset of SURVEY.md §8 d) at the 1e-4 relative Frobenius
+    bar, and all 16 finite, symmetric and positive definite."""
     gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "c4_chom.npz"))
     spec = S.RandomDesignSpec("cubic_octant", 8, 2, -1.0, 1.0)
     designs = [S.random_design(spec, s) for s in range(16)]
