@@ -3,18 +3,15 @@
 // The matrix-free masked operator of the reference's GridSolver::apply
 // (grid_solver.hpp:154-176: y_n = sum_e beta_e K0 u_e, node 0 pinned) applied
 // brick by brick.  Level-0 node ids are numbered brick-major (voxel.cu
-// brick_* kernels): the torus is cut into 8x8x4-node bricks, each active brick
-// owns a contiguous id range [bstart[t], bstart[t+1]).  A CTA takes one brick
-// from the tile queue and
-//   1. stages the node map of the brick + 1-node halo (10x10x6 = 600
-//      positions) and beta of its 9x9x5 elements in shared memory,
-//   2. gathers the 18 components (3 dof x 6 load cases) of the input vector at
-//      every staged position into shared memory ([q][600], converted to the
-//      operator type once per position instead of once per use),
+// brick_* kernels): the torus is cut into 8x4x4-node bricks, each active brick
+// owns a contiguous id range [bstart[t], bstart[t+1]).  One CTA per active brick
+//   1. stages the node map of the brick + 1-node halo (10x6x6 = 360
+//      positions) and beta of its 9x5x5 elements in shared memory (cp.async),
+//   2. stages the 18 components (3 dof x 6 load cases) of the input vector at
+//      every staged position in shared memory (cp.async, bank-swizzled rows),
 //   3. gives each active node of the brick one thread, which builds the 27
-//      neighbour blocks S_m = sum_e beta_e K0[a(n,e), b(m,e)] (K0 from the
-//      constant bank, FP64 or FP32) and applies them to all six load cases
-//      from shared memory,
+//      neighbour blocks S_m = sum_e beta_e K0[a(n,e), b(m,e)] and applies them
+//      to all six load cases from shared memory,
 //   4. runs the caller's epilogue (PCG direction update, smoother or
 //      residual) on the node's own coalesced rows, and reduces its dot
 //      products per brick (fixed order -> reproducible).
@@ -61,15 +58,36 @@ constexpr int kNodes = kBX * kBY * kBZ;    // 128 nodes per brick
 constexpr int kThreads = kNodes;           // one thread per brick node
 constexpr int kWarps = kThreads / 32;
 
-// Staged vector layout: FP64 [q][position]; FP32 [c][load-case pair][position]
-// as float2, so the FP32 arithmetic runs on packed FFMA2 over load-case pairs
-// and reads one 64-bit shared word per pair.
-template <typename TS, bool kPairs = (sizeof(TS) == 4)>
-__device__ __forceinline__ int xs_index(int q, int p) {
+// Staged vector layout.  FP32 arithmetic reads [c][load-case pair][position]
+// as float2 (packed FFMA2 over load-case pairs, one 64-bit word per pair); a
+// position (lx, ly, lz) of the 10x6x6 region lives in row slot 4*ly + prow(lz)
+// of 10 positions, so consecutive y rows sit 40 positions apart and the 2 rows
+// of 8 nodes a half warp reads in a full brick plane fall on disjoint banks
+// (with the packed 10-position row stride 2 of every 16 lanes collided).
+// Planes 0-3 interleave in row slots 0..23, planes 4-5 in 24..45 (460
+// positions instead of 360).  The FP64 operator's [q][position] layout stays
+// packed (its smem footprint sets the CTAs per SM, and it is not bank-bound).
+constexpr int kPhys = 460;
+__device__ __forceinline__ int plane_base(int lz) { return kRX * ((lz & 3) + 24 * (lz >> 2)); }
+constexpr int kRowStep = 4 * kRX;  // positions between staged rows ly and ly + 1 (swizzled)
+template <bool kPairs>
+__device__ __forceinline__ int stage_pos(int lx, int ly, int lz) {
   if constexpr (kPairs)
-    return (((q / 6) * 3 + (q % 6) / 2) * kRegion + p) * 2 + (q & 1);
+    return plane_base(lz) + kRowStep * ly + lx;
   else
-    return q * kRegion + p;
+    return lx + kRX * (ly + kRY * lz);
+}
+template <bool kPairs>
+constexpr int stage_words() {
+  return kPairs ? kPhys : kRegion;
+}
+
+template <typename TS, bool kPairs = (sizeof(TS) == 4)>
+__device__ __forceinline__ int xs_index(int q, int pos) {
+  if constexpr (kPairs)
+    return (((q / 6) * 3 + (q % 6) / 2) * kPhys + pos) * 2 + (q & 1);
+  else
+    return q * kRegion + pos;
 }
 
 // v in [-r, 3r) -> [0, r)   (staged coordinates never leave that range for r >= 4)
@@ -143,7 +161,7 @@ __device__ __forceinline__ void prefetch_rows(const T* v, int nq, int first, int
 // element betas, the node map of the region and the brick's node positions.
 template <typename TS, typename TB = TS>
 struct BrickShared {
-  TS xs[18 * kRegion];        // [q][position], 0 where absent
+  TS xs[18 * stage_words<sizeof(TS) == 4 && sizeof(TB) == 4>()];  // [q][position], 0 where absent
   TB bs[kERegion];            // element betas of the region
   int ms[kRegion];            // node ids of the region (-1 absent)
   unsigned short pc[kNodes];  // region position of brick node first + i
@@ -235,7 +253,7 @@ __device__ __forceinline__ void stencil_block_f32(int m, const float (&be)[8], f
 // FP32 operator: the stencil unrolled with the structured S-build and the
 // application on packed FFMA2 over load-case pairs (one FFMA2 = two load cases).
 __device__ __forceinline__ void brick_gather_f32(float (&y)[18], const float* __restrict__ xs,
-                                                 const float* __restrict__ bs, int pc, int ec) {
+                                                 const float* __restrict__ bs, int pxy, int lz, int ec) {
   float2 acc[9];  // [c][load-case pair]
 #pragma unroll
   for (int q = 0; q < 9; ++q) acc[q] = make_float2(0.f, 0.f);
@@ -251,10 +269,10 @@ __device__ __forceinline__ void brick_gather_f32(float (&y)[18], const float* __
     const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
     float Sm[9];
     stencil_block_f32(m, be, Sm);
-    const float2* xn = x2 + pc + dz * (kRX * kRY) + dy * kRX + dx;
+    const float2* xn = x2 + plane_base(lz + dz) + pxy + dy * kRowStep + dx;
 #pragma unroll
     for (int sp = 0; sp < 3; ++sp) {
-      const float2 z0 = xn[(0 * 3 + sp) * kRegion], z1 = xn[(1 * 3 + sp) * kRegion], z2 = xn[(2 * 3 + sp) * kRegion];
+      const float2 z0 = xn[(0 * 3 + sp) * kPhys], z1 = xn[(1 * 3 + sp) * kPhys], z2 = xn[(2 * 3 + sp) * kPhys];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         float2 v = acc[c * 3 + sp];
@@ -278,9 +296,9 @@ __device__ __forceinline__ void brick_gather_f32(float (&y)[18], const float* __
 // S_m = sum_e beta_e K0[a(n,e), b(m,e)] built from the staged element betas.
 template <typename TS, typename TX = TS>
 __device__ __forceinline__ void brick_gather(TS (&y)[18], const TX* __restrict__ xs, const TS* __restrict__ bs, int pc,
-                                             int ec) {
+                                             int pxy, int lz, int ec) {
   if constexpr (sizeof(TS) == 4) {
-    brick_gather_f32(y, xs, bs, pc, ec);
+    brick_gather_f32(y, xs, bs, pxy, lz, ec);
     return;
   }
 #pragma unroll
@@ -349,6 +367,7 @@ __device__ __forceinline__ void stage_brick(BrickShared<TS, TB>& S, const BrickV
     if (p >= kRegion) continue;
     const int id = S.ms[p];
     const int lx = p % kRX, ly = (p / kRX) % kRY, lz = p / (kRX * kRY);
+    const int ph = stage_pos<kPairs>(lx, ly, lz);
     // interior, unwrapped positions carry the brick's own ids
     const bool inner = lx >= 1 && lx <= kBX && ly >= 1 && ly <= kBY && lz >= 1 && lz <= kBZ && x0 + lx - 1 < r &&
                        y0 + ly - 1 < r && z0 + lz - 1 < r;
@@ -358,13 +377,13 @@ __device__ __forceinline__ void stage_brick(BrickShared<TS, TB>& S, const BrickV
 #pragma unroll
       for (int q = 0; q < 18; ++q) {
         if constexpr (sizeof(TS) == sizeof(TG))
-          cp_async<sizeof(TS)>(&S.xs[xs_index<TS, kPairs>(q, p)], src + q * 32);
+          cp_async<sizeof(TS)>(&S.xs[xs_index<TS, kPairs>(q, ph)], src + q * 32);
         else
-          cp_async<sizeof(TG)>(reinterpret_cast<TG*>(&S.xs[xs_index<TS, kPairs>(q, p)]) + 1, src + q * 32);
+          cp_async<sizeof(TG)>(reinterpret_cast<TG*>(&S.xs[xs_index<TS, kPairs>(q, ph)]) + 1, src + q * 32);
       }
     } else {
 #pragma unroll
-      for (int q = 0; q < 18; ++q) S.xs[xs_index<TS, kPairs>(q, p)] = TS(0);
+      for (int q = 0; q < 18; ++q) S.xs[xs_index<TS, kPairs>(q, ph)] = TS(0);
     }
   }
   cp_async_commit();
@@ -428,8 +447,10 @@ __global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const Apply
     const TV ridge = static_cast<TV>(st->ridge);
     const int pc = S.pc[threadIdx.x];
     const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
+    constexpr bool kPairs = sizeof(TZ) == 4 && sizeof(TV) == 4;  // the layout of stage_brick
+    const int ph = stage_pos<kPairs>(lx, ly, lz);
     TV y[18];
-    brick_gather<TV, TZ>(y, S.xs, S.bs, pc, lz * (kEX * kEY) + ly * kEX + lx);
+    brick_gather<TV, TZ>(y, S.xs, S.bs, pc, kRowStep * ly + lx, lz, lz * (kEX * kEY) + ly * kEX + lx);
     TV* __restrict__ pg = A.p + ob;
     TV* __restrict__ qg = A.q + ob;
     TV pv[18], qv[18];
@@ -441,8 +462,7 @@ __global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const Apply
 #pragma unroll
     for (int q = 0; q < 18; ++q) {
       const int s = q % 6;
-      // (the staged layout of stage_brick: load-case pairs iff all-FP32)
-      const TV zq = static_cast<TV>(S.xs[xs_index<TZ, sizeof(TZ) == 4 && sizeof(TV) == 4>(q, pc)]);
+      const TV zq = static_cast<TV>(S.xs[xs_index<TZ, kPairs>(q, ph)]);
       const TV w = idx == 0 ? TV(0) : fma_t(ridge, zq, y[q]);  // node 0 (id 0) pinned
       TV pn = TV(0), qn = TV(0);
       if (!st->done[s]) {
@@ -502,15 +522,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (valid) {
     const int pc = S.pc[threadIdx.x];
     const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
+    const int ph = stage_pos<sizeof(TV) == 4>(lx, ly, lz);
     TV y[18];
-    brick_gather<TV>(y, S.xs, S.bs, pc, lz * (kEX * kEY) + ly * kEX + lx);
+    brick_gather<TV>(y, S.xs, S.bs, pc, kRowStep * ly + lx, lz, lz * (kEX * kEY) + ly * kEX + lx);
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       TV res[3], xo[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const int q = c * 6 + s;
-        const TV xi = S.xs[xs_index<TV>(q, pc)];
+        const TV xi = S.xs[xs_index<TV>(q, ph)];
         const TV wv = idx == 0 ? TV(0) : fma_t(L.ridge, xi, y[q]);  // node 0 (id 0) pinned
         res[c] = static_cast<TV>(bv[q]) - wv;
         xo[c] = xi;
@@ -624,7 +645,7 @@ template <typename TB, typename TV, typename TO>
 void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, TO* xout, TV omega, int mode,
                         PcgState* st, double* partials, int init, cudaStream_t s) {
   constexpr size_t smem = brick_smem_bytes<TV>();
-  constexpr int kMinB = sizeof(TV) == 8 ? 3 : 5;
+  constexpr int kMinB = sizeof(TV) == 8 ? 3 : 4;
   static const bool configured = brick_configure(brick_sweep_kernel<TB, TV, TO, kMinB>, smem);
   (void)configured;
   launch_pdl(brick_sweep_kernel<TB, TV, TO, kMinB>, L.bricks.nab, kThreads, smem, s, L, b, xin, xout, omega, mode,

@@ -193,8 +193,8 @@ __global__ void scatter_kernel(const int* __restrict__ flag, const int* __restri
 }
 
 // ---- brick-major level-0 node numbering (brick.cuh) -------------------------
-// Padded brick-major index p = brick * 256 + (lz*8 + ly)*8 + lx over
-// ceil(r/8) x ceil(r/8) x ceil(r/4) bricks of 8x8x4 nodes; positions outside
+// Padded brick-major index p = brick * 128 + (lz*4 + ly)*8 + lx over
+// ceil(r/8) x ceil(r/4) x ceil(r/4) bricks of 8x4x4 nodes; positions outside
 // the torus (ragged last bricks) are never active.
 constexpr int kBrickX = 8, kBrickY = 4, kBrickZ = 4, kBrickN = kBrickX * kBrickY * kBrickZ;
 
