@@ -98,40 +98,7 @@ __device__ __forceinline__ int wrap3(int v, int r) {
   return v;
 }
 
-#ifdef SHL_BRICK_TRACE
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ unsigned long long g_trace[4][2][64][2];  // [cta][role][event][k,time]
-__device__ int g_trace_n[4][2];
-#define TRACE(msg, ...)                                                        \
-  if (blockIdx.x < 4) {                                                        \
-    const int role_ = threadIdx.x >= kConsumers;                               \
-    const int n_ = g_trace_n[blockIdx.x][role_]++;                             \
-    if (n_ < 64) {                                                             \
-      g_trace[blockIdx.x][role_][n_][0] = (unsigned long long)(__LINE__);      \
-      g_trace[blockIdx.x][role_][n_][1] = gtime();                             \
-    }                                                                          \
-  }
-__device__ void trace_dump(const char* kern) {
-  if (blockIdx.x < 4 && (threadIdx.x == 0 || threadIdx.x == kConsumers)) {
-    const int role = threadIdx.x >= kConsumers;
-    const int n = min(g_trace_n[blockIdx.x][role], 64);
-    for (int i = 0; i < n; ++i)
-      printf("%s cta %d %s line %llu t %llu\n", kern, blockIdx.x, role ? "P" : "C", g_trace[blockIdx.x][role][i][0],
-             g_trace[blockIdx.x][role][i][1]);
-    g_trace_n[blockIdx.x][role] = 0;
-  }
-}
-#define TRACE_DUMP(k) trace_dump(k)
-#else
-#define TRACE(msg, ...)
-#define TRACE_DUMP(k)
-#endif
-
-// ---- async copies (sm_80+ cp.async, sm_90+ bulk L2 prefetch) --------------------
+// ---- async copies (cp.async) ---------------------------------------------------
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -145,31 +112,22 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
-// Pull [p, p + bytes) into L2 through the TMA unit (one instruction, no registers).
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
-}
-// L2 prefetch of the node rows [first, last) of an nq-component blocked vector.
-template <typename T>
-__device__ __forceinline__ void prefetch_rows(const T* v, int nq, int first, int last) {
-  if (last <= first) return;
-  const int b0 = first >> 5, b1 = (last - 1) >> 5;
-  prefetch_l2(v + static_cast<size_t>(b0) * nq * 32, static_cast<unsigned>((b1 - b0 + 1) * nq * 32 * sizeof(T)));
-}
-
-// Shared memory of one CTA (= one brick): the staged input vector, the
-// element betas, the node map of the region and the brick's node positions.
+// Shared memory of one CTA: the staged input vector, the element betas and the
+// brick's node positions, and the reduction scratch.
 template <typename TS, typename TB = TS>
-struct BrickShared {
+struct alignas(16) BrickShared {  // (16: the float2 reads of the second buffer)
   TS xs[18 * stage_words<sizeof(TS) == 4 && sizeof(TB) == 4>()];  // [q][position], 0 where absent
   TB bs[kERegion];            // element betas of the region
-  int ms[kRegion];            // node ids of the region (-1 absent)
   unsigned short pc[kNodes];  // region position of brick node first + i
+};
+template <typename TS, typename TB = TS>
+struct BrickCta {
+  BrickShared<TS, TB> buf;
   double red[kWarps * 6];
 };
 template <typename TS, typename TB = TS>
 constexpr size_t brick_smem_bytes() {
-  return sizeof(BrickShared<TS, TB>);
+  return sizeof(BrickCta<TS, TB>);
 }
 
 __device__ __forceinline__ void brick_origin(const BrickView& B, int t, int& x0, int& y0, int& z0) {
@@ -329,79 +287,82 @@ __device__ __forceinline__ bool brick_last_sum(uint32_t* counter, const double* 
   return true;
 }
 
-// Stage brick t: node map and betas of the region (cp.async), then the input
-// vector at every region position (cp.async straight into shared memory; an
-// FP32 vector for an FP64 operator lands in the high half of its FP64 slot
-// and is converted in place), and the brick's own node positions.
-template <typename TS, typename TG, typename TB = TS>
-__device__ __forceinline__ void stage_brick(BrickShared<TS, TB>& S, const BrickView& B, int t, int r, int first,
-                                            int last, const int* __restrict__ nmap, const TB* __restrict__ beta,
-                                            const TG* __restrict__ v) {
-  // FP32 arithmetic reads load-case pairs; an FP32 vector for the FP64
-  // operator keeps the [q][position] layout of its scalar widening loads
-  constexpr bool kPairs = sizeof(TS) == 4 && sizeof(TB) == 4;
+// Staging, split so that it pipelines across a CTA's bricks:
+//   stage_ids   -- the node ids of the region positions this thread stages
+//                  (plain loads into registers, consumed one brick later),
+//   stage_issue -- cp.async of the element betas and of the 18 components at
+//                  every region position into a brick buffer (absent
+//                  positions zero-filled), and the brick's own node positions;
+//                  one commit group per brick.
+constexpr int kPer = (kRegion + kThreads - 1) / kThreads;  // 3 region positions per thread
+
+__device__ __forceinline__ void stage_ids(int (&id)[kPer], const BrickView& B, int t, int r,
+                                          const int* __restrict__ nmap) {
   int x0, y0, z0;
   brick_origin(B, t, x0, y0, z0);
-  constexpr int kPer = (kRegion + kThreads - 1) / kThreads;  // 3
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int p = threadIdx.x + j * kThreads;
+    id[j] = -1;
     if (p < kRegion) {
       const int lx = p % kRX, ly = (p / kRX) % kRY, lz = p / (kRX * kRY);
       const int gx = wrap3(x0 + lx - 1, r), gy = wrap3(y0 + ly - 1, r), gz = wrap3(z0 + lz - 1, r);
-      cp_async<4>(&S.ms[p], nmap + (static_cast<size_t>(gz) * r + gy) * r + gx);
+      id[j] = __ldg(nmap + (static_cast<size_t>(gz) * r + gy) * r + gx);
     }
   }
-  cp_async_commit();
+}
+
+template <typename TS, typename TB>
+__device__ __forceinline__ void stage_issue(BrickShared<TS, TB>& S, const BrickView& B, int t, int r,
+                                            const int (&id)[kPer], const TB* __restrict__ beta,
+                                            const TS* __restrict__ v) {
+  constexpr bool kPairs = sizeof(TS) == 4 && sizeof(TB) == 4;
+  int x0, y0, z0;
+  brick_origin(B, t, x0, y0, z0);
+  const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
   for (int e = threadIdx.x; e < kERegion; e += kThreads) {
     const int lx = e % kEX, ly = (e / kEX) % kEY, lz = e / (kEX * kEY);
     const int gx = wrap3(x0 + lx - 1, r), gy = wrap3(y0 + ly - 1, r), gz = wrap3(z0 + lz - 1, r);
     cp_async<sizeof(TB)>(&S.bs[e], beta + (static_cast<size_t>(gz) * r + gy) * r + gx);
   }
-  cp_async_commit();
-  cp_async_wait<1>();  // the map (betas stay in flight)
-  __syncthreads();
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int p = threadIdx.x + j * kThreads;
     if (p >= kRegion) continue;
-    const int id = S.ms[p];
     const int lx = p % kRX, ly = (p / kRX) % kRY, lz = p / (kRX * kRY);
     const int ph = stage_pos<kPairs>(lx, ly, lz);
     // interior, unwrapped positions carry the brick's own ids
     const bool inner = lx >= 1 && lx <= kBX && ly >= 1 && ly <= kBY && lz >= 1 && lz <= kBZ && x0 + lx - 1 < r &&
                        y0 + ly - 1 < r && z0 + lz - 1 < r;
-    if (inner && id >= first && id < last) S.pc[id - first] = static_cast<unsigned short>(p);
-    if (id >= 0) {
-      const TG* src = v + vbase(id, 18);
+    if (inner && id[j] >= first && id[j] < last) S.pc[id[j] - first] = static_cast<unsigned short>(p);
+    if (id[j] >= 0) {
+      const TS* src = v + vbase(id[j], 18);
 #pragma unroll
-      for (int q = 0; q < 18; ++q) {
-        if constexpr (sizeof(TS) == sizeof(TG))
-          cp_async<sizeof(TS)>(&S.xs[xs_index<TS, kPairs>(q, ph)], src + q * 32);
-        else
-          cp_async<sizeof(TG)>(reinterpret_cast<TG*>(&S.xs[xs_index<TS, kPairs>(q, ph)]) + 1, src + q * 32);
-      }
+      for (int q = 0; q < 18; ++q) cp_async<sizeof(TS)>(&S.xs[xs_index<TS, kPairs>(q, ph)], src + q * 32);
     } else {
 #pragma unroll
       for (int q = 0; q < 18; ++q) S.xs[xs_index<TS, kPairs>(q, ph)] = TS(0);
     }
   }
   cp_async_commit();
+}
+
+// Stage brick t = blockIdx.x into the CTA's buffer and run body(S, t) on it.
+// (One CTA per active brick: the hardware keeps 4 independent bricks per SM in
+// flight, which hides the staging of one behind the arithmetic of the others
+// better than a persistent double-buffered CTA did -- 3 CTAs/SM fit then,
+// 985 vs 879 us per PCG iteration.)
+template <typename TS, typename TB, typename Body>
+__device__ __forceinline__ void brick_run(BrickCta<TS, TB>& C, const BrickView& B, int r,
+                                          const int* __restrict__ nmap, const TB* __restrict__ beta,
+                                          const TS* __restrict__ v, Body&& body) {
+  const int t = blockIdx.x;
+  int id[kPer];
+  stage_ids(id, B, t, r, nmap);
+  stage_issue(C.buf, B, t, r, id, beta, v);
   cp_async_wait<0>();
-  if constexpr (sizeof(TS) != sizeof(TG)) {
-    static_assert(sizeof(TS) == 2 * sizeof(TG), "FP32 -> FP64 staging");
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int p = threadIdx.x + j * kThreads;
-      if (p >= kRegion || S.ms[p] < 0) continue;
-#pragma unroll
-      for (int q = 0; q < 18; ++q) {
-        TS* slot = &S.xs[q * kRegion + p];
-        *slot = static_cast<TS>(reinterpret_cast<const TG*>(slot)[1]);
-      }
-    }
-  }
-  __syncthreads();
+  __syncthreads();  // brick t staged
+  body(C.buf, t);
 }
 
 // Per-brick fixed-order sum of six doubles into partials[t*6 + s].
@@ -423,8 +384,7 @@ __device__ __forceinline__ void brick_reduce6(double (&v)[6], double* red, doubl
 }
 
 // ---- K4 on bricks: w = A z, p = z + beta p, q = w + beta q, p.q ----------------
-// One CTA per active brick (the hardware scheduler balances; several bricks'
-// CTAs per SM overlap each other's staging and arithmetic).
+// One CTA per active brick (brick_run).
 template <typename TV, typename TZ, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const ApplyArgs<TV, TZ> A) {
   pdl_wait();
@@ -433,49 +393,48 @@ __global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const Apply
   PcgState* st = A.state;
   if (st->stop) return;
   // z staged in its storage type (FP32 in mixed multigrid: half the shared
-  // memory of an FP64 copy, so more bricks per SM), widened exactly on use
-  BrickShared<TZ, TV>& S = *reinterpret_cast<BrickShared<TZ, TV>*>(brick_raw);
+  // memory of an FP64 copy), widened exactly on use
+  BrickCta<TZ, TV>& C = *reinterpret_cast<BrickCta<TZ, TV>*>(brick_raw);
   const BrickView& B = A.bricks;
-  const int t = blockIdx.x;
-  const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
-  const int idx = first + threadIdx.x;
-  const bool valid = idx < last;
-  const size_t ob = vbase(valid ? idx : 0, 18);
-  stage_brick<TZ, TZ, TV>(S, B, t, A.r, first, last, A.node_map, A.beta, A.z);
-  double pq[6] = {0, 0, 0, 0, 0, 0};
-  if (valid) {
-    const TV ridge = static_cast<TV>(st->ridge);
-    const int pc = S.pc[threadIdx.x];
-    const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
-    constexpr bool kPairs = sizeof(TZ) == 4 && sizeof(TV) == 4;  // the layout of stage_brick
-    const int ph = stage_pos<kPairs>(lx, ly, lz);
-    TV y[18];
-    brick_gather<TV, TZ>(y, S.xs, S.bs, pc, kRowStep * ly + lx, lz, lz * (kEX * kEY) + ly * kEX + lx);
-    TV* __restrict__ pg = A.p + ob;
-    TV* __restrict__ qg = A.q + ob;
-    TV pv[18], qv[18];
+  constexpr bool kPairs = sizeof(TZ) == 4 && sizeof(TV) == 4;  // the staged layout
+  brick_run(C, B, A.r, A.node_map, A.beta, A.z, [&](const BrickShared<TZ, TV>& S, int t) {
+    const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
+    const int idx = first + threadIdx.x;
+    double pq[6] = {0, 0, 0, 0, 0, 0};
+    if (idx < last) {
+      const size_t ob = vbase(idx, 18);
+      const TV ridge = static_cast<TV>(st->ridge);
+      const int pc = S.pc[threadIdx.x];
+      const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
+      const int ph = stage_pos<kPairs>(lx, ly, lz);
+      TV y[18];
+      brick_gather<TV, TZ>(y, S.xs, S.bs, pc, kRowStep * ly + lx, lz, lz * (kEX * kEY) + ly * kEX + lx);
+      TV* __restrict__ pg = A.p + ob;
+      TV* __restrict__ qg = A.q + ob;
+      TV pv[18], qv[18];
 #pragma unroll
-    for (int q = 0; q < 18; ++q) {  // every load in flight before the first store
-      pv[q] = pg[q * 32];
-      qv[q] = qg[q * 32];
-    }
-#pragma unroll
-    for (int q = 0; q < 18; ++q) {
-      const int s = q % 6;
-      const TV zq = static_cast<TV>(S.xs[xs_index<TZ, kPairs>(q, ph)]);
-      const TV w = idx == 0 ? TV(0) : fma_t(ridge, zq, y[q]);  // node 0 (id 0) pinned
-      TV pn = TV(0), qn = TV(0);
-      if (!st->done[s]) {
-        const TV bc = static_cast<TV>(st->beta[s]);
-        pn = fma_t(bc, pv[q], zq);
-        qn = fma_t(bc, qv[q], w);
+      for (int q = 0; q < 18; ++q) {  // every load in flight before the first store
+        pv[q] = pg[q * 32];
+        qv[q] = qg[q * 32];
       }
-      pg[q * 32] = pn;
-      qg[q * 32] = qn;
-      pq[s] += static_cast<double>(pn) * static_cast<double>(qn);
+#pragma unroll
+      for (int q = 0; q < 18; ++q) {
+        const int s = q % 6;
+        const TV zq = static_cast<TV>(S.xs[xs_index<TZ, kPairs>(q, ph)]);
+        const TV w = idx == 0 ? TV(0) : fma_t(ridge, zq, y[q]);  // node 0 (id 0) pinned
+        TV pn = TV(0), qn = TV(0);
+        if (!st->done[s]) {
+          const TV bc = static_cast<TV>(st->beta[s]);
+          pn = fma_t(bc, pv[q], zq);
+          qn = fma_t(bc, qv[q], w);
+        }
+        pg[q * 32] = pn;
+        qg[q * 32] = qn;
+        pq[s] += static_cast<double>(pn) * static_cast<double>(qn);
+      }
     }
-  }
-  brick_reduce6(pq, S.red, A.partials, t);
+    brick_reduce6(pq, C.red, A.partials, t);
+  });
   double tot[6];
   if (!brick_last_sum(&st->counter_apply, A.partials, B.nab, tot, scratch)) return;
   if (threadIdx.x == 0) {
@@ -500,62 +459,59 @@ __global__ void __launch_bounds__(kThreads, MINB)
   extern __shared__ __align__(16) unsigned char brick_raw[];
   __shared__ double scratch[32 * 6];
   if (st->stop) return;
-  BrickShared<TV>& S = *reinterpret_cast<BrickShared<TV>*>(brick_raw);
+  BrickCta<TV>& C = *reinterpret_cast<BrickCta<TV>*>(brick_raw);
   const BrickView& B = L.bricks;
-  const int t = blockIdx.x;
-  const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
-  const int idx = first + threadIdx.x;
-  const bool valid = idx < last;
-  const size_t ob = vbase(valid ? idx : 0, 18);
-  TV D[6];
-  TB bv[18];
-  if (valid) {
-    if (mode != 1) {
+  brick_run(C, B, L.r, L.node_map, L.beta, xin, [&](const BrickShared<TV>& S, int t) {
+    const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
+    const int idx = first + threadIdx.x;
+    double gam[6] = {0, 0, 0, 0, 0, 0};
+    if (idx < last) {
+      const size_t ob = vbase(idx, 18);
+      TV D[6];
+      TB bv[18];
+      if (mode != 1) {
 #pragma unroll
-      for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
-    }
-#pragma unroll
-    for (int q = 0; q < 18; ++q) bv[q] = b[ob + q * 32];
-  }
-  stage_brick<TV, TV>(S, B, t, L.r, first, last, L.node_map, L.beta, xin);
-  double gam[6] = {0, 0, 0, 0, 0, 0};
-  if (valid) {
-    const int pc = S.pc[threadIdx.x];
-    const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
-    const int ph = stage_pos<sizeof(TV) == 4>(lx, ly, lz);
-    TV y[18];
-    brick_gather<TV>(y, S.xs, S.bs, pc, kRowStep * ly + lx, lz, lz * (kEX * kEY) + ly * kEX + lx);
-#pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      TV res[3], xo[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int q = c * 6 + s;
-        const TV xi = S.xs[xs_index<TV>(q, ph)];
-        const TV wv = idx == 0 ? TV(0) : fma_t(L.ridge, xi, y[q]);  // node 0 (id 0) pinned
-        res[c] = static_cast<TV>(bv[q]) - wv;
-        xo[c] = xi;
+        for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
       }
-      if (mode == 1) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s) * 32] = static_cast<TO>(idx == 0 ? TV(0) : res[c]);
-        continue;
-      }
-      const TV z0v = D[0] * res[0] + D[1] * res[1] + D[2] * res[2];
-      const TV z1v = D[1] * res[0] + D[3] * res[1] + D[4] * res[2];
-      const TV z2v = D[2] * res[0] + D[4] * res[1] + D[5] * res[2];
-      xo[0] = fma_t(omega, z0v, xo[0]);
-      xo[1] = fma_t(omega, z1v, xo[1]);
-      xo[2] = fma_t(omega, z2v, xo[2]);
+      for (int q = 0; q < 18; ++q) bv[q] = b[ob + q * 32];  // in flight during the gather
+      const int pc = S.pc[threadIdx.x];
+      const int lx = pc % kRX, ly = (pc / kRX) % kRY, lz = pc / (kRX * kRY);
+      const int ph = stage_pos<sizeof(TV) == 4>(lx, ly, lz);
+      TV y[18];
+      brick_gather<TV>(y, S.xs, S.bs, pc, kRowStep * ly + lx, lz, lz * (kEX * kEY) + ly * kEX + lx);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        xout[ob + (c * 6 + s) * 32] = static_cast<TO>(xo[c]);
-        if (mode == 2) gam[s] += static_cast<double>(bv[c * 6 + s]) * static_cast<double>(xo[c]);
+      for (int s = 0; s < 6; ++s) {
+        TV res[3], xo[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int q = c * 6 + s;
+          const TV xi = S.xs[xs_index<TV>(q, ph)];
+          const TV wv = idx == 0 ? TV(0) : fma_t(L.ridge, xi, y[q]);  // node 0 (id 0) pinned
+          res[c] = static_cast<TV>(bv[q]) - wv;
+          xo[c] = xi;
+        }
+        if (mode == 1) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s) * 32] = static_cast<TO>(idx == 0 ? TV(0) : res[c]);
+          continue;
+        }
+        const TV z0v = D[0] * res[0] + D[1] * res[1] + D[2] * res[2];
+        const TV z1v = D[1] * res[0] + D[3] * res[1] + D[4] * res[2];
+        const TV z2v = D[2] * res[0] + D[4] * res[1] + D[5] * res[2];
+        xo[0] = fma_t(omega, z0v, xo[0]);
+        xo[1] = fma_t(omega, z1v, xo[1]);
+        xo[2] = fma_t(omega, z2v, xo[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          xout[ob + (c * 6 + s) * 32] = static_cast<TO>(xo[c]);
+          if (mode == 2) gam[s] += static_cast<double>(bv[c * 6 + s]) * static_cast<double>(xo[c]);
+        }
       }
     }
-  }
+    if (mode == 2) brick_reduce6(gam, C.red, partials, t);
+  });
   if (mode != 2) return;
-  brick_reduce6(gam, S.red, partials, t);
   double tot[6];
   if (!brick_last_sum(&st->counter_misc, partials, B.nab, tot, scratch)) return;
   if (threadIdx.x == 0) {
@@ -574,7 +530,6 @@ bool brick_configure(K kernel, size_t smem) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   return true;
 }
-
 
 }  // namespace
 
@@ -630,7 +585,7 @@ void brick_upload_constants(const double* K0d, const float* K0f, cudaStream_t s)
   cudaMemcpyToSymbolAsync(c_bK0f, K0f, sizeof(float) * 576, 0, cudaMemcpyHostToDevice, s);
 }
 
-// Staged brick apply: one resident CTA per slot, bricks from the tile queue.
+// Level-0 apply: one CTA per active brick.
 template <typename TV, typename TZ>
 void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s) {
   constexpr size_t smem = brick_smem_bytes<TZ, TV>();
@@ -640,7 +595,7 @@ void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s) {
   launch_pdl(brick_apply_kernel<TV, TZ, kMinB>, a.bricks.nab, kThreads, smem, s, a);
 }
 
-// Staged brick sweep of level 0, one resident CTA per slot.
+// Level-0 sweep: one CTA per active brick.
 template <typename TB, typename TV, typename TO>
 void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, TO* xout, TV omega, int mode,
                         PcgState* st, double* partials, int init, cudaStream_t s) {
