@@ -320,19 +320,28 @@ __global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c
   const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
   TV acc[3] = {TV(0), TV(0), TV(0)};
   if (G != 0) {
-    for (int dk = -1; dk <= 1; ++dk)
-      for (int dj = -1; dj <= 1; ++dj)
-        for (int di = -1; di <= 1; ++di) {
-          const int fi = (2 * I + di + r_f) % r_f, fj = (2 * J + dj + r_f) % r_f,
-                    fk = (2 * K + dk + r_f) % r_f;
-          const int nf = map_f[(static_cast<size_t>(fk) * r_f + fj) * r_f + fi];
-          if (nf < 0) continue;
-          const TV w = TV((di ? 0.5 : 1.0) * (dj ? 0.5 : 1.0) * (dk ? 0.5 : 1.0));
-          const size_t o = vbase(nf, 18) + s * 32;
-          acc[0] = fma_t(w, res_f[o], acc[0]);
-          acc[1] = fma_t(w, res_f[o + 192], acc[1]);
-          acc[2] = fma_t(w, res_f[o + 384], acc[2]);
-        }
+    // the 27 map lookups first (all in flight at once), then the gathers
+    int fx[3], fy[3], fz[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      fx[d] = (2 * I + d - 1 + r_f) % r_f;
+      fy[d] = (2 * J + d - 1 + r_f) % r_f;
+      fz[d] = (2 * K + d - 1 + r_f) % r_f;
+    }
+    int nf[27];
+#pragma unroll
+    for (int m = 0; m < 27; ++m)
+      nf[m] = map_f[(static_cast<size_t>(fz[m / 9]) * r_f + fy[(m / 3) % 3]) * r_f + fx[m % 3]];
+#pragma unroll
+    for (int m = 0; m < 27; ++m) {
+      if (nf[m] < 0) continue;
+      const int di = m % 3 - 1, dj = (m / 3) % 3 - 1, dk = m / 9 - 1;
+      const TV w = TV((di ? 0.5 : 1.0) * (dj ? 0.5 : 1.0) * (dk ? 0.5 : 1.0));
+      const size_t o = vbase(nf[m], 18) + s * 32;
+      acc[0] = fma_t(w, res_f[o], acc[0]);
+      acc[1] = fma_t(w, res_f[o + 192], acc[1]);
+      acc[2] = fma_t(w, res_f[o + 384], acc[2]);
+    }
   }
   const size_t oc = vbase(idx, 18) + s * 32;
   b_c[oc] = acc[0];
@@ -381,15 +390,18 @@ __global__ void restrict_slab_kernel(const int* __restrict__ list_c, int n_c, in
   b_c[oc + 384] += acc[2];
 }
 
-// x_f(n) += sum_N w(n,N) x_c(N) over the 1..8 coarse parents of n
+// x_f(n) += sum_N w(n,N) x_c(N) over the 1..8 coarse parents of n.  One
+// thread per fine node and all 18 components: the parent lookup (two integer
+// divisions and up to 8 dependent map loads) is done once per node, not once
+// per load case.
 template <typename TV>
-__global__ void prolong_kernel(const int* __restrict__ list_f, int n_f, int r_f,
-                               const int* __restrict__ map_c, int r_c, const TV* __restrict__ x_c,
-                               TV* __restrict__ x_f, const PcgState* st) {
+__global__ void __launch_bounds__(128) prolong_kernel(const int* __restrict__ list_f, int n_f, int r_f,
+                                                      const int* __restrict__ map_c, int r_c,
+                                                      const TV* __restrict__ x_c, TV* __restrict__ x_f,
+                                                      const PcgState* st) {
   pdl_wait();
   if (st->stop) return;
-  int idx, s;
-  node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_f) return;
   const int g = list_f[idx];
   if (g == 0) return;
@@ -397,22 +409,29 @@ __global__ void prolong_kernel(const int* __restrict__ list_f, int n_f, int r_f,
   const int pi[2] = {i >> 1, ((i + 1) >> 1) % r_c}, pj[2] = {j >> 1, ((j + 1) >> 1) % r_c},
             pk[2] = {k >> 1, ((k + 1) >> 1) % r_c};
   const int ni = (i & 1) ? 2 : 1, nj = (j & 1) ? 2 : 1, nk = (k & 1) ? 2 : 1;
+  int nc[8];  // parents in (c, b, a) order, -1 where absent
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int a = u & 1, b = (u >> 1) & 1, c = u >> 2;
+    nc[u] = (a < ni && b < nj && c < nk) ? map_c[(static_cast<size_t>(pk[c]) * r_c + pj[b]) * r_c + pi[a]] : -1;
+  }
   const TV w = TV(1.0 / (ni * nj * nk));
-  TV acc[3] = {TV(0), TV(0), TV(0)};
-  for (int c = 0; c < nk; ++c)
-    for (int b = 0; b < nj; ++b)
-      for (int a = 0; a < ni; ++a) {
-        const int nc = map_c[(static_cast<size_t>(pk[c]) * r_c + pj[b]) * r_c + pi[a]];
-        if (nc < 0) continue;
-        const size_t o = vbase(nc, 18) + s * 32;
-        acc[0] += x_c[o];
-        acc[1] += x_c[o + 192];
-        acc[2] += x_c[o + 384];
-      }
-  const size_t of = vbase(idx, 18) + s * 32;
-  x_f[of] = fma_t(w, acc[0], x_f[of]);
-  x_f[of + 192] = fma_t(w, acc[1], x_f[of + 192]);
-  x_f[of + 384] = fma_t(w, acc[2], x_f[of + 384]);
+  const size_t of = vbase(idx, 18);
+  TV acc[18], xf[18];
+#pragma unroll
+  for (int q = 0; q < 18; ++q) {
+    acc[q] = TV(0);
+    xf[q] = x_f[of + q * 32];
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    if (nc[u] < 0) continue;
+    const size_t o = vbase(nc[u], 18);
+#pragma unroll
+    for (int q = 0; q < 18; ++q) acc[q] += x_c[o + q * 32];
+  }
+#pragma unroll
+  for (int q = 0; q < 18; ++q) x_f[of + q * 32] = fma_t(w, acc[q], xf[q]);
 }
 
 // ---------------------------------------------------------------- setup
@@ -729,7 +748,7 @@ template <typename TV>
 void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
                     const PcgState* st, cudaStream_t s) {
   if (F.n)
-    launch_pdl(prolong_kernel<TV>, node_case_blocks(F.n, 192), 192, 0, s, F.node_list, F.n, F.r, C.node_map, C.r, x_c,
+    launch_pdl(prolong_kernel<TV>, (F.n + 127) / 128, 128, 0, s, F.node_list, F.n, F.r, C.node_map, C.r, x_c,
                x_f, st);
 }
 
