@@ -284,6 +284,177 @@ __global__ void __launch_bounds__(256) coarse_warp_sweep_kernel(const LevelArgs<
   coarse_warp_node<TV>(L, b, xin, xout, omega, mode, warp, lane);
 }
 
+// ---- coarsest level (8^3 torus) as one thread-block cluster ---------------------
+// The coarsest solve is jacobi_first + (sweeps - 1) damped block-Jacobi sweeps
+// over <= 512 nodes: as separate launches each sweep costs a launch and a
+// grid-wide dependency for ~6 us of latency (about 10% of a PCG iteration at
+// 128^3).  Here one cluster of 8 CTAs runs them all: CTA c owns z-plane c,
+// keeps its nodes' stencils (up to 64 x 243) in shared memory and its plane of
+// the iterate as a dense 8x8 plane (absent positions 0, so no node-map
+// lookups), double-buffered; each sweep starts with one cluster barrier and a
+// vectorized read of the two neighbour planes from the neighbours' shared
+// memory (distributed shared memory).  Same arithmetic as jacobi_first +
+// coarse_warp_sweep_kernel (mode 0) up to the summation order of the 27
+// neighbour blocks.
+constexpr int kCoR = 8;                // coarsest grid (nodes per axis) this kernel takes
+constexpr int kCoP = kCoR * kCoR;      // positions per plane
+constexpr int kCoThreads = 3 * kCoP;   // (node, neighbour plane) per thread
+constexpr int kCoPlane = 9 * kCoP;     // float2 per plane: [component][load-case pair][position]
+struct CoarsestShared {
+  float S[kStencil][kCoP];             // own nodes' stencils [m*9 + q][local node]
+  float2 own[2][kCoPlane];             // own plane c, double-buffered
+  float2 nb[2][kCoPlane];              // copies of planes c-1 and c+1 for the current sweep
+  float part[3][18][kCoP];             // per-neighbour-plane partial A x
+  float b[18][kCoP];
+  float D[6][kCoP];
+  short pos[kCoP];                     // position of local node u in its plane
+  int range[2];                        // own id range [lo, hi)
+};
+
+__global__ void __cluster_dims__(kCoR, 1, 1) __launch_bounds__(kCoThreads, 1)
+    coarsest_cluster_kernel(const int* __restrict__ node_list, int n, const float* __restrict__ stencil,
+                            const float* __restrict__ dinv, const float* __restrict__ b, float* __restrict__ x,
+                            float omega, int sweeps, const PcgState* st) {
+  namespace cg = cooperative_groups;
+  pdl_wait();
+  if (st->stop) return;  // (uniform: every CTA of the cluster returns)
+  extern __shared__ __align__(16) unsigned char co_raw[];
+  CoarsestShared& C = *reinterpret_cast<CoarsestShared*>(co_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = static_cast<int>(cl.block_rank()), tid = threadIdx.x;
+  // own id range: node ids are ordered by grid index, plane c = ids with g / 64 == c
+  if (tid < 2) C.range[tid] = 0;
+  for (int e = tid; e < 2 * kCoPlane; e += kCoThreads) (&C.own[0][0])[e] = make_float2(0.f, 0.f);
+  __syncthreads();
+  int below = 0, upto = 0;
+  for (int i = tid; i < n; i += kCoThreads) {
+    const int g = node_list[i];
+    below += g < c * kCoP;
+    upto += g < (c + 1) * kCoP;
+  }
+  if (below) atomicAdd(&C.range[0], below);
+  if (upto) atomicAdd(&C.range[1], upto);
+  __syncthreads();
+  const int lo = C.range[0], nl = C.range[1] - C.range[0];
+  // stage the own nodes' stencils, rhs and Dinv (cp.async: every load in flight at once)
+  for (int e = tid; e < kStencil * kCoP; e += kCoThreads) {
+    const int q = e / kCoP, u = e % kCoP;
+    if (u < nl)
+      cp_async<4>(&C.S[q][u], stencil + vbase(lo + u, kStencil) + q * 32);
+    else
+      C.S[q][u] = 0.f;
+  }
+  for (int e = tid; e < 18 * kCoP; e += kCoThreads) {
+    const int q = e / kCoP, u = e % kCoP;
+    if (u < nl)
+      cp_async<4>(&C.b[q][u], b + vbase(lo + u, 18) + q * 32);
+    else
+      C.b[q][u] = 0.f;
+  }
+  for (int e = tid; e < 6 * kCoP; e += kCoThreads) {
+    const int q = e / kCoP, u = e % kCoP;
+    if (u < nl)
+      cp_async<4>(&C.D[q][u], dinv + vbase(lo + u, 6) + q * 32);
+    else
+      C.D[q][u] = 0.f;
+  }
+  cp_async_commit();
+  if (tid < nl) C.pos[tid] = static_cast<short>(node_list[lo + tid] - c * kCoP);
+  cp_async_wait<0>();
+  __syncthreads();
+  const float4* own_lo = reinterpret_cast<const float4*>(cl.map_shared_rank(&C.own[0][0], (c + kCoR - 1) % kCoR));
+  const float4* own_hi = reinterpret_cast<const float4*>(cl.map_shared_rank(&C.own[0][0], (c + 1) % kCoR));
+  const bool pinned0 = c == 0 && nl > 0 && node_list[lo] == 0;  // node 0 stays 0
+  float* const ownf = reinterpret_cast<float*>(&C.own[0][0]);
+  // x_new of this thread's (node, load case) pairs into own[nb]
+  auto finish = [&](int nb, bool first) {
+    for (int k = tid; k < 6 * kCoP; k += kCoThreads) {
+      const int u = k % kCoP, s_ = k / kCoP;
+      if (u >= nl) continue;
+      const int ps = C.pos[u];
+      float xo[3];
+      if (first) {  // from x = 0: x = w Dinv b
+        const float r0 = C.b[s_][u], r1 = C.b[6 + s_][u], r2 = C.b[12 + s_][u];
+        xo[0] = omega * (C.D[0][u] * r0 + C.D[1][u] * r1 + C.D[2][u] * r2);
+        xo[1] = omega * (C.D[1][u] * r0 + C.D[3][u] * r1 + C.D[4][u] * r2);
+        xo[2] = omega * (C.D[2][u] * r0 + C.D[4][u] * r1 + C.D[5][u] * r2);
+      } else {
+        float res[3];
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          const int q = cc * 6 + s_;
+          res[cc] = C.b[q][u] - (C.part[0][q][u] + C.part[1][q][u] + C.part[2][q][u]);
+          xo[cc] = ownf[(((nb ^ 1) * 3 + cc) * 3 * kCoP + (s_ >> 1) * kCoP + ps) * 2 + (s_ & 1)];
+        }
+        xo[0] = fma_t(omega, C.D[0][u] * res[0] + C.D[1][u] * res[1] + C.D[2][u] * res[2], xo[0]);
+        xo[1] = fma_t(omega, C.D[1][u] * res[0] + C.D[3][u] * res[1] + C.D[4][u] * res[2], xo[1]);
+        xo[2] = fma_t(omega, C.D[2][u] * res[0] + C.D[4][u] * res[1] + C.D[5][u] * res[2], xo[2]);
+      }
+      if (pinned0 && u == 0) xo[0] = xo[1] = xo[2] = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        ownf[((nb * 3 + cc) * 3 * kCoP + (s_ >> 1) * kCoP + ps) * 2 + (s_ & 1)] = xo[cc];
+    }
+  };
+  finish(0, true);
+  const int pl = tid / kCoP, u = tid % kCoP;  // gather: neighbour plane pl (dz = pl - 1) of local node u
+  for (int k = 1; k < sweeps; ++k) {
+    const int cur = (k - 1) & 1;
+    cl.sync();  // every plane of sweep k-1 complete
+    {
+      float4* dst = reinterpret_cast<float4*>(&C.nb[0][0]);
+      constexpr int kV = kCoPlane / 2;  // float4 per plane
+      for (int e = tid; e < 2 * kV; e += kCoThreads)
+        dst[e] = e < kV ? own_lo[cur * kV + e] : own_hi[cur * kV + e - kV];
+    }
+    __syncthreads();
+    if (u < nl) {
+      const int ps = C.pos[u], i = ps % kCoR, j = ps / kCoR;
+      const float2* xp = pl == 1 ? C.own[cur] : C.nb[pl >> 1];
+      float2 y[9];  // [component][load-case pair], packed FFMA2 over the pair
+#pragma unroll
+      for (int q = 0; q < 9; ++q) y[q] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int mm = 0; mm < 9; ++mm) {
+        const int dx = mm % 3 - 1, dy = mm / 3 - 1, m = pl * 9 + mm;
+        const int np = ((i + dx + kCoR) % kCoR) + kCoR * ((j + dy + kCoR) % kCoR);
+        float Sv[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Sv[q] = C.S[m * 9 + q][u];
+#pragma unroll
+        for (int sp = 0; sp < 3; ++sp) {
+          const float2 x0 = xp[(0 * 3 + sp) * kCoP + np], x1 = xp[(1 * 3 + sp) * kCoP + np],
+                       x2 = xp[(2 * 3 + sp) * kCoP + np];
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) {
+            float2 v = y[cc * 3 + sp];
+            v = __ffma2_rn(make_float2(Sv[cc * 3 + 2], Sv[cc * 3 + 2]), x2, v);
+            v = __ffma2_rn(make_float2(Sv[cc * 3 + 1], Sv[cc * 3 + 1]), x1, v);
+            v = __ffma2_rn(make_float2(Sv[cc * 3 + 0], Sv[cc * 3 + 0]), x0, v);
+            y[cc * 3 + sp] = v;
+          }
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+        for (int sp = 0; sp < 3; ++sp) {
+          C.part[pl][cc * 6 + 2 * sp][u] = y[cc * 3 + sp].x;
+          C.part[pl][cc * 6 + 2 * sp + 1][u] = y[cc * 3 + sp].y;
+        }
+    }
+    __syncthreads();
+    finish(cur ^ 1, false);
+  }
+  __syncthreads();
+  const int fin = (sweeps - 1) & 1;
+  for (int k = tid; k < 18 * kCoP; k += kCoThreads) {
+    const int q = k / kCoP, uu = k % kCoP, cc = q / 6, s_ = q % 6;
+    if (uu < nl) x[vbase(lo + uu, 18) + q * 32] = ownf[((fin * 3 + cc) * 3 * kCoP + (s_ >> 1) * kCoP + C.pos[uu]) * 2 + (s_ & 1)];
+  }
+  cl.sync();  // no CTA leaves while a neighbour may still read its plane
+}
+
 // first sweep from x = 0: xout = w Dinv b (pointwise)
 template <typename TB, typename TV>
 __global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV* __restrict__ dinv,
@@ -728,6 +899,28 @@ void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV om
                omega, st);
 }
 
+// The coarsest solve (jacobi_first + sweeps - 1 sweeps) as one cluster
+// kernel when the level is the 8^3 torus in FP32; false otherwise (the caller
+// then launches the sweeps one by one).
+template <typename TV>
+bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* x, TV omega, int sweeps, const PcgState* st,
+                     cudaStream_t s) {
+  if constexpr (!std::is_same<TV, float>::value) {
+    return false;
+  } else {
+    if (L.r != kCoR || L.n > kCoR * kCoP || L.n == 0 || sweeps < 1) return false;
+    static const bool configured = [] {
+      cudaFuncSetAttribute(coarsest_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(CoarsestShared)));
+      return true;
+    }();
+    (void)configured;
+    launch_pdl(coarsest_cluster_kernel, kCoR, kCoThreads, sizeof(CoarsestShared), s, L.node_list, L.n, L.stencil,
+               L.dinv, b, x, omega, sweeps, st);
+    return true;
+  }
+}
+
 template <typename TV>
 void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
                      const PcgState* st, cudaStream_t s) {
@@ -760,6 +953,8 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
                                     const PcgState*, cudaStream_t);                                   \
   template void launch_prolong<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,   \
                                    const PcgState*, cudaStream_t);                                   \
+  template bool launch_coarsest<TV>(const GmgLevelView<TV>&, const TV*, TV*, TV, int, const PcgState*, \
+                                    cudaStream_t);                                                   \
   template void launch_restrict_slab<TV>(const GmgLevelView<TV>&, const int*, int, int, int, int, int,   \
                                          const TV*, TV*, const PcgState*, cudaStream_t);
 SHL_GMG_INST(float)

@@ -126,6 +126,10 @@ struct Vcycle {
                                         s);
       ++launches;
     };
+    if (l == L && l > 0 && shl::launch_coarsest<TV>(V, b[l], cur, w, gp.coarse_sweeps, st, s)) {
+      ++launches;
+      return cur;
+    }
     if (!fine) {
       shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, s);
       ++launches;

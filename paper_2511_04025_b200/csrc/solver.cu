@@ -21,6 +21,7 @@
 // Scalars never leave the device: the last block of each reduction kernel
 // (fixed-order sum of the per-block partials -> deterministic) updates the
 // PcgState, so the host only polls a flag every few iterations.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <condition_variable>

@@ -144,6 +144,11 @@ void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV om
 template <typename TV>
 void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
                      const PcgState* st, cudaStream_t s);
+// The whole coarsest-level solve in one cluster kernel (8^3 torus, FP32);
+// false when the level does not qualify.
+template <typename TV>
+bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* x, TV omega, int sweeps, const PcgState* st,
+                     cudaStream_t s);
 template <typename TV>
 void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
                     const PcgState* st, cudaStream_t s);
