@@ -362,8 +362,8 @@ def run_ours(args, rank, world, local):
     if gmg or apply_ms >= update_ms:
         # with multigrid, update_ms also holds the V-cycle; the apply stays the
         # largest single kernel of an iteration
-        kname = ("apply6_kernel (FP64 operator: w=A z gather + p,q update)" if vb == 8 else
-                 "apply_kernel (w=A z gather + p,q update)")
+        kname = ("brick_apply_kernel (FP64 operator w = A z on shared-memory-staged bricks + p,q update)"
+                 if vb == 8 else "brick_apply_kernel (w = A z on staged bricks + p,q update)")
         per_node, tot_ms = bytes_apply, apply_ms
     else:
         kname, per_node, tot_ms = "update_kernel (x,r,z update + dots)", bytes_update, update_ms

@@ -669,17 +669,41 @@ __device__ __forceinline__ const float* cell_matrices<float>() { return g_cellMf
 
 // block (32 coarse nodes, 27 stencil slots): thread (x, m) owns block m of node x,
 // so each stencil store is one coalesced 32-node line.
+// The 4x4x4 fine elements around each of the block's 32 coarse nodes are
+// staged in shared memory first (64 loads per node instead of 8 per shared
+// coarse element per slot thread).
+template <typename TV>
+struct GalerkinFineShared {
+  TV M[8 * 576];
+  TV B[32][64];  // [node][fine element (tz*4 + ty)*4 + tx], origin 2N - 2
+};
 template <typename TV>
 __global__ void __launch_bounds__(864) galerkin_fine_kernel(const int* __restrict__ list_c, int n_c, int r_c,
                                                             const int* __restrict__ map_f, int r_f,
                                                             const TV* __restrict__ betav, TV ridge,
                                                             TV* __restrict__ stencil_c) {
-  __shared__ TV M[8 * 576];
+  extern __shared__ __align__(16) unsigned char gf_raw[];
+  GalerkinFineShared<TV>& Sh = *reinterpret_cast<GalerkinFineShared<TV>*>(gf_raw);
+  TV* M = Sh.M;
   const TV* Mg = cell_matrices<TV>();
-  for (int t = threadIdx.y * 32 + threadIdx.x; t < 8 * 576; t += 864) M[t] = Mg[t];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int t = tid; t < 8 * 576; t += 864) M[t] = Mg[t];
+  for (int t = tid; t < 32 * 64; t += 864) {
+    const int x = t / 64, e = t % 64, id = blockIdx.x * 32 + x;
+    TV v = TV(0);
+    if (id < n_c) {
+      const int Gx = list_c[id];
+      const int I = Gx % r_c, J = (Gx / r_c) % r_c, K = Gx / (r_c * r_c);
+      const int ex = (2 * I - 2 + (e & 3) + r_f) % r_f, ey = (2 * J - 2 + ((e >> 2) & 3) + r_f) % r_f,
+                ez = (2 * K - 2 + (e >> 4) + r_f) % r_f;
+      v = betav[(static_cast<size_t>(ez) * r_f + ey) * r_f + ex];
+    }
+    Sh.B[x][e] = v;
+  }
   __syncthreads();
   const int idx = blockIdx.x * 32 + threadIdx.x;
   if (idx >= n_c) return;
+  const TV* Bn = Sh.B[threadIdx.x];
   const int m = threadIdx.y;
   const int Dx = m % 3 - 1, Dy = (m / 3) % 3 - 1, Dz = m / 9 - 1;
   const int G = list_c[idx];
@@ -692,19 +716,18 @@ __global__ void __launch_bounds__(864) galerkin_fine_kernel(const int* __restric
     for (int az = 0; az < 2; ++az) {
       const int bz = az + Dz;
       if (bz < 0 || bz > 1) continue;
-      const int cz = 2 * ((K - az + r_c) % r_c);
       for (int ay = 0; ay < 2; ++ay) {
         const int by = ay + Dy;
         if (by < 0 || by > 1) continue;
-        const int cy = 2 * ((J - ay + r_c) % r_c);
         for (int ax = 0; ax < 2; ++ax) {
           const int bx = ax + Dx;
           if (bx < 0 || bx > 1) continue;
-          const int cx = 2 * ((I - ax + r_c) % r_c);
           const int A = ax + 2 * ay + 4 * az, B = bx + 2 * by + 4 * bz;
+          // coarse element 2(N - a) = fine elements 2N - 2 + 2(1 - a) + child offset
+          const TV* Be = Bn + (2 * (1 - az)) * 16 + (2 * (1 - ay)) * 4 + 2 * (1 - ax);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const TV be = betav[(static_cast<size_t>(cz + (j >> 2)) * r_f + cy + ((j >> 1) & 1)) * r_f + cx + (j & 1)];
+            const TV be = Be[(j >> 2) * 16 + ((j >> 1) & 1) * 4 + (j & 1)];
             const TV* Mj = M + j * 576 + (3 * A) * 24 + 3 * B;
 #pragma unroll
             for (int c = 0; c < 3; ++c)
@@ -740,57 +763,94 @@ __global__ void __launch_bounds__(864) galerkin_fine_kernel(const int* __restric
 }
 
 // ---- Galerkin from a stored level ----------------------------------------
-// One warp per (coarse node N, stencil slot D); lane t < 27 owns fine node
-// n = 2N + off(t) of N's support and sums w(n,N) A_f(n,m) w(m,N+D) over the
-// fine stencil neighbours m of n inside supp(N+D); a butterfly sums the lanes.
+// A_c(N, N+D) = sum_{n in supp(N)} sum_{m in supp(N+D)} w(n,N) A_f(n,m) w(m,N+D).
+// One warp per coarse node N, lane t < 27 owns fine node n = 2N + off(t) of
+// N's support and reads each of its 27 fine blocks A_f(n, m) once, adding it
+// to every coarse slot D whose support holds m; the 27 slots are done one
+// z-plane (9 slots, 81 register accumulators) at a time and summed over the
+// lanes by a butterfly (fixed order -> reproducible).  8 consecutive coarse
+// nodes per CTA read overlapping fine stencils, which the L1 serves.
 template <typename TV>
 __global__ void __launch_bounds__(256) galerkin_stored_kernel(const int* __restrict__ list_c, int n_c, int r_c,
                                                               const int* __restrict__ map_f, int r_f,
                                                               const TV* __restrict__ stencil_f,
                                                               TV* __restrict__ stencil_c) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= n_c * 27) return;  // whole warps exit together
-  const int idx = warp / 27, slot = warp % 27;
-  const int Dx = slot % 3 - 1, Dy = (slot / 3) % 3 - 1, Dz = slot / 9 - 1;
+  const int idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (idx >= n_c) return;  // whole warps exit together
   const int G = list_c[idx];
-  TV S[9];
-#pragma unroll
-  for (int q = 0; q < 9; ++q) S[q] = TV(0);
+  const int nx = lane % 3 - 1, ny = (lane / 3) % 3 - 1, nz = lane / 9 - 1;
+  int fi = 0, fj = 0, fk = 0;
+  bool act = false;
+  const TV* sb = stencil_f;
   if (G != 0 && lane < 27) {
     const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
-    const int nx = lane % 3 - 1, ny = (lane / 3) % 3 - 1, nz = lane / 9 - 1;
-    const int fi = (2 * I + nx + r_f) % r_f, fj = (2 * J + ny + r_f) % r_f, fk = (2 * K + nz + r_f) % r_f;
+    fi = (2 * I + nx + r_f) % r_f;
+    fj = (2 * J + ny + r_f) % r_f;
+    fk = (2 * K + nz + r_f) % r_f;
     const size_t gn = (static_cast<size_t>(fk) * r_f + fj) * r_f + fi;
     const int nf = map_f[gn];
-    if (nf >= 0 && gn != 0) {
-      const TV wn = TV((nx ? 0.5 : 1.0) * (ny ? 0.5 : 1.0) * (nz ? 0.5 : 1.0));
-      const TV* sb = stencil_f + vbase(nf, kStencil);
+    act = nf >= 0 && gn != 0;
+    if (act) sb = stencil_f + vbase(nf, kStencil);
+  }
+  const TV wn = TV((nx ? 0.5 : 1.0) * (ny ? 0.5 : 1.0) * (nz ? 0.5 : 1.0));
+  auto w1 = [](int e) { return e == 0 ? TV(1) : TV(0.5); };
 #pragma unroll 1
+  for (int Dz = -1; Dz <= 1; ++Dz) {
+    TV S[9][9];  // [slot (Dy, Dx)][q]
+#pragma unroll
+    for (int d = 0; d < 9; ++d)
+#pragma unroll
+      for (int q = 0; q < 9; ++q) S[d][q] = TV(0);
+    if (act) {
+#pragma unroll
       for (int m = 0; m < 27; ++m) {
         const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-        // m relative to 2(N+D): must lie in [-1, 1] on every axis
-        const int ex = nx + dx - 2 * Dx, ey = ny + dy - 2 * Dy, ez = nz + dz - 2 * Dz;
-        if (ex < -1 || ex > 1 || ey < -1 || ey > 1 || ez < -1 || ez > 1) continue;
-        const int mi = (fi + dx + r_f) % r_f, mj = (fj + dy + r_f) % r_f, mk = (fk + dz + r_f) % r_f;
+        const int ez = nz + dz - 2 * Dz;  // m relative to 2(N+D) along z
+        if (ez < -1 || ez > 1) continue;
         // an inactive fine neighbour's block is exactly zero (no active element
         // couples to it on any level), so only the pinned node needs skipping
-        if (mi == 0 && mj == 0 && mk == 0) continue;
-        const TV w = wn * TV((ex ? 0.5 : 1.0) * (ey ? 0.5 : 1.0) * (ez ? 0.5 : 1.0));
+        if ((fi + dx + r_f) % r_f == 0 && (fj + dy + r_f) % r_f == 0 && (fk + dz + r_f) % r_f == 0) continue;
+        TV A[9];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) S[q] = fma_t(w, sb[(m * 9 + q) * 32], S[q]);
+        for (int q = 0; q < 9; ++q) A[q] = sb[(m * 9 + q) * 32];
+        const TV wz = wn * w1(ez);
+#pragma unroll
+        for (int Dy = -1; Dy <= 1; ++Dy) {
+          const int ey = ny + dy - 2 * Dy;
+          if (ey < -1 || ey > 1) continue;
+#pragma unroll
+          for (int Dx = -1; Dx <= 1; ++Dx) {
+            const int ex = nx + dx - 2 * Dx;
+            if (ex < -1 || ex > 1) continue;
+            const TV w = wz * w1(ey) * w1(ex);
+#pragma unroll
+            for (int q = 0; q < 9; ++q) S[(Dy + 1) * 3 + Dx + 1][q] = fma_t(w, A[q], S[(Dy + 1) * 3 + Dx + 1][q]);
+          }
+        }
       }
     }
-  }
 #pragma unroll
-  for (int q = 0; q < 9; ++q)
+    for (int d = 0; d < 9; ++d)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) S[q] += __shfl_xor_sync(0xffffffffu, S[q], o);
-  if (lane < 9) {
-    TV v = S[0];
+      for (int q = 0; q < 9; ++q) {
 #pragma unroll
-    for (int q = 1; q < 9; ++q)
-      if (lane == q) v = S[q];
-    stencil_c[vbase(idx, kStencil) + (slot * 9 + lane) * 32] = v;
+        for (int o = 16; o > 0; o >>= 1) S[d][q] += __shfl_xor_sync(0xffffffffu, S[d][q], o);
+      }
+    // lane d < 9 writes slot (Dz, d) -- the 9 values without dynamic register indexing
+    if (lane < 9) {
+      TV v[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) v[q] = S[0][q];
+#pragma unroll
+      for (int d = 1; d < 9; ++d)
+        if (lane == d) {
+#pragma unroll
+          for (int q = 0; q < 9; ++q) v[q] = S[d][q];
+        }
+      const int slot = (Dz + 1) * 9 + lane;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) stencil_c[vbase(idx, kStencil) + (slot * 9 + q) * 32] = v[q];
+    }
   }
 }
 
@@ -847,12 +907,17 @@ void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int 
                      const TV* beta_f, const TV* stencil_f, TV ridge, TV* stencil_c, cudaStream_t s) {
   if (n_c == 0) return;
   if (stencil_f == nullptr) {
-    galerkin_fine_kernel<TV><<<(n_c + 31) / 32, dim3(32, 27), 0, s>>>(list_c, n_c, r_c, map_f, r_f, beta_f, ridge,
-                                                                      stencil_c);
+    static const bool configured = [] {
+      cudaFuncSetAttribute(galerkin_fine_kernel<TV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(GalerkinFineShared<TV>)));
+      return true;
+    }();
+    (void)configured;
+    galerkin_fine_kernel<TV><<<(n_c + 31) / 32, dim3(32, 27), sizeof(GalerkinFineShared<TV>), s>>>(
+        list_c, n_c, r_c, map_f, r_f, beta_f, ridge, stencil_c);
   } else {
-    const long long threads = static_cast<long long>(n_c) * 27 * 32;
-    galerkin_stored_kernel<TV><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(list_c, n_c, r_c, map_f,
-                                                                                            r_f, stencil_f, stencil_c);
+    galerkin_stored_kernel<TV><<<static_cast<unsigned>((n_c + 7) / 8), 256, 0, s>>>(list_c, n_c, r_c, map_f, r_f,
+                                                                                     stencil_f, stencil_c);
   }
 }
 

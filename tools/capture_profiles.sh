@@ -13,6 +13,6 @@ ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --cs
     --log-file $O/${T}_launches.csv python tools/gmg_one.py --profiling > $O/${T}_launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'brick_apply_kernel' -c 2 \
     -o $O/${T}_apply -f python tools/gmg_one.py > $O/${T}_ncu_apply.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:'brick_sweep_kernel|update_kernel|field_samples_kernel|prolong_kernel' -c 8 \
+ncu --set full --clock-control none --import-source on -k regex:'brick_sweep_kernel|update_kernel|field_samples_kernel|prolong_kernel|restrict_kernel|coarsest_cluster_kernel|level_sweep3_kernel|coarse_warp_sweep_kernel' -c 14 \
     -o $O/${T}_kernels -f python tools/gmg_one.py > $O/${T}_ncu_kernels.log 2>&1
 echo done

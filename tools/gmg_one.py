@@ -15,4 +15,4 @@ d = S.random_design(S.RandomDesignSpec("cubic_octant", 8, 2, -1.0, 1.0), 1)
 opt = S.HomogenizeOptions(residual_tol=1e-5, precision="mixed", preconditioner="gmg")
 for _ in range(2):
     res = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, opt, ctx=ctx)
-print(list(res.iterations), res.timings, "components", res.stats.n_components, "floating", res.stats.n_floating)
+print(list(res.iterations), res.timings, "nodes", res.stats.n_nodes, "components", res.stats.n_components, "floating", res.stats.n_floating)
