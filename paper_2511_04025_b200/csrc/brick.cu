@@ -257,13 +257,9 @@ __device__ __forceinline__ void brick_gather(TS (&y)[18], const TX* __restrict__
 __device__ __forceinline__ bool brick_last_sum(uint32_t* counter, const double* partials, int nab, double (&tot)[6],
                                                double* scratch) {
   __shared__ bool last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  }
+  if (threadIdx.x == 0) last = arrive_last(counter);  // (thread 0 wrote the brick's partials)
   __syncthreads();
   if (!last) return false;
-  __threadfence();
 #pragma unroll
   for (int q = 0; q < 6; ++q) tot[q] = 0.0;
   for (int t = threadIdx.x; t < nab; t += blockDim.x)
@@ -361,11 +357,14 @@ __device__ __forceinline__ void brick_reduce6(double (&v)[6], double* red, doubl
     if (lane == 0) red[w * 6 + s] = v[s];
   }
   __syncthreads();
-  if (threadIdx.x < 6) {
-    double tot = 0.0;
+  if (threadIdx.x == 0) {  // (one thread: its writes are what brick_last_sum's release publishes)
 #pragma unroll
-    for (int u = 0; u < kWarps; ++u) tot += red[u * 6 + threadIdx.x];
-    partials[t * 6 + threadIdx.x] = tot;
+    for (int s = 0; s < 6; ++s) {
+      double tot = 0.0;
+#pragma unroll
+      for (int u = 0; u < kWarps; ++u) tot += red[u * 6 + s];
+      partials[t * 6 + s] = tot;
+    }
   }
 }
 

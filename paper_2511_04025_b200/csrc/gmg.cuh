@@ -176,13 +176,10 @@ __global__ void __launch_bounds__(192)
   tiles_done(&st->tile_next[1], &st->tile_done[1]);
   if (mode != 2) return;
   __shared__ bool last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(&st->counter_misc, 1u) == gridDim.x - 1;
-  }
+  __syncthreads();  // every thread's partial writes ordered before thread 0's release
+  if (threadIdx.x == 0) last = arrive_last(&st->counter_misc);
   __syncthreads();
   if (!last) return;
-  __threadfence();
   const int ntiles = (L.n + 63) / 64;
   double tot[6] = {0, 0, 0, 0, 0, 0};
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x)

@@ -99,6 +99,16 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
 
 // Writes this block's partial; returns true in exactly one block (the last to
 // finish), whose threads then see every partial.
+// Thread 0's arrival at a last-block counter: an acq_rel atomic at GPU scope
+// (release: this block's partials, ordered before it by the preceding
+// barrier; acquire: every other block's, for the last one) instead of a
+// sequentially consistent __threadfence() + atomicAdd.
+__device__ __forceinline__ bool arrive_last(uint32_t* counter) {
+  uint32_t t;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(counter) : "memory");
+  return t == gridDim.x - 1;
+}
+
 template <int NV>
 __device__ __forceinline__ bool publish_partial(const double (&v)[NV], double* partials,
                                                 uint32_t* counter) {
@@ -106,12 +116,9 @@ __device__ __forceinline__ bool publish_partial(const double (&v)[NV], double* p
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int q = 0; q < NV; ++q) partials[blockIdx.x * NV + q] = v[q];
-    __threadfence();
-    const uint32_t t = atomicAdd(counter, 1u);
-    last = (t == gridDim.x - 1);
+    last = arrive_last(counter);
   }
   __syncthreads();
-  if (last) __threadfence();
   return last;
 }
 

@@ -495,13 +495,10 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
   }
   tiles_done(&st->tile_next[0], &st->tile_done[0]);
   __shared__ bool last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(&st->counter_apply, 1u) == gridDim.x - 1;
-  }
+  __syncthreads();  // every thread's partial writes ordered before thread 0's release
+  if (threadIdx.x == 0) last = arrive_last(&st->counter_apply);
   __syncthreads();
   if (!last) return;
-  __threadfence();
   const int ntiles = (A.n + 32 * G - 1) / (32 * G);
   double tot[6] = {0, 0, 0, 0, 0, 0};
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
