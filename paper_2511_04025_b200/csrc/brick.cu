@@ -509,6 +509,120 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// ---- stored (Galerkin) levels on bricks ------------------------------------------
+// The coarse levels' 27-point 3x3-block stencils are stored (243 floats per
+// node); the per-node gather of the neighbours' 18 components was a chain of
+// dependent L2 loads (level_sweep3 / coarse_warp_sweep).  Here one CTA per
+// active 8x4x4-position brick of the level stages the iterate of the brick +
+// halo in shared memory (node map -> ids in registers, cp.async, the FP32
+// load-case-pair layout with swizzled rows of the level-0 sweeps) and each
+// thread owns one brick position: it streams its node's stencil (each warp
+// load is 4 row segments of consecutive grid-ordered ids) and gathers the
+// neighbours from shared memory.  mode 0: xout = xin + w Dinv (b - A xin);
+// mode 1: xout = b - A xin.  Node 0 (grid index 0) is pinned: output 0.
+struct alignas(16) StencilBrickShared {
+  float xs[18 * kPhys];
+};
+
+__global__ void __launch_bounds__(kThreads, 4)
+    stencil_brick_sweep_kernel(const GmgLevelView<float> L, const float* __restrict__ b,
+                               const float* __restrict__ xin, float* __restrict__ xout, float omega, int mode,
+                               const PcgState* st) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char sb_raw[];
+  if (st->stop) return;
+  StencilBrickShared& S = *reinterpret_cast<StencilBrickShared*>(sb_raw);
+  const BrickView& B = L.bricks;
+  const int t = blockIdx.x, tid = threadIdx.x, r = L.r;
+  int x0, y0, z0;
+  brick_origin(B, t, x0, y0, z0);
+  int id[kPer];
+  stage_ids(id, B, t, r, L.node_map);
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int p = tid + j * kThreads;
+    if (p >= kRegion) continue;
+    const int ph = stage_pos<true>(p % kRX, (p / kRX) % kRY, p / (kRX * kRY));
+    if (id[j] >= 0) {
+      const float* src = xin + vbase(id[j], 18);
+#pragma unroll
+      for (int q = 0; q < 18; ++q) cp_async<4>(&S.xs[xs_index<float, true>(q, ph)], src + q * 32);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 18; ++q) S.xs[xs_index<float, true>(q, ph)] = 0.f;
+    }
+  }
+  cp_async_commit();
+  // this thread's brick position and node (the map load overlaps the staging)
+  const int bx = tid & 7, by = (tid >> 3) & 3, bz = tid >> 5;
+  const int gx = x0 + bx, gy = y0 + by, gz = z0 + bz;
+  const int G = (gz * r + gy) * r + gx;
+  const int idx = __ldg(L.node_map + G);
+  cp_async_wait<0>();
+  __syncthreads();
+  if (idx < 0) return;  // (no barrier below)
+  const size_t ob = vbase(idx, 18);
+  if (G == 0) {  // pinned node
+#pragma unroll
+    for (int q = 0; q < 18; ++q) xout[ob + q * 32] = 0.f;
+    return;
+  }
+  const int lx = bx + 1, ly = by + 1, lz = bz + 1;
+  const int pxy = kRowStep * ly + lx;
+  const float* __restrict__ Sg = L.stencil + vbase(idx, 243);  // 27 x 3x3 blocks per node
+  const float2* __restrict__ x2 = reinterpret_cast<const float2*>(S.xs);
+  float2 acc[9];  // [c][load-case pair]
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll 3
+  for (int m = 0; m < 27; ++m) {
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
+    float Sm[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) Sm[q] = __ldg(Sg + (m * 9 + q) * 32);
+    const float2* xn = x2 + plane_base(lz + dz) + pxy + dy * kRowStep + dx;
+#pragma unroll
+    for (int sp = 0; sp < 3; ++sp) {
+      const float2 z0v = xn[(0 * 3 + sp) * kPhys], z1v = xn[(1 * 3 + sp) * kPhys], z2v = xn[(2 * 3 + sp) * kPhys];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float2 v = acc[c * 3 + sp];
+        v = __ffma2_rn(make_float2(Sm[c * 3 + 0], Sm[c * 3 + 0]), z0v, v);
+        v = __ffma2_rn(make_float2(Sm[c * 3 + 1], Sm[c * 3 + 1]), z1v, v);
+        v = __ffma2_rn(make_float2(Sm[c * 3 + 2], Sm[c * 3 + 2]), z2v, v);
+        acc[c * 3 + sp] = v;
+      }
+    }
+  }
+  float D[6];
+  if (mode != 1) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) D[q] = L.dinv[vbase(idx, 6) + q * 32];
+  }
+  const int ph = plane_base(lz) + pxy;
+#pragma unroll
+  for (int sp = 0; sp < 3; ++sp)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int s_ = 2 * sp + h;
+      float res[3], xo[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float y = h ? acc[c * 3 + sp].y : acc[c * 3 + sp].x;
+        res[c] = b[ob + (c * 6 + s_) * 32] - y;
+        xo[c] = S.xs[xs_index<float, true>(c * 6 + s_, ph)];
+      }
+      if (mode == 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xout[ob + (c * 6 + s_) * 32] = res[c];
+        continue;
+      }
+      xout[ob + (0 * 6 + s_) * 32] = fma_t(omega, D[0] * res[0] + D[1] * res[1] + D[2] * res[2], xo[0]);
+      xout[ob + (1 * 6 + s_) * 32] = fma_t(omega, D[1] * res[0] + D[3] * res[1] + D[4] * res[2], xo[1]);
+      xout[ob + (2 * 6 + s_) * 32] = fma_t(omega, D[2] * res[0] + D[4] * res[1] + D[5] * res[2], xo[2]);
+    }
+}
+
 // Opt a brick kernel into its dynamic shared memory (> 48 KB for FP64).
 template <typename K>
 bool brick_configure(K kernel, size_t smem) {
@@ -590,6 +704,15 @@ void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, T
   (void)configured;
   launch_pdl(brick_sweep_kernel<TB, TV, TO, kMinB>, L.bricks.nab, kThreads, smem, s, L, b, xin, xout, omega, mode,
              st, partials, init);
+}
+
+// Stored-level sweep on the level's active bricks (FP32 levels).
+void launch_stencil_brick_sweep(const GmgLevelView<float>& L, const float* b, const float* xin, float* xout,
+                                float omega, int mode, const PcgState* st, cudaStream_t s) {
+  static const bool configured = brick_configure(stencil_brick_sweep_kernel, sizeof(StencilBrickShared));
+  (void)configured;
+  launch_pdl(stencil_brick_sweep_kernel, L.bricks.nab, kThreads, sizeof(StencilBrickShared), s, L, b, xin, xout,
+             omega, mode, st);
 }
 
 template void launch_brick_apply<double, float>(const ApplyArgs<double, float>&, cudaStream_t);

@@ -154,6 +154,18 @@ struct shl_ctx {
   struct GmgLevel {
     int r = 0, n = 0, ld = 0;
     DevBuf flag, off, map, list, stencil, dinv, vec, scan_tmp;
+    DevBuf bflag, boff, blist;  // active 8x4x4 bricks (stencil_brick_sweep), r % 8 == 0 and r >= 16
+    int nab = 0;
+    shl::BrickView brick_view() const {
+      shl::BrickView v;
+      if (nab > 0) {
+        v.bcoord = blist.as<int>();
+        v.nab = nab;
+        v.nbx = r / 8;
+        v.nby = r / 4;
+      }
+      return v;
+    }
   };
   std::vector<GmgLevel> gmg;
   DevBuf gmg0;  // level-0 V-cycle work vectors (xa, xb, res)

@@ -603,6 +603,19 @@ __global__ void __launch_bounds__(128) prolong_kernel(const int* __restrict__ li
 }
 
 // ---------------------------------------------------------------- setup
+// brick (8x4x4 positions of a coarse level, r % 8 == 0, r % 4 == 0) active iff
+// one of its nodes is
+__global__ void coarse_brick_flag_kernel(const int* __restrict__ map, int r, int* __restrict__ flag) {
+  const int nbx = r / 8, nby = r / 4, nb = nbx * nby * (r / 4);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nb) return;
+  const int x0 = (t % nbx) * 8, y0 = ((t / nbx) % nby) * 4, z0 = (t / (nbx * nby)) * 4;
+  int any = 0;
+  for (int k = 0; k < 128 && !any; ++k)
+    any = map[(static_cast<size_t>(z0 + (k >> 5)) * r + y0 + ((k >> 3) & 3)) * r + x0 + (k & 7)] >= 0;
+  flag[t] = any;
+}
+
 // coarse node active iff a fine node of its support is active
 __global__ void coarse_flag_kernel(const int* __restrict__ map_f, int r_f, int r_c,
                                    int* __restrict__ flag_c) {
@@ -894,6 +907,11 @@ __global__ void coarse_dinv_kernel(const int* __restrict__ list_c, int n_c,
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
+void launch_coarse_brick_flags(const int* map, int r, int* flag, cudaStream_t s) {
+  const int nb = (r / 8) * (r / 4) * (r / 4);
+  coarse_brick_flag_kernel<<<(nb + 127) / 128, 128, 0, s>>>(map, r, flag);
+}
+
 void launch_coarse_flags(const int* map_f, int r_f, int r_c, int* flag_c, cudaStream_t s) {
   const size_t n3 = static_cast<size_t>(r_c) * r_c * r_c;
   coarse_flag_kernel<<<static_cast<unsigned>((n3 + 255) / 256), 256, 0, s>>>(map_f, r_f, r_c, flag_c);
@@ -930,6 +948,15 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
   if (fine && L.bricks.nab > 0) {
     launch_brick_sweep<TB, TV, TV>(L, b, xin, xout, omega, mode, st, partials, init, s);
     return;
+  }
+  if constexpr (std::is_same<TV, float>::value && std::is_same<TB, float>::value) {
+    // (at 64^3 and up the node-ordered level_sweep3 streams the stencils better:
+    //  61 vs 38 us at level 1 of 128^3; at 16^3 the warp-per-node sweep wins:
+    //  14 vs 10 us; at 32^3 the staged bricks: 20 vs 29 us)
+    if (!fine && L.bricks.nab > 0 && mode != 2 && L.n <= 32768 && L.r >= 32) {
+      launch_stencil_brick_sweep(L, b, xin, xout, omega, mode, st, s);
+      return;
+    }
   }
   LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
   if (fine) {

@@ -62,6 +62,24 @@ int gmg_setup(shl_ctx* c, const GmgParams& gp, TV ridge) {
                          c->stream));
       CK(cudaMemcpyAsync(&c->hlevels[2 * L + 1], Lv.flag.as<int>() + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost,
                          c->stream));
+      // active bricks of the level for the staged stored-level sweep (FP32; the
+      // sizes where it beats the node-ordered sweeps, launch_level_sweep: ~32^3)
+      c->hlevels[32 + 2 * L] = c->hlevels[32 + 2 * L + 1] = 0;
+      if (sizeof(TV) == 4 && rc % 8 == 0 && rc >= 32 && rc <= 40 && L < 16) {
+        const int nb = (rc / 8) * (rc / 4) * (rc / 4);
+        Lv.bflag.ensure(static_cast<size_t>(nb) * sizeof(int));
+        Lv.boff.ensure(static_cast<size_t>(nb) * sizeof(int));
+        Lv.blist.ensure(static_cast<size_t>(nb) * sizeof(int));
+        shl::launch_coarse_brick_flags(Lv.map.as<int>(), rc, Lv.bflag.as<int>(), c->stream);
+        shl::launch_exclusive_scan(Lv.bflag.as<int>(), Lv.boff.as<int>(), nb, Lv.scan_tmp.p, Lv.scan_tmp.cap,
+                                   c->stream);
+        shl::launch_scatter_compact(Lv.bflag.as<int>(), Lv.boff.as<int>(), nb, nullptr, Lv.blist.as<int>(),
+                                    c->stream);
+        CK(cudaMemcpyAsync(&c->hlevels[32 + 2 * L], Lv.boff.as<int>() + nb - 1, sizeof(int),
+                           cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&c->hlevels[32 + 2 * L + 1], Lv.bflag.as<int>() + nb - 1, sizeof(int),
+                           cudaMemcpyDeviceToHost, c->stream));
+      }
       Lv.r = rc;
       map_f = Lv.map.as<int>();
       rf = rc;
@@ -78,6 +96,7 @@ int gmg_setup(shl_ctx* c, const GmgParams& gp, TV ridge) {
     auto& Lv = c->gmg[l];
     const int rc = Lv.r;
     Lv.n = c->hlevels[2 * l] + c->hlevels[2 * l + 1];
+    Lv.nab = c->hlevels[32 + 2 * l] + c->hlevels[32 + 2 * l + 1];
     Lv.ld = round_up(Lv.n + 1, 32);
     Lv.stencil.ensure(static_cast<size_t>(243) * Lv.ld * sizeof(TV));
     Lv.dinv.ensure(static_cast<size_t>(6) * Lv.ld * sizeof(TV));

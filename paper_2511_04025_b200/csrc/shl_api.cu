@@ -350,6 +350,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
       auto& Lv = c->gmg[l];
       vc.view.push_back({Lv.list.as<int>(), Lv.map.as<int>(), nullptr, Lv.stencil.as<TZ>(), Lv.dinv.as<TZ>(),
                          Lv.r, Lv.n, Lv.n, TZ(0)});
+      vc.view.back().bricks = Lv.brick_view();
       TZ* v = Lv.vec.as<TZ>();
       const size_t s18 = static_cast<size_t>(18) * Lv.ld;
       vc.b.push_back(v);

@@ -178,6 +178,11 @@ template <typename TB, typename TV, typename TO>
 void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, TO* xout, TV omega, int mode,
                         PcgState* st, double* partials, int init, cudaStream_t s);
 void brick_upload_constants(const double* K0d, const float* K0f, cudaStream_t s);
+// stored (Galerkin) FP32 level, one CTA per active 8x4x4 brick (L.bricks: bcoord = active brick ids)
+void launch_stencil_brick_sweep(const GmgLevelView<float>& L, const float* b, const float* xin, float* xout,
+                                float omega, int mode, const PcgState* st, cudaStream_t s);
+// active 8x4x4 bricks of a coarse level's node map: flags, then (scan + compaction) their ids
+void launch_coarse_brick_flags(const int* map, int r, int* flag, cudaStream_t s);
 // Grid (block count) launch_apply / launch_level_sweep use for n nodes; the
 // caller sizes its partials buffer as 6 doubles per block.
 int apply_grid(int n, int num_sms);
