@@ -53,9 +53,9 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=16)
     p.add_argument("--warmup", type=int, default=4)
-    p.add_argument("--lanes", type=int, default=1,
-                   help="designs in flight at once per GPU (shl_set_batch_lanes); 1 = reproducible "
-                        "(2 lanes can fall into a contended mode, DESIGN.md 4.2)")
+    p.add_argument("--lanes", type=int, default=2,
+                   help="designs in flight at once per GPU (shl_set_batch_lanes); 2 fills the GPU's "
+                        "idle time inside one design's V-cycle (DESIGN.md 4.2); 1 = one design at a time")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--r", type=int, default=128)
     p.add_argument("--tol", type=float, default=1e-5)
