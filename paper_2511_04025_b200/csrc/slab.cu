@@ -24,6 +24,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <type_traits>
 #include <string>
@@ -103,10 +104,35 @@ struct SlabTransport {
   virtual ~SlabTransport() = default;
   virtual void allreduce(void* dev, size_t n, bool f64, cudaStream_t s) = 0;
   // send send_hi to rank+1 and send_lo to rank-1; receive recv_lo from rank-1
-  // and recv_hi from rank+1 (counts in values)
+  // and recv_hi from rank+1 (counts in values).  `during` enqueues work on s
+  // that needs none of the received planes (the interior apply): it is issued
+  // once the sends are in flight, so it overlaps the transfer; the received
+  // planes are ready on s when exchange returns.
   virtual void exchange(const void* send_hi, size_t n_send_hi, const void* send_lo, size_t n_send_lo,
                         void* recv_lo, size_t n_recv_lo, void* recv_hi, size_t n_recv_hi, bool f64,
-                        cudaStream_t s) = 0;
+                        cudaStream_t s, const std::function<void()>& during) = 0;
+  // true when exchange() and allreduce() only enqueue device work (capturable
+  // into a CUDA graph)
+  virtual bool capturable() const { return false; }
+};
+
+// A side stream for the transfers and the two events that fork it from / join
+// it to the solver's stream.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  SideStream() {
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  }
+  ~SideStream() {
+    if (join) cudaEventDestroy(join);
+    if (fork) cudaEventDestroy(fork);
+    if (s) cudaStreamDestroy(s);
+  }
+  SideStream(const SideStream&) = delete;
+  SideStream& operator=(const SideStream&) = delete;
 };
 
 struct NcclTransport : SlabTransport {
@@ -118,17 +144,27 @@ struct NcclTransport : SlabTransport {
   void allreduce(void* dev, size_t n, bool f64, cudaStream_t s) override {
     NK(nccl().AllReduce(dev, dev, n, f64 ? ncclFloat64 : ncclFloat32, ncclSum, comm->comm, s));
   }
+  // the ring send/recv runs on a side stream forked after the packs, the
+  // interior work on s beside it, and s joins the side stream before the unpack
   void exchange(const void* send_hi, size_t n_send_hi, const void* send_lo, size_t n_send_lo, void* recv_lo,
-                size_t n_recv_lo, void* recv_hi, size_t n_recv_hi, bool f64, cudaStream_t s) override {
+                size_t n_recv_lo, void* recv_hi, size_t n_recv_hi, bool f64, cudaStream_t s,
+                const std::function<void()>& during) override {
     const ncclDataType_t dt = f64 ? ncclFloat64 : ncclFloat32;
     const int lo = (rank - 1 + nranks) % nranks, hi = (rank + 1) % nranks;
+    CK(cudaEventRecord(side.fork, s));
+    CK(cudaStreamWaitEvent(side.s, side.fork, 0));
     NK(nccl().GroupStart());
-    NK(nccl().Send(send_hi, n_send_hi, dt, hi, comm->comm, s));
-    NK(nccl().Send(send_lo, n_send_lo, dt, lo, comm->comm, s));
-    NK(nccl().Recv(recv_lo, n_recv_lo, dt, lo, comm->comm, s));
-    NK(nccl().Recv(recv_hi, n_recv_hi, dt, hi, comm->comm, s));
+    NK(nccl().Send(send_hi, n_send_hi, dt, hi, comm->comm, side.s));
+    NK(nccl().Send(send_lo, n_send_lo, dt, lo, comm->comm, side.s));
+    NK(nccl().Recv(recv_lo, n_recv_lo, dt, lo, comm->comm, side.s));
+    NK(nccl().Recv(recv_hi, n_recv_hi, dt, hi, comm->comm, side.s));
     NK(nccl().GroupEnd());
+    if (during) during();
+    CK(cudaEventRecord(side.join, side.s));
+    CK(cudaStreamWaitEvent(s, side.join, 0));
   }
+  bool capturable() const override { return true; }
+  SideStream side;
 };
 
 struct HostTransport : SlabTransport {
@@ -160,21 +196,35 @@ struct HostTransport : SlabTransport {
       throw ShlError(SHL_IO, "z-slab transport: allreduce_sum callback failed");
     CK(cudaMemcpyAsync(dev, h, bytes, cudaMemcpyHostToDevice, s));
   }
+  // D2H of the packed planes on s, then the interior work is enqueued on s and
+  // the host waits for the D2H only (not for the interior work); the host
+  // round trip and the H2D (side stream) overlap the interior work, and s
+  // joins the side stream before the unpack
   void exchange(const void* send_hi, size_t n_send_hi, const void* send_lo, size_t n_send_lo, void* recv_lo,
-                size_t n_recv_lo, void* recv_hi, size_t n_recv_hi, bool f64, cudaStream_t s) override {
+                size_t n_recv_lo, void* recv_hi, size_t n_recv_hi, bool f64, cudaStream_t s,
+                const std::function<void()>& during) override {
     const size_t w = f64 ? 8 : 4;
     unsigned char* h = staging(w * (n_send_hi + n_send_lo + n_recv_lo + n_recv_hi));
     unsigned char *hs_hi = h, *hs_lo = hs_hi + w * n_send_hi, *hr_lo = hs_lo + w * n_send_lo,
                   *hr_hi = hr_lo + w * n_recv_lo;
     if (n_send_hi) CK(cudaMemcpyAsync(hs_hi, send_hi, w * n_send_hi, cudaMemcpyDeviceToHost, s));
     if (n_send_lo) CK(cudaMemcpyAsync(hs_lo, send_lo, w * n_send_lo, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(cudaEventRecord(side.fork, s));
+    if (during) during();
+    CK(cudaEventSynchronize(side.fork));
     if (cb.ring_exchange(cb.user, hs_hi, n_send_hi, hs_lo, n_send_lo, hr_lo, n_recv_lo, hr_hi, n_recv_hi,
                          f64 ? 1 : 0) != 0)
       throw ShlError(SHL_IO, "z-slab transport: ring_exchange callback failed");
-    if (n_recv_lo) CK(cudaMemcpyAsync(recv_lo, hr_lo, w * n_recv_lo, cudaMemcpyHostToDevice, s));
-    if (n_recv_hi) CK(cudaMemcpyAsync(recv_hi, hr_hi, w * n_recv_hi, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamWaitEvent(side.s, side.fork, 0));
+    if (n_recv_lo) CK(cudaMemcpyAsync(recv_lo, hr_lo, w * n_recv_lo, cudaMemcpyHostToDevice, side.s));
+    if (n_recv_hi) CK(cudaMemcpyAsync(recv_hi, hr_hi, w * n_recv_hi, cudaMemcpyHostToDevice, side.s));
+    CK(cudaEventRecord(side.join, side.s));
+    CK(cudaStreamWaitEvent(s, side.join, 0));
+    // (the pinned staging is reused by the next exchange / allreduce only after
+    // a host wait on s or side.s, so the H2D has finished reading it)
+    CK(cudaStreamSynchronize(side.s));
   }
+  SideStream side;
 };
 
 // ---------------------------------------------------------------- slab plan
@@ -233,6 +283,15 @@ __global__ void slab_map_kernel(const int* __restrict__ node_flag, const int* __
     list[id] = static_cast<int>(g);
   }
   map[t] = id;
+}
+
+// totals[6 s + q] = the slab's three apply ranges (low boundary plane,
+// interior, high boundary plane) summed in that fixed order
+__global__ void sum_ranges_kernel(const double* __restrict__ tr, double* __restrict__ totals, int nloc) {
+  const int t = threadIdx.x;
+  if (t >= 6 * nloc) return;
+  const int s = t / 6, q = t % 6;
+  totals[t] = (tr[(3 * s + 0) * 6 + q] + tr[(3 * s + 1) * 6 + q]) + tr[(3 * s + 2) * 6 + q];
 }
 
 }  // namespace
@@ -318,7 +377,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     max_plane = std::max({max_plane, P.n_glo, P.n_ghi, P.cnt_first, P.cnt_last});
   }
   DevBuf tot, xfer;
-  tot.ensure(sizeof(double) * 21 * nloc);
+  tot.ensure(sizeof(double) * (21 + 18) * nloc);  // totals + the apply's per-range sums
   xfer.ensure(4 * 18 * static_cast<size_t>(std::max(max_plane, 1)) * sizeof(double));
   c->state.ensure(sizeof(PcgState));
   c->cout.ensure(36 * sizeof(double));
@@ -394,10 +453,11 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     if (dist) comm->allreduce(totals, k, true, c->stream);
   };
   // ghost exchange of an 18-component vector (z each iteration, x for C^H)
-  auto exchange = [&](auto vec_of) {
+  auto exchange = [&](auto vec_of, const std::function<void()>& during = {}) {
     using T = std::remove_pointer_t<decltype(vec_of(slabs[0]))>;
     T* buf = xfer.as<T>();
     if (!dist) {
+      if (during) during();  // (one stream: nothing to overlap, same order as the ranks)
       for (int s = 0; s < nloc; ++s) {
         Slab& me = slabs[s];
         Slab& lo = slabs[(s - 1 + nloc) % nloc];
@@ -416,12 +476,12 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     launch_pack<T>(vec_of(me), 0, me.P.cnt_first, send_lo, c->stream);
     comm->exchange(send_hi, 18 * static_cast<size_t>(me.P.cnt_last), send_lo, 18 * static_cast<size_t>(me.P.cnt_first),
                    recv_lo, 18 * static_cast<size_t>(me.P.n_glo), recv_hi, 18 * static_cast<size_t>(me.P.n_ghi),
-                   sizeof(T) == 8, c->stream);
+                   sizeof(T) == 8, c->stream, during);
     launch_unpack<T>(vec_of(me), me.P.n_owned, me.P.n_glo, recv_lo, c->stream);
     launch_unpack<T>(vec_of(me), me.P.n_owned + me.P.n_glo, me.P.n_ghi, recv_hi, c->stream);
   };
   auto grid_u = [&](const Slab& S) { return 6 * std::max(1, std::min((S.P.n_owned + 255) / 256, c->num_sms * 2)); };
-  auto grid_a = [&](const Slab& S) { return apply_grid(S.P.n_owned, c->num_sms); };
+  auto grid_a_n = [&](int n) { return apply_grid(n, c->num_sms); };
   auto update_all = [&](int init) {
     for (int s = 0; s < nloc; ++s) {
       Slab& S = slabs[s];
@@ -496,15 +556,37 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
       launch_finalize_gamma(dst, totals, nloc, init, c->stream);
     }
   };
+  // The apply in three node ranges per slab: the interior planes read no
+  // ghost values, so they run while the ghost planes of z are in flight
+  // (SlabTransport::exchange's `during`); the two boundary planes follow the
+  // unpack.  Owned ids are plane-ordered: plane z0 = [0, cnt_first), plane
+  // z1-1 = [n_owned - cnt_last, n_owned).  Each range defers its 6 sums into
+  // rtot[slab][range]; sum_ranges_kernel adds them in fixed order, so the
+  // in-process slabs and the ranks produce the same bits.
+  double* rtot = totals + 21 * nloc;
+  auto apply_range = [&](Slab& S, int s, int k) {
+    const SlabPlan& P = S.P;
+    const bool one_plane = P.z1 - P.z0 == 1;
+    const int lo_end = one_plane ? P.n_owned : P.cnt_first;
+    const int hi_beg = one_plane ? P.n_owned : P.n_owned - P.cnt_last;
+    const int n0 = k == 0 ? 0 : (k == 1 ? lo_end : hi_beg);
+    const int n1 = k == 0 ? lo_end : (k == 1 ? hi_beg : P.n_owned);
+    ApplyArgs<TV, TZ> aa{S.list.as<int>(), S.map.as<int>(), beta_apply, Z(S), Pv(S), Q(S),
+                         S.partials.as<double>(), dst, r, n1, static_cast<int>(S.ld),
+                         P.n_local, P.zbase, P.nzl, rtot + (3 * s + k) * 6, 1};
+    aa.n0 = n0;
+    launch_apply<TV, TZ>(aa, std::max(1, grid_a_n(n1 - n0)), c->stream);
+  };
   auto apply_all = [&]() {
-    exchange([&](Slab& S) { return Z(S); });
+    exchange([&](Slab& S) { return Z(S); },
+             [&] {
+               for (int s = 0; s < nloc; ++s) apply_range(slabs[s], s, 1);
+             });
     for (int s = 0; s < nloc; ++s) {
-      Slab& S = slabs[s];
-      ApplyArgs<TV, TZ> aa{S.list.as<int>(), S.map.as<int>(), beta_apply, Z(S), Pv(S), Q(S),
-                           S.partials.as<double>(), dst, r, S.P.n_owned, static_cast<int>(S.ld),
-                           S.P.n_local, S.P.zbase, S.P.nzl, totals + 6 * s, 1};
-      launch_apply<TV, TZ>(aa, grid_a(S), c->stream);
+      apply_range(slabs[s], s, 0);
+      apply_range(slabs[s], s, 2);
     }
+    sum_ranges_kernel<<<1, 32 * ((6 * nloc + 31) / 32), 0, c->stream>>>(rtot, totals, nloc);
     reduce(6);
     launch_finalize_apply(dst, totals, nloc, c->stream);
   };
@@ -514,13 +596,46 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
   apply_all();
   const int check = opt.check_every > 0 ? opt.check_every : 16;
   int64_t launches = 0;
-  for (;;) {
+  auto iterations = [&]() {
     for (int it = 0; it < check; ++it) {
       update_all(0);
       if (use_gmg) precondition_all(0);
       apply_all();
-      launches += 2 * nloc + 2 + 8 * nloc;
     }
+  };
+  // The `check` iterations between host polls as one CUDA graph (in-process
+  // slabs, or ranks whose transport only enqueues device work: NCCL on the
+  // side stream is captured with its fork/join events).  A capture the
+  // transport refuses falls back to eager launches.
+  struct ExecGuard {
+    cudaGraphExec_t e = nullptr;
+    ~ExecGuard() {
+      if (e) cudaGraphExecDestroy(e);
+    }
+  } guard;
+  cudaGraphExec_t& exec = guard.e;
+  if (!c->profiling && (!dist || comm->capturable())) {
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      iterations();
+    } catch (const ShlError&) {
+      cudaStreamEndCapture(c->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      graph = nullptr;
+      cudaGetLastError();
+    }
+    if (graph == nullptr && cudaStreamEndCapture(c->stream, &graph) != cudaSuccess) graph = nullptr;
+    if (graph && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) exec = nullptr;
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+  }
+  for (;;) {
+    if (exec)
+      CK(cudaGraphLaunch(exec, c->stream));
+    else
+      iterations();
+    launches += check * (2 * nloc + 2 + 11 * nloc);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->hstate, c->state.p, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
     c->sync();

@@ -366,8 +366,8 @@ __global__ void __launch_bounds__(192) apply3_kernel(const ApplyArgs<TV, TZ> A) 
     bcoef[k] = static_cast<TV>(st->beta[2 * part + k]);
   }
   double pq2[2] = {0, 0};
-  for (int tile = blockIdx.x; tile * 64 < A.n; tile += gridDim.x) {
-    const int idx = tile * 64 + grp * 32 + lane;
+  for (int tile = blockIdx.x; A.n0 + tile * 64 < A.n; tile += gridDim.x) {
+    const int idx = A.n0 + tile * 64 + grp * 32 + lane;
     const bool valid = idx < A.n;
     const int g = valid ? A.node_list[idx] : -1;
     gather3_tile<TV, TZ>(part_s[grp], part, lane, idx, valid, g, zv, A.beta, A.node_map, A.r, A.zbase,
@@ -440,9 +440,9 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
   __shared__ int tq_slot[2];
   TileQueue tq{&st->tile_next[0], tq_slot};
   for (int tile = tq.first();; tile = tq.advance()) {
-    if (tile * (32 * G) >= A.n) break;
+    if (A.n0 + tile * (32 * G) >= A.n) break;
     tq.request();
-    const int idx = tile * (32 * G) + grp * 32 + lane;
+    const int idx = A.n0 + tile * (32 * G) + grp * 32 + lane;
     const bool valid = idx < A.n;
     const int g = valid ? A.node_list[idx] : -1;
     {
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
   if (threadIdx.x == 0) last = arrive_last(&st->counter_apply);
   __syncthreads();
   if (!last) return;
-  const int ntiles = (A.n + 32 * G - 1) / (32 * G);
+  const int ntiles = (A.n - A.n0 + 32 * G - 1) / (32 * G);
   double tot[6] = {0, 0, 0, 0, 0, 0};
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
 #pragma unroll

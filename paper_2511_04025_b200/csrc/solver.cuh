@@ -44,6 +44,7 @@ struct ApplyArgs {
   double* totals; // defer != 0: write the 6 reduced sums here, leave state alone
   int defer;
   BrickView bricks;  // nab > 0: staged brick kernel (brick.cuh)
+  int n0 = 0;        // per-node gather kernels: iterate nodes [n0, n) (z-slab interior / boundary planes)
 };
 
 template <typename TX, typename TV, typename TZ = TV>
