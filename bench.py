@@ -388,6 +388,23 @@ def run_ours(args, rank, world, local):
     sv_time = sum(r_.timings["t_solve"] for r_ in prof) / 1e3
     survey_formula = {"bytes": sv_bytes, "solve_s": sv_time, "achieved_gbs": sv_bytes / sv_time / 1e9,
                       "frac": sv_bytes / sv_time / 1e9 / peaks()[0], "designs": len(prof)}
+    # The FP64 operator's arithmetic side of the same roofline: 2034 FMA per node
+    # (576 to build the 27 neighbour blocks S_m = sum_e beta_e K0[a,b], 1458 to
+    # apply them to 6 load cases) against the B200 FP64 FMA rate
+    # (64 per SM per clock, the rate ncu's fp64 pipe percentage is quoted
+    # against).  Intensity 4068 flop / 648 B = 6.3 flop/B sits right of the
+    # FP64 ridge (peak FP64 / HBM): the kernel is FP64-arithmetic bound.
+    fp64_roofline = None
+    if vb == 8 and per_node == bytes_apply:
+        sm_mhz = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
+        fp64_peak = 64 * 2 * torch.cuda.get_device_properties(local).multi_processor_count * sm_mhz * 1e6 / 1e12
+        fl = 2 * 2034 * prof_nodes
+        fp64_roofline = {"flop_per_node": 2 * 2034, "achieved_tflops": fl / avg_launch_s / 1e12,
+                         "peak_tflops": fp64_peak, "frac": fl / avg_launch_s / 1e12 / fp64_peak,
+                         "intensity_flop_per_byte": 2 * 2034 / per_node if per_node else None,
+                         "ridge_flop_per_byte": fp64_peak * 1e12 / (peak * 1e9),
+                         "peak_source": "64 FP64 FMA per SM per clock x SMs x sm_max_mhz (B200)"}
     line = {"metric": METRIC, "value": total_designs / dev_max, "unit": UNIT, "n_gpus": world,
             "steps": len(designs), "warmup": args.warmup, "ms_per_step": dev_max / len(designs) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -414,7 +431,8 @@ def run_ours(args, rank, world, local):
                           "achieved_gbs": iter_bytes / iter_s / 1e9 if iter_s else None,
                           "frac": iter_bytes / iter_s / 1e9 / peak if iter_s else None},
                          "iteration_us": iter_s * 1e6,
-                         "survey_solver_formula": survey_formula},
+                         "survey_solver_formula": survey_formula,
+                         "fp64": fp64_roofline},
             "stages_ms": {k: statistics.mean(s_.timings[k] for s_ in st)
                           for k in ("t_field", "t_mesh", "t_AS", "t_solve", "t_C", "t_fwd")},
             "stages_ms_single_lane": {k: statistics.mean(r_.timings[k] for r_ in prof)
