@@ -175,6 +175,29 @@ def test_homogenize_c1_vs_oracle(S, O, seed):
     assert res.stats.converged
 
 
+@pytest.mark.parametrize("r,seed,prec,tol,bar", [(20, 3, "mixed", 1e-6, 1e-4), (25, 5, "mixed", 1e-6, 1e-4),
+                                                 (36, 7, "mixed", 1e-6, 1e-4), (44, 9, "fp64", 1e-10, 1e-7),
+                                                 (18, 11, "fp64", 1e-10, 1e-7)])
+def test_homogenize_ragged_sizes_vs_oracle(S, O, r, seed, prec, tol, bar):
+    """Grid sizes that are not multiples of the 8x4x4 level-0 brick (ragged last
+    bricks on the periodic seam), odd r (AUTO picks block Jacobi: no multigrid)
+    and even r whose multigrid hierarchy stops at an odd coarse size (36 -> 18
+    -> 9, 44 -> 22 -> 11, 18 -> 9): C^H from the product path against the
+    oracle's masked PCG (pipeline.hpp:61-113), same element and node sets."""
+    sd, od = pair(S, O, "cubic_octant", seed, 4)
+    res = S.homogenize(sd, S.ShellParams(), S.BaseMaterial(), r,
+                       S.HomogenizeOptions(residual_tol=tol, precision=prec))
+    ref = O.homogenize(od, r, tol=min(tol, 1e-9) * 1e-2)
+    assert res.stats.n_elements == ref.n_elements
+    assert res.stats.n_nodes == ref.n_nodes
+    assert res.stats.converged and np.all(res.iterations > 0)
+    if r % 2 == 0 and r // 2 >= 8:
+        assert res.stats.gmg_levels >= 1
+    else:
+        assert res.stats.gmg_levels == 0
+    assert rel_fro(res.tensor, ref.C) < bar
+
+
 def test_homogenize_gyroid_c2(S, O):
     """Config C2: 64^3 gyroid fixture -> cubic C^H, against the oracle."""
     r = 64
