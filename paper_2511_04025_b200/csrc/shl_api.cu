@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <string>
 #include <thread>
@@ -679,13 +680,17 @@ void validate_inputs(const shl_design* design, const shl_shell_params* sp, const
 
 void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params* sp,
                     const shl_material* mat, int r, const shl_solve_options* o, double* C_out,
-                    shl_stats* st) {
+                    shl_stats* st, std::future<FieldInputs>* prepared = nullptr) {
   if (!C_out) throw ShlError(SHL_VALIDATION, "null argument");
   const shl_solve_options opt = default_opts(o);
   double K0[576];
   validate_inputs(design, sp, mat, r, K0);
   const int64_t l0 = c->launches, h0 = c->h2d, d0 = c->d2h;
-  FieldInputs fin = tagged("field", [&] { return prepare_field(shl::HostDesign::from_abi(*design), r); });
+  // (the batch path prepares the host tables of a lane's next design while the
+  // current one runs on the GPU: `prepared` holds them, or their exception)
+  FieldInputs fin = tagged("field", [&] {
+    return prepared && prepared->valid() ? prepared->get() : prepare_field(shl::HostDesign::from_abi(*design), r);
+  });
   CK(cudaEventRecord(c->ev[0], c->stream));
   tagged("field", [&] {
     run_field(c, fin);
@@ -1010,20 +1015,36 @@ int shl_homogenize_batch(shl_ctx* c, int n, const shl_design* designs, const shl
   std::atomic<int> next{0};
   std::atomic<int> device_failed{0};
   std::string device_msg;
+  // Each lane claims its next design one step ahead and builds that design's
+  // host inputs (symmetry expansion, glibc cosine tables: ~1 ms at 128^3) on a
+  // helper thread while the current design runs, so the GPU does not wait for
+  // the host between designs.
+  auto prepare_async = [&](int k) {
+    return std::async(std::launch::async,
+                      [&designs, r, k] { return prepare_field(shl::HostDesign::from_abi(designs[k]), r); });
+  };
   auto work = [&](shl_ctx* lc, int lane) {
     cudaSetDevice(c->device);
     lc->profiling = c->profiling;
-    for (;;) {
-      const int i = next.fetch_add(1);
-      if (i >= n || device_failed.load()) break;
+    int i = next.fetch_add(1);
+    std::future<FieldInputs> pre;
+    if (i < n) pre = prepare_async(i);
+    while (i < n && !device_failed.load()) {
+      const int j = next.fetch_add(1);
+      std::future<FieldInputs> pre_next;
+      if (j < n) pre_next = prepare_async(j);
       shl_stats* st = stats ? stats + i : nullptr;
       if (st) std::memset(st, 0, sizeof(*st));
       const int rc =
-          guarded(lc, [&] { homogenize_one(lc, designs + i, sp, mat, r, opt, C_out + 36 * i, st); });
+          guarded(lc, [&] { homogenize_one(lc, designs + i, sp, mat, r, opt, C_out + 36 * i, st, &pre); });
       if (st) st->lane = lane;
       if (status) status[i] = rc;
       if (rc == SHL_CUDA && !device_failed.exchange(1)) device_msg = lc->err;
+      i = j;
+      pre = std::move(pre_next);
     }
+    // a design claimed but not run (device failure): report it
+    if (i < n && status) status[i] = SHL_CUDA;
   };
   std::vector<std::thread> threads;
   for (int l = 1; l < L; ++l) threads.emplace_back(work, c->lanes[l - 1], l);
