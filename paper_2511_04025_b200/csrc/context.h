@@ -3,6 +3,7 @@
 // decomposition).  Internal; not part of the public ABI.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,6 +39,18 @@ extern thread_local cudaStream_t g_alloc_stream;
 
 // Owning device allocation that only grows.  Move-only: a copied raw pointer
 // would be freed twice (e.g. when a std::vector of levels reallocates).
+struct DevBuf;
+
+// NVTX range for one pipeline stage (header-only nvtx3: a no-op unless a
+// profiler's injection library is attached).  Host-side ranges: with
+// asynchronous launches they bracket the enqueueing of the stage's work.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;

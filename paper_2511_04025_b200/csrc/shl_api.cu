@@ -333,7 +333,10 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   vc.s = c->stream;
   if (vc.gp.nu <= 0) vc.gp.nu = sizeof(TV) == 8 ? 1 : 2;
   if (use_gmg) {
-    vc.L = gmg_setup<TZ>(c, vc.gp, static_cast<TZ>(ridge));
+    {
+      NvtxRange nr("shellular: multigrid setup (Galerkin levels)");
+      vc.L = gmg_setup<TZ>(c, vc.gp, static_cast<TZ>(ridge));
+    }
     if (vc.L == 0) throw ShlError(SHL_VALIDATION, "multigrid needs r divisible by 2 with r/2 >= 8");
     c->gmg0.ensure(static_cast<size_t>(3) * nV * sizeof(TZ));
     CK(cudaMemsetAsync(c->gmg0.p, 0, static_cast<size_t>(3) * nV * sizeof(TZ), c->stream));
@@ -478,6 +481,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
       if (g) cudaGraphExecDestroy(g);
     }
   } graph_guard{gexec};
+  NvtxRange pcg_range("shellular: PCG iterations");
   if (use_while) {
     CK(cudaGraphLaunch(gexec, c->stream));
     CK(cudaMemcpyAsync(c->hstate, c->state.p, sizeof(shl::PcgState), cudaMemcpyDeviceToHost, c->stream));
@@ -569,7 +573,10 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   shl::ChomArgs<TX> ca{c->elem_list.as<int>(), c->node_map.as<int>(), c->beta64.as<double>(), x,
                        c->partials.as<double>(), c->cout.as<double>(), dst,
                        static_cast<int>(c->n_elem), r, ld, 0, r, 0};
-  shl::launch_chom<TX>(ca, grid_c, c->stream);
+  {
+    NvtxRange nr("shellular: C^H reduction");
+    shl::launch_chom<TX>(ca, grid_c, c->stream);
+  }
   launches += 1;
   CK(cudaGetLastError());
   c->d2h += 36 * sizeof(double);
@@ -688,11 +695,13 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
   const int64_t l0 = c->launches, h0 = c->h2d, d0 = c->d2h;
   // (the batch path prepares the host tables of a lane's next design while the
   // current one runs on the GPU: `prepared` holds them, or their exception)
+  NvtxRange design_range("shellular: homogenize");
   FieldInputs fin = tagged("field", [&] {
     return prepared && prepared->valid() ? prepared->get() : prepare_field(shl::HostDesign::from_abi(*design), r);
   });
   CK(cudaEventRecord(c->ev[0], c->stream));
   tagged("field", [&] {
+    NvtxRange nr("shellular: field");
     run_field(c, fin);
     return 0;
   });
@@ -702,6 +711,7 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
   // design (norm 0) still fails with the field-stage error, before any solve.
   c->norm = 1.0;  // placeholder for run_mesh's host-side check
   tagged("mesh", [&] {
+    NvtxRange nr("shellular: mesh + topology");
     run_mesh(c, *sp);
     return 0;
   });
@@ -709,6 +719,7 @@ void homogenize_one(shl_ctx* c, const shl_design* design, const shl_shell_params
   if (c->norm == 0.0) throw ShlError(SHL_DEGENERATE, "field: design is degenerate (norm = 0)");
   CK(cudaEventRecord(c->ev[2], c->stream));
   tagged("solve", [&] {
+    NvtxRange nr("shellular: solve + C^H");
     solve_dispatch(c, K0, opt, C_out, st);
     return 0;
   });

@@ -596,6 +596,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
   apply_all();
   const int check = opt.check_every > 0 ? opt.check_every : 16;
   int64_t launches = 0;
+  NvtxRange pcg_range("shellular: z-slab PCG iterations");
   auto iterations = [&]() {
     for (int it = 0; it < check; ++it) {
       update_all(0);
