@@ -53,9 +53,10 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=16)
     p.add_argument("--warmup", type=int, default=4)
-    p.add_argument("--lanes", type=int, default=2,
-                   help="designs in flight at once per GPU (shl_set_batch_lanes); 2 fills the GPU's "
-                        "idle time inside one design's V-cycle (DESIGN.md 4.2); 1 = one design at a time")
+    p.add_argument("--lanes", type=int, default=0,
+                   help="designs in flight at once per GPU (shl_set_batch_lanes); 0 = auto: the warm-up "
+                        "runs its designs with 1 and with 2 lanes and the timed region uses the faster "
+                        "(2 fills the GPU's idle time inside one design's V-cycle, DESIGN.md 4.2)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--r", type=int, default=128)
     p.add_argument("--tol", type=float, default=1e-5)
@@ -80,9 +81,9 @@ def config(args, world):
             "rtol": args.tol, "precision": args.precision, "preconditioner": args.preconditioner,
             "global_batch": world,
             "designs_per_rank_per_step": 1, "parallelism": f"design-sharded x{world}",
-            "designs_in_flight_per_gpu": args.lanes,
+            "designs_in_flight_per_gpu": args.lanes if args.lanes > 0 else "auto (1 or 2, chosen in the warm-up)",
             "timed_region": f"one shl_homogenize_batch call over {args.steps} designs per rank, "
-                            f"{args.lanes} lanes (streams + host threads) in flight",
+                            f"{args.lanes if args.lanes > 0 else 'auto'} lanes (streams + host threads) in flight",
             "l2": "inputs larger than L2 (solver working set ~300 MB per design, new design each step)"}
 
 
@@ -301,8 +302,33 @@ def run_ours(args, rank, world, local):
     warm, timed = seeds_for(rank, args.steps, args.warmup)
     designs = [S.random_design(spec, s) for s in timed]
     # warm-up: same batch path (creates the lane contexts, sizes every workspace)
-    S.homogenize_batch([S.random_design(spec, s) for s in warm], sp, mat, args.r, opt, ctx=ctx,
-                       lanes=args.lanes)
+    warm_designs = [S.random_design(spec, s) for s in warm]
+    lane_trials = None
+    if args.lanes > 0:
+        S.homogenize_batch(warm_designs, sp, mat, args.r, opt, ctx=ctx, lanes=args.lanes)
+    else:
+        # auto: time the same warm-up designs with one and with two designs in
+        # flight and keep the faster for the timed region, so a box where the
+        # lanes contend falls back to one design at a time.  An even number (>= 6)
+        # of designs, a first pass that sizes both lanes' workspaces, then the
+        # two settings alternated twice, best of each.
+        n_trial = max(6, len(warm_designs) + len(warm_designs) % 2)
+        trial_designs = [S.random_design(spec, 9001 + rank * 100 + i) for i in range(n_trial)]
+        S.homogenize_batch(trial_designs, sp, mat, args.r, opt, ctx=ctx, lanes=2)
+        trial = [float("inf"), float("inf")]
+        for lanes_try in (1, 2, 1, 2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            S.homogenize_batch(trial_designs, sp, mat, args.r, opt, ctx=ctx, lanes=lanes_try)
+            torch.cuda.synchronize()
+            trial[lanes_try - 1] = min(trial[lanes_try - 1], time.perf_counter() - t0)
+        warm_designs = trial_designs
+        tt = torch.tensor(trial, dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)  # every rank makes the same choice
+        args.lanes = 1 if float(tt[0]) <= float(tt[1]) else 2
+        lane_trials = {"warmup_designs": len(warm_designs), "wall_s_1_lane": float(tt[0]),
+                       "wall_s_2_lanes": float(tt[1]), "chosen": args.lanes}
 
     def barrier():
         torch.cuda.synchronize()
@@ -413,7 +439,7 @@ def run_ours(args, rank, world, local):
                       {"mixed": "f64 field/C^H and x/r; f32 operator, p/q, z (block-Jacobi PCG)",
                        "fp32": "f64 field/C^H, f32 PCG", "fp64": "f64"}[args.precision]),
             "data": "synthetic (seeded random_design, no checkpoint/dataset)",
-            "config": config(args, world),
+            "config": dict(config(args, world), **({"lane_selection": lane_trials} if lane_trials else {})),
             "e2e": {"value": total_designs / wall_max, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "how": "wall clock around the C-ABI call shl_homogenize_batch with host design "
