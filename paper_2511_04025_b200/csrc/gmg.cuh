@@ -43,6 +43,7 @@ struct LevelArgs {
   TV ridge;           // level 0 only
   int zbase;          // level 0 of a z-slab (0 otherwise)
   double* totals;     // mode 2: write the r.z sums here instead of finalizing (slabs)
+  int n0;             // nodes [n0, n) are swept (a z-slab's owned level-1 planes; 0 otherwise)
 };
 
 // stencil_gather restricted to neighbour plane dz = PLANE-1.
@@ -93,10 +94,10 @@ __global__ void __launch_bounds__(192)
   __shared__ int tq_slot[2];
   TileQueue tq{&st->tile_next[1], tq_slot};
   for (int tile = tq.first();; tile = tq.advance()) {
-    if (tile * 64 >= L.n) break;
+    if (L.n0 + tile * 64 >= L.n) break;
     tq.request();
     gam2[0] = gam2[1] = 0.0;
-    const int idx = tile * 64 + grp * 32 + lane;
+    const int idx = L.n0 + tile * 64 + grp * 32 + lane;
     const bool valid = idx < L.n;
     const int g = valid ? L.node_list[idx] : -1;
     {
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(256) coarse_warp_sweep_kernel(const LevelArgs<
                                                                 TV omega, int mode, const PcgState* st) {
   pdl_wait();
   if (st->stop) return;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int warp = L.n0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (warp >= L.n) return;  // whole warps exit together
   coarse_warp_node<TV>(L, b, xin, xout, omega, mode, warp, lane);
 }
@@ -456,11 +457,12 @@ __global__ void __cluster_dims__(kCoR, 1, 1) __launch_bounds__(kCoThreads, 1)
 template <typename TB, typename TV>
 __global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV* __restrict__ dinv,
                                     int n, const TB* __restrict__ b, TV* __restrict__ xout, TV omega,
-                                    const PcgState* st) {
+                                    const PcgState* st, int n0) {
   pdl_wait();
   if (st->stop) return;
   int idx, s;
   node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
+  idx += n0;
   if (idx >= n) return;
   const size_t ob = vbase(idx, 18) + s * 32;
   TV D[6];
@@ -475,10 +477,12 @@ __global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV*
 
 // ---------------------------------------------------------------- transfers
 // b_c(N) = sum_{n in supp(N)} w(n,N) res_f(n), w = prod over axes (1 | 1/2)
+// (f1 > 0: only fine ids in [f0, f1) contribute and b_c accumulates -- the
+// partial restriction of a z-slab's owned level-1 nodes, summed over slabs)
 template <typename TV>
 __global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c,
                                 const int* __restrict__ map_f, int r_f, const TV* __restrict__ res_f,
-                                TV* __restrict__ b_c, const PcgState* st) {
+                                TV* __restrict__ b_c, const PcgState* st, int f0 = 0, int f1 = 0) {
   pdl_wait();
   if (st->stop) return;
   int idx, s;
@@ -502,13 +506,59 @@ __global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c
       nf[m] = map_f[(static_cast<size_t>(fz[m / 9]) * r_f + fy[(m / 3) % 3]) * r_f + fx[m % 3]];
 #pragma unroll
     for (int m = 0; m < 27; ++m) {
-      if (nf[m] < 0) continue;
+      if (nf[m] < 0 || (f1 > 0 && (nf[m] < f0 || nf[m] >= f1))) continue;
       const int di = m % 3 - 1, dj = (m / 3) % 3 - 1, dk = m / 9 - 1;
       const TV w = TV((di ? 0.5 : 1.0) * (dj ? 0.5 : 1.0) * (dk ? 0.5 : 1.0));
       const size_t o = vbase(nf[m], 18) + s * 32;
       acc[0] = fma_t(w, res_f[o], acc[0]);
       acc[1] = fma_t(w, res_f[o + 192], acc[1]);
       acc[2] = fma_t(w, res_f[o + 384], acc[2]);
+    }
+  }
+  const size_t oc = vbase(idx, 18) + s * 32;
+  if (f1 > 0) {
+    b_c[oc] += acc[0];
+    b_c[oc + 192] += acc[1];
+    b_c[oc + 384] += acc[2];
+  } else {
+    b_c[oc] = acc[0];
+    b_c[oc + 192] = acc[1];
+    b_c[oc + 384] = acc[2];
+  }
+}
+
+// z-slab restriction onto the slab's OWNED coarse (level-1) nodes [c0, c1)
+// from the slab's level-0 residual, ghost planes included (the coarse planes a
+// slab owns gather fine planes z0-1 .. z1, all inside its local node map)
+template <typename TV>
+__global__ void restrict_own_kernel(const int* __restrict__ list_c, int c0, int c1, int r_c,
+                                    const int* __restrict__ map_s, int zbase, int nzl, int r_f,
+                                    const TV* __restrict__ res_f, TV* __restrict__ b_c, const PcgState* st) {
+  pdl_wait();
+  if (st->stop) return;
+  int idx, s;
+  node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
+  idx += c0;
+  if (idx >= c1) return;
+  const int G = list_c[idx];
+  const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
+  TV acc[3] = {TV(0), TV(0), TV(0)};
+  if (G != 0) {
+    for (int dk = -1; dk <= 1; ++dk) {
+      int lz = (2 * K + dk + r_f) % r_f - zbase;
+      lz += lz < 0 ? r_f : 0;
+      if (lz >= nzl) continue;  // (never for an owned coarse plane)
+      for (int dj = -1; dj <= 1; ++dj)
+        for (int di = -1; di <= 1; ++di) {
+          const int fi = (2 * I + di + r_f) % r_f, fj = (2 * J + dj + r_f) % r_f;
+          const int nf = map_s[(static_cast<size_t>(lz) * r_f + fj) * r_f + fi];
+          if (nf < 0) continue;
+          const TV w = TV((di ? 0.5 : 1.0) * (dj ? 0.5 : 1.0) * (dk ? 0.5 : 1.0));
+          const size_t o = vbase(nf, 18) + s * 32;
+          acc[0] = fma_t(w, res_f[o], acc[0]);
+          acc[1] = fma_t(w, res_f[o + 192], acc[1]);
+          acc[2] = fma_t(w, res_f[o + 384], acc[2]);
+        }
     }
   }
   const size_t oc = vbase(idx, 18) + s * 32;
@@ -566,10 +616,10 @@ template <typename TV>
 __global__ void __launch_bounds__(128) prolong_kernel(const int* __restrict__ list_f, int n_f, int r_f,
                                                       const int* __restrict__ map_c, int r_c,
                                                       const TV* __restrict__ x_c, TV* __restrict__ x_f,
-                                                      const PcgState* st) {
+                                                      const PcgState* st, int n0) {
   pdl_wait();
   if (st->stop) return;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int idx = n0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_f) return;
   const int g = list_f[idx];
   if (g == 0) return;
@@ -953,19 +1003,20 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
     // (at 64^3 and up the node-ordered level_sweep3 streams the stencils better:
     //  61 vs 38 us at level 1 of 128^3; at 16^3 the warp-per-node sweep wins:
     //  14 vs 10 us; at 32^3 the staged bricks: 20 vs 29 us)
-    if (!fine && L.bricks.nab > 0 && mode != 2 && L.n <= 32768 && L.r >= 32) {
+    if (!fine && L.bricks.nab > 0 && L.n0 == 0 && mode != 2 && L.n <= 32768 && L.r >= 32) {
       launch_stencil_brick_sweep(L, b, xin, xout, omega, mode, st, s);
       return;
     }
   }
-  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals,
+                  L.n0};
   if (fine) {
     launch_pdl(level_sweep3_kernel<TB, TV, true>, grid, 192, 0, s, a, b, xin, xout, omega, mode, st, partials, init);
-  } else if (L.n > 32768) {  // large stored level: thread per node is throughput-bound
+  } else if (L.n - L.n0 > 32768) {  // large stored level: thread per node is throughput-bound
     launch_pdl(level_sweep3_kernel<TB, TV, false>, grid, 192, 0, s, a, b, xin, xout, omega, mode, st, partials, init);
   } else {  // small stored level: latency-bound, one warp per node (mode 2 is level-0 only)
-    launch_pdl(coarse_warp_sweep_kernel<TV>, (L.n + 7) / 8, 256, 0, s, a, reinterpret_cast<const TV*>(b), xin, xout,
-               omega, mode, st);
+    launch_pdl(coarse_warp_sweep_kernel<TV>, std::max(1, (L.n - L.n0 + 7) / 8), 256, 0, s, a,
+               reinterpret_cast<const TV*>(b), xin, xout, omega, mode, st);
   }
 }
 
@@ -976,16 +1027,17 @@ void launch_level_sweep_out(const GmgLevelView<TV>& L, const TB* b, const TV* xi
     launch_brick_sweep<TB, TV, TO>(L, b, xin, xout, omega, 2, st, partials, init, s);
     return;
   }
-  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals};
+  LevelArgs<TV> a{L.node_list, L.node_map, L.beta, L.stencil, L.dinv, L.r, L.n, L.zero_slot, L.ridge, L.zbase, L.totals,
+                  L.n0};
   launch_pdl(level_sweep3_kernel<TB, TV, true, TO>, grid, 192, 0, s, a, b, xin, xout, omega, 2, st, partials, init);
 }
 
 template <typename TB, typename TV>
 void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV omega, const PcgState* st,
                          cudaStream_t s) {
-  if (L.n)
-    launch_pdl(jacobi_first_kernel<TB, TV>, node_case_blocks(L.n, 192), 192, 0, s, L.node_list, L.dinv, L.n, b, xout,
-               omega, st);
+  if (L.n > L.n0)
+    launch_pdl(jacobi_first_kernel<TB, TV>, node_case_blocks(L.n - L.n0, 192), 192, 0, s, L.node_list, L.dinv, L.n, b,
+               xout, omega, st, L.n0);
 }
 
 // The coarsest solve (jacobi_first + sweeps - 1 sweeps) as one cluster
@@ -1015,7 +1067,23 @@ void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const
                      const PcgState* st, cudaStream_t s) {
   if (C.n)
     launch_pdl(restrict_kernel<TV>, node_case_blocks(C.n, 192), 192, 0, s, C.node_list, C.n, C.r, F.node_map, F.r,
-               res_f, b_c, st);
+               res_f, b_c, st, 0, 0);
+}
+
+template <typename TV>
+void launch_restrict_partial(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
+                             const PcgState* st, cudaStream_t s) {
+  if (C.n)
+    launch_pdl(restrict_kernel<TV>, node_case_blocks(C.n, 192), 192, 0, s, C.node_list, C.n, C.r, F.node_map, F.r,
+               res_f, b_c, st, F.n0, std::max(F.n, 1));
+}
+
+template <typename TV>
+void launch_restrict_own(const GmgLevelView<TV>& C, const int* map_s, int zbase, int nzl, int r_f, const TV* res_f,
+                         TV* b_c, const PcgState* st, cudaStream_t s) {
+  if (C.n > C.n0)
+    launch_pdl(restrict_own_kernel<TV>, node_case_blocks(C.n - C.n0, 192), 192, 0, s, C.node_list, C.n0, C.n, C.r,
+               map_s, zbase, nzl, r_f, res_f, b_c, st);
 }
 
 template <typename TV>
@@ -1029,9 +1097,9 @@ void launch_restrict_slab(const GmgLevelView<TV>& C, const int* map_s, int zbase
 template <typename TV>
 void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const TV* x_c, TV* x_f,
                     const PcgState* st, cudaStream_t s) {
-  if (F.n)
-    launch_pdl(prolong_kernel<TV>, (F.n + 127) / 128, 128, 0, s, F.node_list, F.n, F.r, C.node_map, C.r, x_c,
-               x_f, st);
+  if (F.n > F.n0)
+    launch_pdl(prolong_kernel<TV>, (F.n - F.n0 + 127) / 128, 128, 0, s, F.node_list, F.n, F.r, C.node_map, C.r, x_c,
+               x_f, st, F.n0);
 }
 
 #define SHL_GMG_INST(TV)                                                                               \
@@ -1045,7 +1113,11 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
   template bool launch_coarsest<TV>(const GmgLevelView<TV>&, const TV*, TV*, TV, int, const PcgState*, \
                                     cudaStream_t);                                                   \
   template void launch_restrict_slab<TV>(const GmgLevelView<TV>&, const int*, int, int, int, int, int,   \
-                                         const TV*, TV*, const PcgState*, cudaStream_t);
+                                         const TV*, TV*, const PcgState*, cudaStream_t);                \
+  template void launch_restrict_partial<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, \
+                                            TV*, const PcgState*, cudaStream_t);                        \
+  template void launch_restrict_own<TV>(const GmgLevelView<TV>&, const int*, int, int, int, const TV*, TV*, \
+                                        const PcgState*, cudaStream_t);
 SHL_GMG_INST(float)
 SHL_GMG_INST(double)
 template void launch_level_sweep<double, float>(const GmgLevelView<float>&, bool, const double*, const float*,

@@ -237,10 +237,24 @@ struct SlabPlan {
   int noff_z0 = 0;                  // global node id of the first owned node
 };
 
+// A slab's share of multigrid level 1 (levels >= 2 stay replicated).  Level-1
+// ids are grid-ordered, so the coarse planes [cz0, cz1) a slab owns -- the
+// planes cz with z0 <= 2 cz < z1 -- are the id range [c0, c1); the ghost planes
+// cz0-1 and cz1 (periodic) are the neighbours' boundary planes, the same ids in
+// every slab's full-length level-1 vectors.
+struct Level1Plan {
+  int c0 = 0, c1 = 0;          // owned ids
+  int first_n = 0, last0 = 0;  // owned plane cz0: [c0, c0 + first_n); plane cz1-1: [last0, c1)
+  int glo0 = 0, glo_n = 0;     // ghost plane cz0-1
+  int ghi0 = 0, ghi_n = 0;     // ghost plane cz1
+};
+
 struct Slab {
   SlabPlan P;
   DevBuf map, list, vec, partials;
   size_t ld = 0;
+  Level1Plan P1;
+  DevBuf v1;  // level-1 b, x (two), residual: 4 full-length vectors
 };
 
 namespace {
@@ -346,6 +360,12 @@ void build_slabs(shl_ctx* c, int G, int first, int count, std::vector<Slab>& sla
   c->sync();  // `counts` dies here
 }
 
+// level-1 plane start ids: out[cz] = off[cz * rc^2] (grid-order exclusive scan)
+__global__ void plane_start_kernel(const int* __restrict__ off, int rc, int* __restrict__ out) {
+  const int cz = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cz < rc) out[cz] = off[static_cast<size_t>(cz) * rc * rc];
+}
+
 // ---------------------------------------------------------------- solve
 // TX: x, r; TV: p, q and the operator; TZ: z, Dinv and the V-cycle (as in the
 // single-device solve).  use_gmg: multigrid-preconditioned, with level 0
@@ -433,6 +453,42 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
       vc.res.push_back(v + 3 * s18);
     }
   }
+  // Level 1 distributed over the slabs when there is a level 2 below it (the
+  // coarsest level itself stays replicated: it is one cluster kernel)
+  const bool dist1 = use_gmg && vc.L >= 2;
+  int max_plane1 = 0;
+  if (dist1) {
+    const auto& L1 = c->gmg[0];
+    const int rc = L1.r;
+    std::vector<int> ps(rc + 1);
+    {
+      DevBuf pbuf;
+      pbuf.ensure(sizeof(int) * rc);
+      plane_start_kernel<<<(rc + 127) / 128, 128, 0, c->stream>>>(L1.off.as<int>(), rc, pbuf.as<int>());
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(ps.data(), pbuf.p, sizeof(int) * rc, cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+    }
+    ps[rc] = L1.n;
+    for (auto& S : slabs) {
+      Level1Plan& Q = S.P1;
+      const int cz0 = (S.P.z0 + 1) / 2, cz1 = (S.P.z1 + 1) / 2;
+      const int glo = (cz0 - 1 + rc) % rc, ghi = cz1 % rc;
+      Q.c0 = ps[cz0];
+      Q.c1 = ps[cz1];
+      Q.first_n = ps[cz0 + 1] - ps[cz0];
+      Q.last0 = ps[cz1 - 1];
+      Q.glo0 = ps[glo];
+      Q.glo_n = ps[glo + 1] - ps[glo];
+      Q.ghi0 = ps[ghi];
+      Q.ghi_n = ps[ghi + 1] - ps[ghi];
+      max_plane1 = std::max({max_plane1, Q.first_n, Q.c1 - Q.last0, Q.glo_n, Q.ghi_n});
+      const size_t bytes = static_cast<size_t>(4) * 18 * L1.ld * sizeof(TZ);
+      S.v1.ensure(bytes);
+      CK(cudaMemsetAsync(S.v1.p, 0, bytes, c->stream));
+    }
+    xfer.ensure(std::max(xfer.cap, 4 * 18 * static_cast<size_t>(std::max(max_plane1, 1)) * sizeof(double)));
+  }
   PcgState hs{};
   hs.tol = opt.tol;
   hs.ridge = ridge_op;
@@ -505,6 +561,89 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     return v;
   };
   std::vector<TZ*> cur(nloc), oth(nloc);
+  // level-1 vectors of slab s: b, x (two buffers), residual
+  const size_t ld1 = dist1 ? static_cast<size_t>(c->gmg[0].ld) : 0;
+  auto B1 = [&](Slab& S) { return S.v1.as<TZ>(); };
+  auto XA1 = [&](Slab& S) { return S.v1.as<TZ>() + 18 * ld1; };
+  auto XB1 = [&](Slab& S) { return S.v1.as<TZ>() + 36 * ld1; };
+  auto RES1 = [&](Slab& S) { return S.v1.as<TZ>() + 54 * ld1; };
+  auto view1 = [&](Slab& S) {  // level 1 restricted to the slab's own nodes
+    GmgLevelView<TZ> v = vc.view[1];
+    v.n0 = S.P1.c0;
+    v.n = S.P1.c1;
+    v.bricks = BrickView{};
+    return v;
+  };
+  // ghost-plane exchange of a level-1 vector: each slab's boundary planes
+  // become its neighbours' ghost planes (same ids in every slab's vector)
+  std::vector<TZ*> cur1(nloc), oth1(nloc);
+  auto exchange1 = [&](std::vector<TZ*>& v) {
+    TZ* buf = xfer.as<TZ>();
+    if (!dist) {
+      for (int s = 0; s < nloc; ++s) {
+        const Level1Plan& Q = slabs[s].P1;
+        TZ* lo = v[(s - 1 + nloc) % nloc];
+        TZ* hi = v[(s + 1) % nloc];
+        launch_pack<TZ>(v[s], Q.c0, Q.first_n, buf, c->stream);
+        launch_unpack<TZ>(lo, Q.c0, Q.first_n, buf, c->stream);
+        launch_pack<TZ>(v[s], Q.last0, Q.c1 - Q.last0, buf, c->stream);
+        launch_unpack<TZ>(hi, Q.last0, Q.c1 - Q.last0, buf, c->stream);
+      }
+      return;
+    }
+    const Level1Plan& Q = slabs[0].P1;
+    const size_t stride = 18 * static_cast<size_t>(std::max(max_plane1, 1));
+    TZ *send_hi = buf, *send_lo = buf + stride, *recv_lo = buf + 2 * stride, *recv_hi = buf + 3 * stride;
+    launch_pack<TZ>(v[0], Q.last0, Q.c1 - Q.last0, send_hi, c->stream);
+    launch_pack<TZ>(v[0], Q.c0, Q.first_n, send_lo, c->stream);
+    comm->exchange(send_hi, 18 * static_cast<size_t>(Q.c1 - Q.last0), send_lo, 18 * static_cast<size_t>(Q.first_n),
+                   recv_lo, 18 * static_cast<size_t>(Q.glo_n), recv_hi, 18 * static_cast<size_t>(Q.ghi_n),
+                   sizeof(TZ) == 8, c->stream, {});
+    launch_unpack<TZ>(v[0], Q.glo0, Q.glo_n, recv_lo, c->stream);
+    launch_unpack<TZ>(v[0], Q.ghi0, Q.ghi_n, recv_hi, c->stream);
+  };
+  // Level 1 on the slabs (dist1): restriction onto each slab's own coarse
+  // nodes (after a ghost exchange of the level-0 residual), damped block
+  // Jacobi with a ghost exchange before every sweep, the residual's partial
+  // restrictions summed into the replicated level 2 (an all-reduce 8x smaller
+  // than level 1's), level 2.. as before, prolongation onto the own nodes and
+  // a last ghost exchange for the level-0 prolongation.
+  auto level1_slabs = [&](int init) {
+    const TZ wc = static_cast<TZ>(vc.gp.omega_c);
+    const int nu1 = vc.gp.nu_at(1);
+    exchange([&](Slab& S) { return RES(S); });
+    for (int s = 0; s < nloc; ++s) {
+      Slab& S = slabs[s];
+      launch_restrict_own<TZ>(view1(S), S.map.as<int>(), S.P.zbase, S.P.nzl, r, RES(S), B1(S), dst, c->stream);
+      launch_jacobi_first<TZ, TZ>(view1(S), B1(S), XA1(S), wc, dst, c->stream);
+      cur1[s] = XA1(S);
+      oth1[s] = XB1(S);
+    }
+    auto sweep1 = [&](int mode) {  // mode 0: cur1 -> oth1 (swap); 1: cur1 -> RES1
+      exchange1(cur1);
+      for (int s = 0; s < nloc; ++s) {
+        Slab& S = slabs[s];
+        launch_level_sweep<TZ, TZ>(view1(S), false, B1(S), cur1[s], mode == 1 ? RES1(S) : oth1[s], wc, mode, dst,
+                                   vc.partials, init, apply_grid(S.P1.c1 - S.P1.c0, c->num_sms), c->stream);
+        if (mode == 0) std::swap(cur1[s], oth1[s]);
+      }
+    };
+    for (int k = 1; k < nu1; ++k) sweep1(0);
+    sweep1(1);
+    TZ* b2 = vc.b[2];
+    CK(cudaMemsetAsync(b2, 0, static_cast<size_t>(18) * c->gmg[1].ld * sizeof(TZ), c->stream));
+    for (int s = 0; s < nloc; ++s)
+      launch_restrict_partial<TZ>(vc.view[2], view1(slabs[s]), RES1(slabs[s]), b2, dst, c->stream);
+    if (dist) comm->allreduce(b2, 18 * static_cast<size_t>(c->gmg[1].ld), sizeof(TZ) == 8, c->stream);
+    TZ* x2 = vc.level(2, nullptr, init);  // levels 2.., replicated
+    for (int s = 0; s < nloc; ++s) launch_prolong<TZ>(view1(slabs[s]), vc.view[2], x2, cur1[s], dst, c->stream);
+    for (int k = 1; k <= nu1; ++k) sweep1(0);
+    exchange1(cur1);
+    for (int s = 0; s < nloc; ++s) {
+      Slab& S = slabs[s];
+      launch_prolong<TZ>(fine_view(S, nullptr), vc.view[1], cur1[s], cur[s], dst, c->stream);
+    }
+  };
   // z = M r: the V-cycle with level 0 on the slabs
   auto precondition_all = [&](int init) {
     const TZ w = static_cast<TZ>(vc.gp.omega);
@@ -525,20 +664,25 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     };
     for (int k = 1; k < nu; ++k) sweep_all(0);
     sweep_all(1);
-    // restriction of the owned fine residuals, summed over slabs / ranks
-    TZ* b1 = vc.b[1];
-    const auto& C1 = vc.view[1];
-    CK(cudaMemsetAsync(b1, 0, static_cast<size_t>(18) * c->gmg[0].ld * sizeof(TZ), c->stream));
-    for (int s = 0; s < nloc; ++s) {
-      Slab& S = slabs[s];
-      launch_restrict_slab<TZ>(C1, S.map.as<int>(), S.P.zbase, S.P.nzl, S.P.z0, S.P.z1, r, RES(S), b1, dst,
-                               c->stream);
-    }
-    if (dist) comm->allreduce(b1, 18 * static_cast<size_t>(c->gmg[0].ld), sizeof(TZ) == 8, c->stream);
-    TZ* x1 = vc.level(1, nullptr, init);  // coarse levels, replicated
-    for (int s = 0; s < nloc; ++s) {
-      Slab& S = slabs[s];
-      launch_prolong<TZ>(fine_view(S, nullptr), C1, x1, cur[s], dst, c->stream);
+    if (dist1) {
+      level1_slabs(init);
+    } else {
+      // restriction of the owned fine residuals, summed over slabs / ranks,
+      // into the replicated coarse levels
+      TZ* b1 = vc.b[1];
+      const auto& C1 = vc.view[1];
+      CK(cudaMemsetAsync(b1, 0, static_cast<size_t>(18) * c->gmg[0].ld * sizeof(TZ), c->stream));
+      for (int s = 0; s < nloc; ++s) {
+        Slab& S = slabs[s];
+        launch_restrict_slab<TZ>(C1, S.map.as<int>(), S.P.zbase, S.P.nzl, S.P.z0, S.P.z1, r, RES(S), b1, dst,
+                                 c->stream);
+      }
+      if (dist) comm->allreduce(b1, 18 * static_cast<size_t>(c->gmg[0].ld), sizeof(TZ) == 8, c->stream);
+      TZ* x1 = vc.level(1, nullptr, init);  // coarse levels, replicated
+      for (int s = 0; s < nloc; ++s) {
+        Slab& S = slabs[s];
+        launch_prolong<TZ>(fine_view(S, nullptr), C1, x1, cur[s], dst, c->stream);
+      }
     }
     for (int k = 1; k <= nu; ++k) {
       if (k < nu) {

@@ -108,6 +108,7 @@ struct GmgLevelView {
   int r, n, zero_slot;
   TV ridge;
   int zbase = 0;             // level 0 of a z-slab: global z of local node-map plane 0
+  int n0 = 0;                // sweeps / Jacobi / prolongation cover nodes [n0, n) (a slab's own level-1 planes)
   double* totals = nullptr;  // non-null: the last sweep writes its 6 r.z sums here (slabs)
   BrickView bricks{};        // level 0 with brick numbering: staged brick sweeps
 };
@@ -119,6 +120,16 @@ void launch_coarse_flags(const int* map_f, int r_f, int r_c, int* flag_c, cudaSt
 template <typename TV>
 void launch_restrict_slab(const GmgLevelView<TV>& C, const int* map_s, int zbase, int nzl, int z0, int z1, int r_f,
                           const TV* res_f, TV* b_c, const PcgState* st, cudaStream_t s);
+// b_c += P^T res_f over the fine nodes [F.n0, F.n) only (a slab's own level-1
+// nodes; the slabs' / ranks' partial sums add up to the full restriction)
+template <typename TV>
+void launch_restrict_partial(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
+                             const PcgState* st, cudaStream_t s);
+// b_c = P^T res on the coarse nodes [C.n0, C.n) a slab owns, from its level-0
+// residual (local node map over planes zbase.., ghost planes exchanged first)
+template <typename TV>
+void launch_restrict_own(const GmgLevelView<TV>& C, const int* map_s, int zbase, int nzl, int r_f, const TV* res_f,
+                         TV* b_c, const PcgState* st, cudaStream_t s);
 // cross-slab finalize of the multigrid update (r.r only) and of the last sweep's r.z
 void launch_finalize_update_gmg(PcgState* st, const double* totals, int nslab, int init, cudaStream_t s);
 // set a graph WHILE node's condition to !st->stop (the solve loop runs on the device)

@@ -308,11 +308,16 @@ def test_zslab_matches_single_device(S, r, G, prec, tol):
 
 
 @pytest.mark.parametrize("r,G,prec,tol", [(32, 2, "fp64", 1e-10), (64, 3, "mixed", 1e-6),
-                                          (64, 4, "fp32", 1e-5), (128, 4, "mixed", 1e-5)])
+                                          (64, 4, "fp32", 1e-5), (128, 4, "mixed", 1e-5),
+                                          (32, 3, "fp64", 1e-10), (32, 16, "fp64", 1e-10),
+                                          (16, 2, "fp64", 1e-10)])
 def test_zslab_multigrid_matches_single_device(S, r, G, prec, tol):
-    """Multigrid z-slab solve (level 0 on the slabs with ghost exchanges before
-    every sweep, restriction summed over slabs, coarse levels replicated): same
-    C^H as the undecomposed multigrid solve, iteration counts within 1."""
+    """Multigrid z-slab solve (levels 0 and 1 on the slabs with ghost exchanges
+    before every sweep, the level-2 restriction summed over slabs, levels >= 2
+    replicated; with only one coarse level it stays replicated): same C^H as the
+    undecomposed multigrid solve, iteration counts within 1.  G = 3 at r = 32
+    puts slab boundaries on odd planes; G = r/2 leaves each slab two fine
+    planes and one level-1 plane."""
     d = S.random_design(S.RandomDesignSpec("cubic_octant", 8), 3)
     opt = S.HomogenizeOptions(residual_tol=tol, precision=prec, preconditioner="gmg")
     ref = S.homogenize(d, S.ShellParams(), S.BaseMaterial(), r, opt)
