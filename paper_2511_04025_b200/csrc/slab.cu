@@ -244,6 +244,7 @@ struct SlabPlan {
 // every slab's full-length level-1 vectors.
 struct Level1Plan {
   int c0 = 0, c1 = 0;          // owned ids
+  int planes = 0;              // owned planes cz1 - cz0
   int first_n = 0, last0 = 0;  // owned plane cz0: [c0, c0 + first_n); plane cz1-1: [last0, c1)
   int glo0 = 0, glo_n = 0;     // ghost plane cz0-1
   int ghi0 = 0, ghi_n = 0;     // ghost plane cz1
@@ -476,6 +477,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
       const int glo = (cz0 - 1 + rc) % rc, ghi = cz1 % rc;
       Q.c0 = ps[cz0];
       Q.c1 = ps[cz1];
+      Q.planes = cz1 - cz0;
       Q.first_n = ps[cz0 + 1] - ps[cz0];
       Q.last0 = ps[cz1 - 1];
       Q.glo0 = ps[glo];
@@ -560,6 +562,18 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     v.totals = tot_s;
     return v;
   };
+  // A slab's own ids are plane-ordered: the interior planes read no ghost value
+  // and run while the ghost planes are in flight (the exchange's `during`),
+  // the first and last planes after the unpack.
+  struct NodeRanges {
+    int lo0, lo1, in0, in1, hi0, hi1;
+  };
+  auto node_ranges = [](int a0, int a1, int first_n, int last0, bool one_plane) {
+    return one_plane ? NodeRanges{a0, a1, a1, a1, a1, a1} : NodeRanges{a0, a0 + first_n, a0 + first_n, last0, last0, a1};
+  };
+  auto ranges0 = [&](const Slab& S) {
+    return node_ranges(0, S.P.n_owned, S.P.cnt_first, S.P.n_owned - S.P.cnt_last, S.P.z1 - S.P.z0 == 1);
+  };
   std::vector<TZ*> cur(nloc), oth(nloc);
   // level-1 vectors of slab s: b, x (two buffers), residual
   const size_t ld1 = dist1 ? static_cast<size_t>(c->gmg[0].ld) : 0;
@@ -577,9 +591,10 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
   // ghost-plane exchange of a level-1 vector: each slab's boundary planes
   // become its neighbours' ghost planes (same ids in every slab's vector)
   std::vector<TZ*> cur1(nloc), oth1(nloc);
-  auto exchange1 = [&](std::vector<TZ*>& v) {
+  auto exchange1 = [&](std::vector<TZ*>& v, const std::function<void()>& during = {}) {
     TZ* buf = xfer.as<TZ>();
     if (!dist) {
+      if (during) during();
       for (int s = 0; s < nloc; ++s) {
         const Level1Plan& Q = slabs[s].P1;
         TZ* lo = v[(s - 1 + nloc) % nloc];
@@ -598,7 +613,7 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
     launch_pack<TZ>(v[0], Q.c0, Q.first_n, send_lo, c->stream);
     comm->exchange(send_hi, 18 * static_cast<size_t>(Q.c1 - Q.last0), send_lo, 18 * static_cast<size_t>(Q.first_n),
                    recv_lo, 18 * static_cast<size_t>(Q.glo_n), recv_hi, 18 * static_cast<size_t>(Q.ghi_n),
-                   sizeof(TZ) == 8, c->stream, {});
+                   sizeof(TZ) == 8, c->stream, during);
     launch_unpack<TZ>(v[0], Q.glo0, Q.glo_n, recv_lo, c->stream);
     launch_unpack<TZ>(v[0], Q.ghi0, Q.ghi_n, recv_hi, c->stream);
   };
@@ -620,11 +635,25 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
       oth1[s] = XB1(S);
     }
     auto sweep1 = [&](int mode) {  // mode 0: cur1 -> oth1 (swap); 1: cur1 -> RES1
-      exchange1(cur1);
-      for (int s = 0; s < nloc; ++s) {
+      auto run = [&](int s, int a, int b) {
         Slab& S = slabs[s];
-        launch_level_sweep<TZ, TZ>(view1(S), false, B1(S), cur1[s], mode == 1 ? RES1(S) : oth1[s], wc, mode, dst,
-                                   vc.partials, init, apply_grid(S.P1.c1 - S.P1.c0, c->num_sms), c->stream);
+        auto V = view1(S);
+        V.n0 = a;
+        V.n = b;
+        if (b > a)
+          launch_level_sweep<TZ, TZ>(V, false, B1(S), cur1[s], mode == 1 ? RES1(S) : oth1[s], wc, mode, dst,
+                                     vc.partials, init, apply_grid(b - a, c->num_sms), c->stream);
+      };
+      auto rg = [&](int s) {
+        const Level1Plan& Q = slabs[s].P1;
+        return node_ranges(Q.c0, Q.c1, Q.first_n, Q.last0, Q.planes == 1);
+      };
+      exchange1(cur1, [&] {
+        for (int s = 0; s < nloc; ++s) run(s, rg(s).in0, rg(s).in1);
+      });
+      for (int s = 0; s < nloc; ++s) {
+        run(s, rg(s).lo0, rg(s).lo1);
+        run(s, rg(s).hi0, rg(s).hi1);
         if (mode == 0) std::swap(cur1[s], oth1[s]);
       }
     };
@@ -653,12 +682,22 @@ void run_solve_slabs(shl_ctx* c, const double* K0, const shl_solve_options& opt,
       oth[s] = XB(slabs[s]);
     }
     auto sweep_all = [&](int mode) {  // mode 0: cur -> oth (swap); 1: cur -> RES
-      exchange([&](Slab& S) { return cur[&S - slabs.data()]; });
-      for (int s = 0; s < nloc; ++s) {
+      auto run = [&](int s, int a, int b) {
         Slab& S = slabs[s];
-        const auto V = fine_view(S, nullptr);
-        launch_level_sweep<TX, TZ>(V, true, R(S), cur[s], mode == 1 ? RES(S) : oth[s], w, mode, dst,
-                                   S.partials.as<double>(), init, apply_grid(S.P.n_owned, c->num_sms), c->stream);
+        auto V = fine_view(S, nullptr);
+        V.n0 = a;
+        V.n = b;
+        if (b > a)
+          launch_level_sweep<TX, TZ>(V, true, R(S), cur[s], mode == 1 ? RES(S) : oth[s], w, mode, dst,
+                                     S.partials.as<double>(), init, apply_grid(b - a, c->num_sms), c->stream);
+      };
+      exchange([&](Slab& S) { return cur[&S - slabs.data()]; },
+               [&] {
+                 for (int s = 0; s < nloc; ++s) run(s, ranges0(slabs[s]).in0, ranges0(slabs[s]).in1);
+               });
+      for (int s = 0; s < nloc; ++s) {
+        run(s, ranges0(slabs[s]).lo0, ranges0(slabs[s]).lo1);
+        run(s, ranges0(slabs[s]).hi0, ranges0(slabs[s]).hi1);
         if (mode == 0) std::swap(cur[s], oth[s]);
       }
     };
