@@ -479,10 +479,15 @@ __global__ void jacobi_first_kernel(const int* __restrict__ node_list, const TV*
 // b_c(N) = sum_{n in supp(N)} w(n,N) res_f(n), w = prod over axes (1 | 1/2)
 // (f1 > 0: only fine ids in [f0, f1) contribute and b_c accumulates -- the
 // partial restriction of a z-slab's owned level-1 nodes, summed over slabs)
+// (x_c != nullptr: also the coarse level's first damped Jacobi sweep from
+// x = 0, x_c = omega Dinv b_c -- jacobi_first_kernel fused into the
+// restriction that produces b_c, same arithmetic)
 template <typename TV>
 __global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c,
                                 const int* __restrict__ map_f, int r_f, const TV* __restrict__ res_f,
-                                TV* __restrict__ b_c, const PcgState* st, int f0 = 0, int f1 = 0) {
+                                TV* __restrict__ b_c, const PcgState* st, int f0 = 0, int f1 = 0,
+                                const TV* __restrict__ dinv_c = nullptr, TV* __restrict__ x_c = nullptr,
+                                TV omega = TV(0)) {
   pdl_wait();
   if (st->stop) return;
   int idx, s;
@@ -524,6 +529,14 @@ __global__ void restrict_kernel(const int* __restrict__ list_c, int n_c, int r_c
     b_c[oc] = acc[0];
     b_c[oc + 192] = acc[1];
     b_c[oc + 384] = acc[2];
+    if (x_c) {
+      TV D[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) D[q] = dinv_c[vbase(idx, 6) + q * 32];
+      x_c[oc] = omega * (D[0] * acc[0] + D[1] * acc[1] + D[2] * acc[2]);
+      x_c[oc + 192] = omega * (D[1] * acc[0] + D[3] * acc[1] + D[4] * acc[2]);
+      x_c[oc + 384] = omega * (D[2] * acc[0] + D[4] * acc[1] + D[5] * acc[2]);
+    }
   }
 }
 
@@ -1064,10 +1077,10 @@ bool launch_coarsest(const GmgLevelView<TV>& L, const TV* b, TV* x, TV omega, in
 
 template <typename TV>
 void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
-                     const PcgState* st, cudaStream_t s) {
+                     const PcgState* st, cudaStream_t s, TV* x_c, TV omega) {
   if (C.n)
     launch_pdl(restrict_kernel<TV>, node_case_blocks(C.n, 192), 192, 0, s, C.node_list, C.n, C.r, F.node_map, F.r,
-               res_f, b_c, st, 0, 0);
+               res_f, b_c, st, 0, 0, static_cast<const TV*>(C.dinv), x_c, omega);
 }
 
 template <typename TV>
@@ -1075,7 +1088,8 @@ void launch_restrict_partial(const GmgLevelView<TV>& C, const GmgLevelView<TV>& 
                              const PcgState* st, cudaStream_t s) {
   if (C.n)
     launch_pdl(restrict_kernel<TV>, node_case_blocks(C.n, 192), 192, 0, s, C.node_list, C.n, C.r, F.node_map, F.r,
-               res_f, b_c, st, F.n0, std::max(F.n, 1));
+               res_f, b_c, st, F.n0, std::max(F.n, 1), static_cast<const TV*>(nullptr), static_cast<TV*>(nullptr),
+               TV(0));
 }
 
 template <typename TV>
@@ -1107,7 +1121,7 @@ void launch_prolong(const GmgLevelView<TV>& F, const GmgLevelView<TV>& C, const 
                                     cudaStream_t);                                                     \
   template void launch_coarse_dinv<TV>(const int*, int, const TV*, TV*, int, cudaStream_t);            \
   template void launch_restrict<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,  \
-                                    const PcgState*, cudaStream_t);                                   \
+                                    const PcgState*, cudaStream_t, TV*, TV);                          \
   template void launch_prolong<TV>(const GmgLevelView<TV>&, const GmgLevelView<TV>&, const TV*, TV*,   \
                                    const PcgState*, cudaStream_t);                                   \
   template bool launch_coarsest<TV>(const GmgLevelView<TV>&, const TV*, TV*, TV, int, const PcgState*, \

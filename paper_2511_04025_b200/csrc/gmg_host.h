@@ -131,7 +131,9 @@ struct Vcycle {
 
   int grid(int n) const { return shl::apply_grid(n, c->num_sms); }
 
-  TV* level(int l, const TX* b0, int init) {
+  // first_done: the restriction into b[l] already wrote x = omega Dinv b[l]
+  // into xa[l] (restrict_kernel's fused first sweep)
+  TV* level(int l, const TX* b0, int init, bool first_done = false) {
     const auto& V = view[l];
     const bool fine = l == 0;
     const TV w = static_cast<TV>(fine ? gp.omega : gp.omega_c);
@@ -149,7 +151,7 @@ struct Vcycle {
       ++launches;
       return cur;
     }
-    if (!fine) {
+    if (!fine && !first_done) {
       shl::launch_jacobi_first<TV, TV>(V, b[l], cur, w, st, s);
       ++launches;
     }  // level 0: the update kernel already wrote w Dinv r into xa[0]
@@ -161,8 +163,12 @@ struct Vcycle {
     }
     if (l == L) return cur;
     sweep(cur, res[l], 1);
-    shl::launch_restrict<TV>(view[l + 1], V, res[l], b[l + 1], st, s);
-    TV* xc = level(l + 1, b0, init);
+    // the child's first sweep rides on the restriction, except on an 8^3
+    // coarsest level (its cluster kernel starts from b itself)
+    const bool fuse = !(l + 1 == L && view[l + 1].r == 8);
+    shl::launch_restrict<TV>(view[l + 1], V, res[l], b[l + 1], st, s, fuse ? xa[l + 1] : nullptr,
+                             static_cast<TV>(gp.omega_c));
+    TV* xc = level(l + 1, b0, init, fuse);
     shl::launch_prolong<TV>(V, view[l + 1], xc, cur, st, s);
     launches += 2;
     for (int k = 1; k <= nu; ++k) {

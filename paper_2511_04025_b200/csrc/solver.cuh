@@ -155,7 +155,8 @@ void launch_jacobi_first(const GmgLevelView<TV>& L, const TB* b, TV* xout, TV om
                          cudaStream_t s);
 template <typename TV>
 void launch_restrict(const GmgLevelView<TV>& C, const GmgLevelView<TV>& F, const TV* res_f, TV* b_c,
-                     const PcgState* st, cudaStream_t s);
+                     const PcgState* st, cudaStream_t s, TV* x_c = nullptr,
+                     TV omega = TV(0));
 // The whole coarsest-level solve in one cluster kernel (8^3 torus, FP32);
 // false when the level does not qualify.
 template <typename TV>
