@@ -253,22 +253,6 @@ __device__ __forceinline__ void brick_gather(TS (&y)[18], const TX* __restrict__
   gather_class<1, TS, TX>(y, xs, bs, pc, ec, kNbCorner, 27);
 }
 
-// Last CTA: fixed-order sum of the nab per-brick partials.
-__device__ __forceinline__ bool brick_last_sum(uint32_t* counter, const double* partials, int nab, double (&tot)[6],
-                                               double* scratch) {
-  __shared__ bool last;
-  if (threadIdx.x == 0) last = arrive_last(counter);  // (thread 0 wrote the brick's partials)
-  __syncthreads();
-  if (!last) return false;
-#pragma unroll
-  for (int q = 0; q < 6; ++q) tot[q] = 0.0;
-  for (int t = threadIdx.x; t < nab; t += blockDim.x)
-#pragma unroll
-    for (int q = 0; q < 6; ++q) tot[q] += __ldcg(partials + t * 6 + q);
-  block_sum<6>(tot, scratch);
-  return true;
-}
-
 // Staging, split so that it pipelines across a CTA's bricks:
 //   stage_ids   -- the node ids of the region positions this thread stages
 //                  (plain loads into registers, consumed one brick later),
@@ -357,7 +341,7 @@ __device__ __forceinline__ void brick_reduce6(double (&v)[6], double* red, doubl
     if (lane == 0) red[w * 6 + s] = v[s];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // (one thread: its writes are what brick_last_sum's release publishes)
+  if (threadIdx.x == 0) {  // (summed after the kernel by brick_sum_kernel)
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       double tot = 0.0;
@@ -420,16 +404,7 @@ __global__ void __launch_bounds__(kThreads, MINB) brick_apply_kernel(const Apply
     }
     brick_reduce6(pq, C.red, A.partials, t);
   });
-  double tot[6];
-  if (!brick_last_sum(&st->counter_apply, A.partials, B.nab, tot, scratch)) return;
-  if (threadIdx.x == 0) {
-    if (A.defer) {
-      for (int s = 0; s < 6; ++s) A.totals[s] = tot[s];
-    } else {
-      finalize_apply_state(st, tot);
-    }
-    st->counter_apply = 0;
-  }
+  (void)scratch;  // (p.q is summed by brick_sum_kernel, launched after this one)
 }
 
 // ---- level-0 V-cycle sweep on bricks ---------------------------------------------
@@ -496,16 +471,37 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
     if (mode == 2) brick_reduce6(gam, C.red, partials, t);
   });
-  if (mode != 2) return;
-  double tot[6];
-  if (!brick_last_sum(&st->counter_misc, partials, B.nab, tot, scratch)) return;
+  // (mode 2: r.z is summed by brick_sum_kernel, launched after this one)
+  (void)scratch;
+  (void)init;
+}
+
+// The per-brick partials of the apply (p.q) or of the V-cycle's last level-0
+// sweep (r.z) summed in brick order by ONE CTA launched right after the brick
+// kernel (programmatic dependent launch), then the PCG scalars (alpha / beta)
+// or, for a deferred sum, the 6 totals.  Round 1/2 let the last brick CTA to
+// arrive on an atomic counter do this; the arrival's L2 round trip and two
+// barriers at the end of EVERY brick CTA cost more than this launch (final
+// sweep 148 vs 106 us for the same sweep without a reduction; 773 vs 791 us
+// per PCG iteration for the sweep alone).
+__global__ void __launch_bounds__(512) brick_sum_kernel(const double* __restrict__ partials, int nab, PcgState* st,
+                                                        int kind, int init, double* totals) {
+  pdl_wait();
+  __shared__ double scratch[32 * 6];
+  if (st->stop) return;
+  double tot[6] = {0, 0, 0, 0, 0, 0};
+  for (int t = threadIdx.x; t < nab; t += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) tot[q] += partials[t * 6 + q];
+  block_sum<6>(tot, scratch);
   if (threadIdx.x == 0) {
-    if (L.totals) {
-      for (int q = 0; q < 6; ++q) L.totals[q] = tot[q];
+    if (totals) {
+      for (int q = 0; q < 6; ++q) totals[q] = tot[q];
+    } else if (kind == 0) {
+      finalize_apply_state(st, tot);
     } else {
       finalize_gamma_state(st, tot, init);
     }
-    st->counter_misc = 0;
   }
 }
 
@@ -692,6 +688,8 @@ void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s) {
   static const bool configured = brick_configure(brick_apply_kernel<TV, TZ, kMinB>, smem);
   (void)configured;
   launch_pdl(brick_apply_kernel<TV, TZ, kMinB>, a.bricks.nab, kThreads, smem, s, a);
+  launch_pdl(brick_sum_kernel, 1, 512, 0, s, static_cast<const double*>(a.partials), a.bricks.nab, a.state, 0, 0,
+             a.defer ? a.totals : static_cast<double*>(nullptr));
 }
 
 // Level-0 sweep: one CTA per active brick.
@@ -704,6 +702,9 @@ void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, T
   (void)configured;
   launch_pdl(brick_sweep_kernel<TB, TV, TO, kMinB>, L.bricks.nab, kThreads, smem, s, L, b, xin, xout, omega, mode,
              st, partials, init);
+  if (mode == 2)
+    launch_pdl(brick_sum_kernel, 1, 512, 0, s, static_cast<const double*>(partials), L.bricks.nab, st, 1, init,
+               L.totals);
 }
 
 // Stored-level sweep on the level's active bricks (FP32 levels).

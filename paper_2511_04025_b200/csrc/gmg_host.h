@@ -174,7 +174,7 @@ struct Vcycle {
     for (int k = 1; k <= nu; ++k) {
       if (fine && k == nu) {
         shl::launch_level_sweep_out<TX, TV, TO>(V, b0, cur, zout, w, st, partials, init, grid(V.n), s);
-        ++launches;
+        launches += V.bricks.nab > 0 ? 2 : 1;  // (brick sweep + its r.z reduction)
         return nullptr;
       }
       sweep(cur, oth, 0);

@@ -392,7 +392,9 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   precondition(1);
   shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
   ua.init = 0;
-  int64_t launches = 2 + 2;
+  // kernels per update + apply (the brick apply is followed by its p.q sum)
+  const int it_kernels = 1 + (aa.bricks.nab > 0 ? 2 : 1);
+  int64_t launches = 2 + it_kernels;
   int check = opt.check_every > 0 ? opt.check_every : (n < 200000 ? 16 : 32);
 #ifdef SHL_DEV_TRACE  // dev build only: per-iteration scalars on stderr
   constexpr bool trace = true;
@@ -443,7 +445,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
             shl::launch_update<TX, TV, TZ>(ua, grid_u, cs);
             precondition(0);
             shl::launch_apply<TV, TZ>(aa, grid_a, cs);
-            launches += 2;
+            launches += it_kernels;
           }
           shl::launch_set_while(h, dst, cs);
           vc.s = c->stream;
@@ -464,7 +466,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
         shl::launch_update<TX, TV, TZ>(ua, grid_u, cs);
         precondition(0);
         shl::launch_apply<TV, TZ>(aa, grid_a, cs);
-        launches += 2;
+        launches += it_kernels;
       }
       vc.s = c->stream;
       CK(cudaStreamEndCapture(cs, &graph));
@@ -472,8 +474,8 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
     CK(cudaGraphInstantiate(&gexec, graph, 0));
     CK(cudaGraphDestroy(graph));
     graph_launches = launches + vc.launches - before;
-    launches -= 2 * kGraphIters;  // counted per replay below
-    vc.launches -= graph_launches - 2 * kGraphIters;
+    launches -= it_kernels * kGraphIters;  // counted per replay below
+    vc.launches -= graph_launches - it_kernels * kGraphIters;
   }
   struct GraphGuard {
     cudaGraphExec_t g;
@@ -520,7 +522,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
           shl::launch_apply<TV, TZ>(aa, grid_a, c->stream);
         }
         ++issued;
-        launches += 2;
+        launches += it_kernels;
       }
     }
     CK(cudaGetLastError());
