@@ -484,15 +484,31 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // barriers at the end of EVERY brick CTA cost more than this launch (final
 // sweep 148 vs 106 us for the same sweep without a reduction; 773 vs 791 us
 // per PCG iteration for the sweep alone).
-__global__ void __launch_bounds__(512) brick_sum_kernel(const double* __restrict__ partials, int nab, PcgState* st,
-                                                        int kind, int init, double* totals) {
+constexpr int kSumThreads = 1024;
+__global__ void __launch_bounds__(kSumThreads) brick_sum_kernel(const double* __restrict__ partials, int nab,
+                                                                PcgState* st, int kind, int init, double* totals) {
   pdl_wait();
   __shared__ double scratch[32 * 6];
   if (st->stop) return;
   double tot[6] = {0, 0, 0, 0, 0, 0};
-  for (int t = threadIdx.x; t < nab; t += blockDim.x)
+  // four bricks' loads in flight per thread (16-byte loads), then the adds
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(partials);
+  for (int t0 = threadIdx.x; t0 < nab; t0 += 4 * kSumThreads) {
+    double2 v[4][3];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) tot[q] += partials[t * 6 + q];
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * kSumThreads;
+#pragma unroll
+      for (int h = 0; h < 3; ++h) v[u][h] = t < nab ? __ldcg(p2 + t * 3 + h) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 3; ++h) {
+        tot[2 * h] += v[u][h].x;
+        tot[2 * h + 1] += v[u][h].y;
+      }
+  }
   block_sum<6>(tot, scratch);
   if (threadIdx.x == 0) {
     if (totals) {
@@ -688,7 +704,7 @@ void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s) {
   static const bool configured = brick_configure(brick_apply_kernel<TV, TZ, kMinB>, smem);
   (void)configured;
   launch_pdl(brick_apply_kernel<TV, TZ, kMinB>, a.bricks.nab, kThreads, smem, s, a);
-  launch_pdl(brick_sum_kernel, 1, 512, 0, s, static_cast<const double*>(a.partials), a.bricks.nab, a.state, 0, 0,
+  launch_pdl(brick_sum_kernel, 1, kSumThreads, 0, s, static_cast<const double*>(a.partials), a.bricks.nab, a.state, 0, 0,
              a.defer ? a.totals : static_cast<double*>(nullptr));
 }
 
@@ -703,7 +719,7 @@ void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, T
   launch_pdl(brick_sweep_kernel<TB, TV, TO, kMinB>, L.bricks.nab, kThreads, smem, s, L, b, xin, xout, omega, mode,
              st, partials, init);
   if (mode == 2)
-    launch_pdl(brick_sum_kernel, 1, 512, 0, s, static_cast<const double*>(partials), L.bricks.nab, st, 1, init,
+    launch_pdl(brick_sum_kernel, 1, kSumThreads, 0, s, static_cast<const double*>(partials), L.bricks.nab, st, 1, init,
                L.totals);
 }
 
