@@ -76,7 +76,10 @@ __device__ __forceinline__ void stencil_gather_plane(GatherAcc<TV>& acc, int idx
 
 // level_sweep_kernel latency-split three ways: three warps per 32 nodes, warp p
 // gathers plane dz=p-1, warp p then finishes load-case pair p (gather3_tile).
-template <typename TB, typename TV, bool kFine, typename TO = TV>
+// kQueue: CTAs take 64-node tiles from the shared counter (level 0 of the
+// z-slabs); otherwise one CTA per tile (grid = tiles: the stored levels, no
+// tile atomics, and lanes cannot leave a CTA with a late full share).
+template <typename TB, typename TV, bool kFine, typename TO = TV, bool kQueue = kFine>
 __global__ void __launch_bounds__(192)
     level_sweep3_kernel(const LevelArgs<TV> L, const TB* __restrict__ b, const TV* __restrict__ xin,
                         TO* __restrict__ xout, TV omega, int mode, PcgState* st, double* partials,
@@ -93,9 +96,9 @@ __global__ void __launch_bounds__(192)
   __shared__ double red[2][6];
   __shared__ int tq_slot[2];
   TileQueue tq{&st->tile_next[1], tq_slot};
-  for (int tile = tq.first();; tile = tq.advance()) {
+  for (int tile = kQueue ? tq.first() : static_cast<int>(blockIdx.x);; tile = tq.advance()) {
     if (L.n0 + tile * 64 >= L.n) break;
-    tq.request();
+    if (kQueue) tq.request();
     gam2[0] = gam2[1] = 0.0;
     const int idx = L.n0 + tile * 64 + grp * 32 + lane;
     const bool valid = idx < L.n;
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(192)
 #pragma unroll
       for (int q = 0; q < 18; ++q) part_s[grp][(part * 18 + q) * 32 + lane] = acc.get(q);
     }
-    tq.publish();
+    if (kQueue) tq.publish();
     __syncthreads();
     if (valid) {
       const size_t ob = vbase(idx, 18);
@@ -173,7 +176,9 @@ __global__ void __launch_bounds__(192)
     }
     __syncthreads();
     if (mode == 2 && threadIdx.x < 6) partials[tile * 6 + threadIdx.x] = red[0][threadIdx.x] + red[1][threadIdx.x];
+    if (!kQueue) break;
   }
+  if (!kQueue) return;  // (stored levels: mode 0 / 1 only)
   tiles_done(&st->tile_next[1], &st->tile_done[1]);
   if (mode != 2) return;
   __shared__ bool last;
@@ -1026,7 +1031,8 @@ void launch_level_sweep(const GmgLevelView<TV>& L, bool fine, const TB* b, const
   if (fine) {
     launch_pdl(level_sweep3_kernel<TB, TV, true>, grid, 192, 0, s, a, b, xin, xout, omega, mode, st, partials, init);
   } else if (L.n - L.n0 > 32768) {  // large stored level: thread per node is throughput-bound
-    launch_pdl(level_sweep3_kernel<TB, TV, false>, grid, 192, 0, s, a, b, xin, xout, omega, mode, st, partials, init);
+    launch_pdl(level_sweep3_kernel<TB, TV, false>, (L.n - L.n0 + 63) / 64, 192, 0, s, a, b, xin, xout, omega, mode, st,
+               partials, init);
   } else {  // small stored level: latency-bound, one warp per node (mode 2 is level-0 only)
     launch_pdl(coarse_warp_sweep_kernel<TV>, std::max(1, (L.n - L.n0 + 7) / 8), 256, 0, s, a,
                reinterpret_cast<const TV*>(b), xin, xout, omega, mode, st);
