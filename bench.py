@@ -55,8 +55,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=4)
     p.add_argument("--lanes", type=int, default=0,
                    help="designs in flight at once per GPU (shl_set_batch_lanes); 0 = auto: the warm-up "
-                        "runs its designs with 1, 2 and 3 lanes and the timed region uses the fastest "
-                        "(more lanes fill the GPU's idle time inside a design's V-cycle, DESIGN.md 4.2)")
+                        "runs its designs with 1 and 2 lanes and the timed region uses the faster "
+                        "(a second lane fills the GPU's idle time inside a design's V-cycle, DESIGN.md 4.2)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--r", type=int, default=128)
     p.add_argument("--tol", type=float, default=1e-5)
@@ -81,7 +81,7 @@ def config(args, world):
             "rtol": args.tol, "precision": args.precision, "preconditioner": args.preconditioner,
             "global_batch": world,
             "designs_per_rank_per_step": 1, "parallelism": f"design-sharded x{world}",
-            "designs_in_flight_per_gpu": args.lanes if args.lanes > 0 else "auto (1-3, chosen in the warm-up)",
+            "designs_in_flight_per_gpu": args.lanes if args.lanes > 0 else "auto (1 or 2, chosen in the warm-up)",
             "timed_region": f"one shl_homogenize_batch call over {args.steps} designs per rank, "
                             f"{args.lanes if args.lanes > 0 else 'auto'} lanes (streams + host threads) in flight",
             "l2": "inputs larger than L2 (solver working set ~300 MB per design, new design each step)"}
@@ -307,16 +307,19 @@ def run_ours(args, rank, world, local):
     if args.lanes > 0:
         S.homogenize_batch(warm_designs, sp, mat, args.r, opt, ctx=ctx, lanes=args.lanes)
     else:
-        # auto: time the same warm-up designs with one, two and three designs in
-        # flight and keep the fastest for the timed region, so a box where the
-        # lanes contend falls back to fewer.  A multiple of 6 designs (>= 6), a
-        # first pass that sizes every lane's workspaces, then the settings
-        # alternated twice, best of each.
-        n_trial = max(6, -(-len(warm_designs) // 6) * 6)
+        # auto: time the same warm-up designs with one and two designs in flight
+        # and keep the faster for the timed region, so a box where the lanes
+        # contend falls back to one.  (Three lanes won the 6-design trial but
+        # fell into a setup-starved mode in 2 of 3 timed runs, 27.8 designs/s;
+        # DESIGN.md 4.2.)  An even number (>= 6) of designs, a first pass that
+        # sizes both lanes' workspaces, then the settings alternated twice,
+        # best of each.
+        LANE_CHOICES = (1, 2)
+        n_trial = max(6, len(warm_designs) + len(warm_designs) % 2)
         trial_designs = [S.random_design(spec, 9001 + rank * 100 + i) for i in range(n_trial)]
-        S.homogenize_batch(trial_designs, sp, mat, args.r, opt, ctx=ctx, lanes=3)
-        trial = [float("inf")] * 3
-        for lanes_try in (1, 2, 3, 1, 2, 3):
+        S.homogenize_batch(trial_designs, sp, mat, args.r, opt, ctx=ctx, lanes=max(LANE_CHOICES))
+        trial = [float("inf")] * len(LANE_CHOICES)
+        for lanes_try in LANE_CHOICES + LANE_CHOICES:
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             S.homogenize_batch(trial_designs, sp, mat, args.r, opt, ctx=ctx, lanes=lanes_try)
@@ -326,9 +329,9 @@ def run_ours(args, rank, world, local):
         tt = torch.tensor(trial, dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)  # every rank makes the same choice
-        args.lanes = 1 + min(range(3), key=lambda k: float(tt[k]))
-        lane_trials = {"warmup_designs": len(warm_designs), "wall_s_1_lane": float(tt[0]),
-                       "wall_s_2_lanes": float(tt[1]), "wall_s_3_lanes": float(tt[2]), "chosen": args.lanes}
+        args.lanes = LANE_CHOICES[min(range(len(LANE_CHOICES)), key=lambda k: float(tt[k]))]
+        lane_trials = {"warmup_designs": len(warm_designs), "chosen": args.lanes,
+                       **{f"wall_s_{L}_lanes": float(tt[k]) for k, L in enumerate(LANE_CHOICES)}}
 
     def barrier():
         torch.cuda.synchronize()
