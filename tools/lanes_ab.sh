@@ -1,4 +1,4 @@
-# dev aid: repeated bench runs at several lane counts (same box)
+# dev aid: repeated bench runs at several lane counts (same box); SHL_LIB selects a variant
 T=$1; shift
 for L in "$@"; do for i in 1 2 3; do
   python bench.py --steps 20 --warmup 5 --lanes $L --no-cpu-baseline > gpurun_out/${T}_l${L}_$i.json 2> gpurun_out/${T}_l${L}_$i.err
