@@ -756,7 +756,10 @@ struct GalerkinFineShared {
   TV B[32][64];  // [node][fine element (tz*4 + ty)*4 + tx], origin 2N - 2
 };
 template <typename TV>
-__global__ void __launch_bounds__(864) galerkin_fine_kernel(const int* __restrict__ list_c, int n_c, int r_c,
+// (grid.y = 3: each CTA computes 9 of the 27 neighbour blocks of its 32 coarse
+// nodes, 288 threads -- an 864-thread CTA waited for a nearly empty SM while
+// other batch lanes' small CTAs kept backfilling, starving the setup)
+__global__ void __launch_bounds__(288) galerkin_fine_kernel(const int* __restrict__ list_c, int n_c, int r_c,
                                                             const int* __restrict__ map_f, int r_f,
                                                             const TV* __restrict__ betav, TV ridge,
                                                             TV* __restrict__ stencil_c) {
@@ -765,8 +768,9 @@ __global__ void __launch_bounds__(864) galerkin_fine_kernel(const int* __restric
   TV* M = Sh.M;
   const TV* Mg = cell_matrices<TV>();
   const int tid = threadIdx.y * 32 + threadIdx.x;
-  for (int t = tid; t < 8 * 576; t += 864) M[t] = Mg[t];
-  for (int t = tid; t < 32 * 64; t += 864) {
+  const int nthr = blockDim.x * blockDim.y;
+  for (int t = tid; t < 8 * 576; t += nthr) M[t] = Mg[t];
+  for (int t = tid; t < 32 * 64; t += nthr) {
     const int x = t / 64, e = t % 64, id = blockIdx.x * 32 + x;
     TV v = TV(0);
     if (id < n_c) {
@@ -782,7 +786,7 @@ __global__ void __launch_bounds__(864) galerkin_fine_kernel(const int* __restric
   const int idx = blockIdx.x * 32 + threadIdx.x;
   if (idx >= n_c) return;
   const TV* Bn = Sh.B[threadIdx.x];
-  const int m = threadIdx.y;
+  const int m = blockIdx.y * blockDim.y + threadIdx.y;
   const int Dx = m % 3 - 1, Dy = (m / 3) % 3 - 1, Dz = m / 9 - 1;
   const int G = list_c[idx];
   TV S[9];
@@ -996,7 +1000,7 @@ void launch_galerkin(const int* list_c, int n_c, int r_c, const int* map_f, int 
       return true;
     }();
     (void)configured;
-    galerkin_fine_kernel<TV><<<(n_c + 31) / 32, dim3(32, 27), sizeof(GalerkinFineShared<TV>), s>>>(
+    galerkin_fine_kernel<TV><<<dim3((n_c + 31) / 32, 3), dim3(32, 9), sizeof(GalerkinFineShared<TV>), s>>>(
         list_c, n_c, r_c, map_f, r_f, beta_f, ridge, stencil_c);
   } else {
     galerkin_stored_kernel<TV><<<static_cast<unsigned>((n_c + 7) / 8), 256, 0, s>>>(list_c, n_c, r_c, map_f, r_f,
