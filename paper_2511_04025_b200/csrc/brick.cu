@@ -17,6 +17,7 @@
 //      products per brick (fixed order -> reproducible).
 // The dependent map -> vector load chain of a per-node gather becomes two
 // bulk phases per brick; the arithmetic reads shared memory only.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -484,25 +485,33 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // barriers at the end of EVERY brick CTA cost more than this launch (final
 // sweep 148 vs 106 us for the same sweep without a reduction; 773 vs 791 us
 // per PCG iteration for the sweep alone).
-constexpr int kSumThreads = 1024;
-__global__ void __launch_bounds__(kSumThreads) brick_sum_kernel(const double* __restrict__ partials, int nab,
-                                                                PcgState* st, int kind, int init, double* totals) {
+constexpr int kSumThreads = 512;
+constexpr int kSumCtas = 8;  // one portable cluster
+__global__ void __cluster_dims__(kSumCtas, 1, 1) __launch_bounds__(kSumThreads)
+    brick_sum_kernel(const double* __restrict__ partials, int nab, PcgState* st, int kind, int init,
+                     double* totals) {
+  namespace cg = cooperative_groups;
   pdl_wait();
   __shared__ double scratch[32 * 6];
-  if (st->stop) return;
+  __shared__ double cta_tot[6];
+  if (st->stop) return;  // (every CTA of the cluster sees the same flag)
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  // CTA `rank` sums the contiguous chunk of bricks [t0, t1), 16-byte loads
+  const int chunk = (nab + kSumCtas - 1) / kSumCtas;
+  const int t0 = rank * chunk, t1 = min(nab, t0 + chunk);
   double tot[6] = {0, 0, 0, 0, 0, 0};
-  // four bricks' loads in flight per thread (16-byte loads), then the adds
   const double2* __restrict__ p2 = reinterpret_cast<const double2*>(partials);
-  for (int t0 = threadIdx.x; t0 < nab; t0 += 4 * kSumThreads) {
-    double2 v[4][3];
+  for (int tb = t0 + static_cast<int>(threadIdx.x); tb < t1; tb += 2 * kSumThreads) {
+    double2 v[2][3];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int t = t0 + u * kSumThreads;
+    for (int u = 0; u < 2; ++u) {
+      const int t = tb + u * kSumThreads;
 #pragma unroll
-      for (int h = 0; h < 3; ++h) v[u][h] = t < nab ? __ldcg(p2 + t * 3 + h) : make_double2(0.0, 0.0);
+      for (int h = 0; h < 3; ++h) v[u][h] = t < t1 ? __ldcg(p2 + t * 3 + h) : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int h = 0; h < 3; ++h) {
         tot[2 * h] += v[u][h].x;
@@ -510,15 +519,24 @@ __global__ void __launch_bounds__(kSumThreads) brick_sum_kernel(const double* __
       }
   }
   block_sum<6>(tot, scratch);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 6; ++q) cta_tot[q] = tot[q];
+  cluster.sync();  // every CTA's total in its shared memory
+  if (rank == 0 && threadIdx.x == 0) {
+    double g[6] = {0, 0, 0, 0, 0, 0};
+    for (int c = 0; c < kSumCtas; ++c) {  // CTA order: fixed summation order
+      const double* ct = cluster.map_shared_rank(cta_tot, c);
+      for (int q = 0; q < 6; ++q) g[q] += ct[q];
+    }
     if (totals) {
-      for (int q = 0; q < 6; ++q) totals[q] = tot[q];
+      for (int q = 0; q < 6; ++q) totals[q] = g[q];
     } else if (kind == 0) {
-      finalize_apply_state(st, tot);
+      finalize_apply_state(st, g);
     } else {
-      finalize_gamma_state(st, tot, init);
+      finalize_gamma_state(st, g, init);
     }
   }
+  cluster.sync();  // (no CTA exits while CTA 0 may still read its total)
 }
 
 // ---- stored (Galerkin) levels on bricks ------------------------------------------
@@ -704,7 +722,7 @@ void launch_brick_apply(const ApplyArgs<TV, TZ>& a, cudaStream_t s) {
   static const bool configured = brick_configure(brick_apply_kernel<TV, TZ, kMinB>, smem);
   (void)configured;
   launch_pdl(brick_apply_kernel<TV, TZ, kMinB>, a.bricks.nab, kThreads, smem, s, a);
-  launch_pdl(brick_sum_kernel, 1, kSumThreads, 0, s, static_cast<const double*>(a.partials), a.bricks.nab, a.state, 0, 0,
+  launch_pdl(brick_sum_kernel, kSumCtas, kSumThreads, 0, s, static_cast<const double*>(a.partials), a.bricks.nab, a.state, 0, 0,
              a.defer ? a.totals : static_cast<double*>(nullptr));
 }
 
@@ -719,7 +737,7 @@ void launch_brick_sweep(const GmgLevelView<TV>& L, const TB* b, const TV* xin, T
   launch_pdl(brick_sweep_kernel<TB, TV, TO, kMinB>, L.bricks.nab, kThreads, smem, s, L, b, xin, xout, omega, mode,
              st, partials, init);
   if (mode == 2)
-    launch_pdl(brick_sum_kernel, 1, kSumThreads, 0, s, static_cast<const double*>(partials), L.bricks.nab, st, 1, init,
+    launch_pdl(brick_sum_kernel, kSumCtas, kSumThreads, 0, s, static_cast<const double*>(partials), L.bricks.nab, st, 1, init,
                L.totals);
 }
 
