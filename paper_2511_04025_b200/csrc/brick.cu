@@ -275,6 +275,7 @@ __device__ __forceinline__ void stage_ids(int (&id)[kPer], const BrickView& B, i
       const int lx = p % kRX, ly = (p / kRX) % kRY, lz = p / (kRX * kRY);
       const int gx = wrap3(x0 + lx - 1, r), gy = wrap3(y0 + ly - 1, r), gz = wrap3(z0 + lz - 1, r);
       id[j] = __ldg(nmap + (static_cast<size_t>(gz) * r + gy) * r + gx);
+      SHL_DCHECK(id[j] < 0 || B.n_nodes == 0 || id[j] < B.n_nodes);
     }
   }
 }
@@ -287,6 +288,7 @@ __device__ __forceinline__ void stage_issue(BrickShared<TS, TB>& S, const BrickV
   int x0, y0, z0;
   brick_origin(B, t, x0, y0, z0);
   const int first = __ldg(B.bstart + t), last = __ldg(B.bstart + t + 1);
+  SHL_DCHECK(t >= 0 && t < B.nab && first >= 0 && first <= last && last - first <= kNodes);
   for (int e = threadIdx.x; e < kERegion; e += kThreads) {
     const int lx = e % kEX, ly = (e / kEX) % kEY, lz = e / (kEX * kEY);
     const int gx = wrap3(x0 + lx - 1, r), gy = wrap3(y0 + ly - 1, r), gz = wrap3(z0 + lz - 1, r);
@@ -302,6 +304,7 @@ __device__ __forceinline__ void stage_issue(BrickShared<TS, TB>& S, const BrickV
     const bool inner = lx >= 1 && lx <= kBX && ly >= 1 && ly <= kBY && lz >= 1 && lz <= kBZ && x0 + lx - 1 < r &&
                        y0 + ly - 1 < r && z0 + lz - 1 < r;
     if (inner && id[j] >= first && id[j] < last) S.pc[id[j] - first] = static_cast<unsigned short>(p);
+    SHL_DCHECK(!(inner && id[j] >= 0) || (id[j] >= first && id[j] < last));  // a brick's nodes are its id range
     if (id[j] >= 0) {
       const TS* src = v + vbase(id[j], 18);
 #pragma unroll
@@ -498,6 +501,7 @@ __global__ void __cluster_dims__(kSumCtas, 1, 1) __launch_bounds__(kSumThreads)
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   // CTA `rank` sums the contiguous chunk of bricks [t0, t1), 16-byte loads
+  SHL_DCHECK(nab > 0);
   const int chunk = (nab + kSumCtas - 1) / kSumCtas;
   const int t0 = rank * chunk, t1 = min(nab, t0 + chunk);
   double tot[6] = {0, 0, 0, 0, 0, 0};

@@ -156,6 +156,7 @@ struct shl_ctx {
     v.nab = n_bricks;
     v.nbx = d.nbx;
     v.nby = d.nby;
+    v.n_nodes = n_nodes;
     return v;
   }
   int64_t n_surface = 0, n_elem = 0;

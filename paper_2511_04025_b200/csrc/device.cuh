@@ -5,8 +5,27 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 namespace shl {
+
+// Bounds-checked build (compute-sanitizer is closed on the gpurun pool):
+// `make DEBUG_CHECKS=1` compiles device-side index checks that trap on the
+// first out-of-range access; the product build compiles them out.
+#ifdef SHL_DEBUG_CHECKS
+#define SHL_DCHECK(cond)                                                                         \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("SHL_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                       \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define SHL_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 constexpr int kFieldRows = 8;        // (y,z)-rows per field block (charge tables reused 8x)
 constexpr int kFieldThreads = 128;   // x samples per field block pass

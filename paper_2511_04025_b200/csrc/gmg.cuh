@@ -558,6 +558,7 @@ __global__ void restrict_own_kernel(const int* __restrict__ list_c, int c0, int 
   node_case(blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x, idx, s);
   idx += c0;
   if (idx >= c1) return;
+  SHL_DCHECK(c0 >= 0 && c0 <= c1);
   const int G = list_c[idx];
   const int I = G % r_c, J = (G / r_c) % r_c, K = G / (r_c * r_c);
   TV acc[3] = {TV(0), TV(0), TV(0)};
@@ -579,6 +580,7 @@ __global__ void restrict_own_kernel(const int* __restrict__ list_c, int c0, int 
         }
     }
   }
+  SHL_DCHECK(G != 0 || idx == 0);
   const size_t oc = vbase(idx, 18) + s * 32;
   b_c[oc] = acc[0];
   b_c[oc + 192] = acc[1];

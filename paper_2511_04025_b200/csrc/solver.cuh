@@ -19,6 +19,7 @@ struct BrickView {
   const int* bstart = nullptr;  // nab + 1 entries
   int nab = 0;
   int nbx = 0, nby = 0;
+  int n_nodes = 0;  // node ids in [0, n_nodes) (bounds-checked build)
 };
 
 // TV: Krylov vectors p, q and the operator arithmetic; TZ: the preconditioned
