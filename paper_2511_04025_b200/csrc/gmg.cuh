@@ -65,13 +65,27 @@ __device__ __forceinline__ void stencil_gather_plane(GatherAcc<TV>& acc, int idx
   for (int mm = 0; mm < 9; ++mm) {
     const int m = PLANE * 9 + mm;
     const int dx = mm % 3 - 1, dy = mm / 3 - 1;
-    int nb = (m == 13) ? idx : nmap[zl + ys[dy + 1] + xs[dx + 1]];
-    nb = nb < 0 ? zero_slot : nb;
+    const int nb = (m == 13) ? idx : nmap[zl + ys[dy + 1] + xs[dx + 1]];
+    if (nb < 0) continue;  // absent neighbour: no coupling
     TV S[9];
+    if (m < 13) {
+      // backward neighbour: the Galerkin operator is symmetric, S_m(n) =
+      // S_{26-m}(n+m)^T, so read the neighbour's forward block transposed.
+      // Each forward block is then read twice in a sweep (by its node and by
+      // that neighbour), the second time mostly from L2: the stencils' DRAM
+      // traffic halves, and the operator applied is exactly symmetric.
+      const TV* sn = stencil + vbase(nb, kStencil) + (26 - m) * 9 * 32;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) S[q] = sb[(m * 9 + q) * 32];
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) S[c * 3 + d] = sn[(d * 3 + c) * 32];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) S[q] = sb[(m * 9 + q) * 32];
+    }
     acc.add(S, xv + vbase(nb, 18));
   }
+  (void)zero_slot;
 }
 
 // level_sweep_kernel latency-split three ways: three warps per 32 nodes, warp p
