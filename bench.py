@@ -437,7 +437,7 @@ def run_ours(args, rank, world, local):
     line = {"metric": METRIC, "value": total_designs / dev_max, "unit": UNIT, "n_gpus": world,
             "steps": len(designs), "warmup": args.warmup, "ms_per_step": dev_max / len(designs) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": ({"mixed": "f64 (field, C^H, Krylov x/r/p/q and the A.z operator); f32 multigrid V-cycle and z",
+            "dtype": ({"mixed": "f64 (field, C^H, Krylov r/p/q and dots, the A.z operator); f32 multigrid V-cycle, z and the stored solution x",
                        "fp32": "f64 field/C^H, f32 PCG", "fp64": "f64"}[args.precision] if gmg else
                       {"mixed": "f64 field/C^H and x/r; f32 operator, p/q, z (block-Jacobi PCG)",
                        "fp32": "f64 field/C^H, f32 PCG", "fp64": "f64"}[args.precision]),

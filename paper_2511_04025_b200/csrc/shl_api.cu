@@ -265,8 +265,9 @@ int resolve_precision(const shl_solve_options& o) {
 }
 
 // ---- solve on the resident mesh ----------------------------------------------
-// TX: x, r; TV: p, q and the operator; TZ: z and the V-cycle (solver.cuh).
-template <typename TX, typename TV, typename TZ>
+// TX: r (and x unless TXS says otherwise); TV: p, q and the operator; TZ: z
+// and the V-cycle; TXS: storage of x (solver.cuh UpdateArgs).
+template <typename TX, typename TV, typename TZ, typename TXS = TX>
 void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, double* C_out,
                shl_stats* st, int prec, bool use_gmg) {
   const int r = c->r;
@@ -281,10 +282,11 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   // sweep (multigrid) in TZ, read by the apply.  (An FP64 z for the FP64
   // operator of mixed multigrid removes the FP32->FP64 conversions from the
   // apply but doubles its L1 traffic; measured slower, 364 vs 330 us at 128^3.)
-  c->vec.ensure(2 * nX * sizeof(TX) + 2 * nV * sizeof(TV) + (nV + 6 * static_cast<size_t>(ld)) * sizeof(TZ));
-  TX* x = c->vec.as<TX>();
-  TX* rv = x + nX;
-  TV* p = reinterpret_cast<TV*>(rv + nX);
+  c->vec.ensure(nX * sizeof(TX) + nX * sizeof(TXS) + 2 * nV * sizeof(TV) +
+                (nV + 6 * static_cast<size_t>(ld)) * sizeof(TZ));
+  TX* rv = c->vec.as<TX>();
+  TXS* x = reinterpret_cast<TXS*>(rv + nX);  // (nX is a multiple of 32: every vector stays 128-byte aligned)
+  TV* p = reinterpret_cast<TV*>(x + nX);
   TV* q = p + nV;
   TZ* z = reinterpret_cast<TZ*>(q + nV);
   TZ* dinv = z + nV;
@@ -321,7 +323,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   const double ridge = diag_mean * (sizeof(TZ) == 8 ? 1e-11 : 1e-8);
   CK(cudaEventRecord(c->ev[3], c->stream));
   shl::ElementConstLease const_lease(K0, W, T, r, c->stream);
-  CK(cudaMemsetAsync(x, 0, nX * sizeof(TX), c->stream));
+  CK(cudaMemsetAsync(x, 0, nX * sizeof(TXS), c->stream));
   CK(cudaMemsetAsync(p, 0, 2 * nV * sizeof(TV), c->stream));
   CK(cudaMemsetAsync(z, 0, nV * sizeof(TZ), c->stream));
   CK(cudaEventRecord(c->ev[8], c->stream));
@@ -376,7 +378,7 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
   shl::PcgState* dst = c->state.as<shl::PcgState>();
   const TV* beta_apply = sizeof(TV) == 8 ? reinterpret_cast<const TV*>(c->beta64.p)
                                          : reinterpret_cast<const TV*>(c->beta32.p);
-  shl::UpdateArgs<TX, TV, TZ> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1,
+  shl::UpdateArgs<TX, TV, TZ, TXS> ua{x, rv, p, q, z, dinv, c->partials.as<double>(), dst, n, ld, 1,
                                 nullptr, 0, use_gmg ? 1 : 0, use_gmg ? vc.xa[0] : nullptr,
                                 static_cast<TZ>(vc.gp.omega)};
   shl::ApplyArgs<TV, TZ> aa{c->node_list.as<int>(), c->node_map.as<int>(), beta_apply, z, p, q,
@@ -572,12 +574,12 @@ void run_solve(shl_ctx* c, const double* K0, const shl_solve_options& opt, doubl
                   fin.max_iter);
     throw ShlError(SHL_SOLVER, buf);
   }
-  shl::ChomArgs<TX> ca{c->elem_list.as<int>(), c->node_map.as<int>(), c->beta64.as<double>(), x,
+  shl::ChomArgs<TXS> ca{c->elem_list.as<int>(), c->node_map.as<int>(), c->beta64.as<double>(), x,
                        c->partials.as<double>(), c->cout.as<double>(), dst,
                        static_cast<int>(c->n_elem), r, ld, 0, r, 0};
   {
     NvtxRange nr("shellular: C^H reduction");
-    shl::launch_chom<TX>(ca, grid_c, c->stream);
+    shl::launch_chom<TXS>(ca, grid_c, c->stream);
   }
   launches += 1;
   CK(cudaGetLastError());
@@ -627,7 +629,7 @@ void solve_dispatch_once(shl_ctx* c, const double* K0, const shl_solve_options& 
       if (!gmg)
         run_solve<double, float, float>(c, K0, opt, C_out, st, prec, gmg);
       else
-        run_solve<double, double, float>(c, K0, opt, C_out, st, prec, gmg);
+        run_solve<double, double, float, float>(c, K0, opt, C_out, st, prec, gmg);
       break;
     }
     default: run_solve<float, float, float>(c, K0, opt, C_out, st, prec, gmg); break;

@@ -521,13 +521,13 @@ __global__ void __launch_bounds__(192 * G, MINB) apply6_kernel(const ApplyArgs<d
 // Dinv entries -> ~30 registers, full occupancy, every access a coalesced
 // 32-node plane segment.  blockIdx.x = node_block * 6 + s so the six blocks
 // of a node block run together and Dinv is re-read from L2, not DRAM.
-template <typename TX, typename TV, typename TZ>
-__global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV, TZ> U) {
+template <typename TX, typename TV, typename TZ, typename TXS>
+__global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV, TZ, TXS> U) {
   pdl_wait();
   __shared__ double scratch[32 * 2];
   PcgState* st = U.state;
   if (st->stop) return;
-  TX* __restrict__ xv = U.x;
+  TXS* __restrict__ xv = U.x;
   TX* __restrict__ rv = U.r;
   const TV* __restrict__ pv = U.p;
   const TV* __restrict__ qv = U.q;
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV, TZ
     if (!U.init) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        xc[c] = xv[ob + c * 192];
+        xc[c] = static_cast<TX>(xv[ob + c * 192]);
         pc[c] = pv[ob + c * 192];
         qc[c] = qv[ob + c * 192];
       }
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV, TZ
       if (!U.init) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          xv[ob + c * 192] = xc[c];
+          xv[ob + c * 192] = static_cast<TXS>(xc[c]);
           rv[ob + c * 192] = rc[c];
         }
       }
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(256) update_kernel(const UpdateArgs<TX, TV, TZ
     if (!U.init) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        xv[ob + c * 192] = xc[c];
+        xv[ob + c * 192] = static_cast<TXS>(xc[c]);
         rv[ob + c * 192] = rc[c];
       }
     }
@@ -905,9 +905,9 @@ void launch_apply(const ApplyArgs<TV, TZ>& a, int grid, cudaStream_t s) {
 
 int apply_grid(int n, int num_sms) { return std::max(1, std::min((n + 63) / 64, num_sms * 4)); }
 
-template <typename TX, typename TV, typename TZ>
-void launch_update(const UpdateArgs<TX, TV, TZ>& u, int grid, cudaStream_t s) {
-  launch_pdl(update_kernel<TX, TV, TZ>, grid, 256, 0, s, u);
+template <typename TX, typename TV, typename TZ, typename TXS>
+void launch_update(const UpdateArgs<TX, TV, TZ, TXS>& u, int grid, cudaStream_t s) {
+  launch_pdl(update_kernel<TX, TV, TZ, TXS>, grid, 256, 0, s, u);
 }
 
 template <typename TX>
@@ -926,6 +926,8 @@ template void launch_apply<double, float>(const ApplyArgs<double, float>&, int, 
 template void launch_apply<float, float>(const ApplyArgs<float, float>&, int, cudaStream_t);
 template void launch_update<double, double, double>(const UpdateArgs<double, double>&, int, cudaStream_t);
 template void launch_update<double, double, float>(const UpdateArgs<double, double, float>&, int, cudaStream_t);
+template void launch_update<double, double, float, float>(const UpdateArgs<double, double, float, float>&, int,
+                                                         cudaStream_t);
 template void launch_update<double, float, float>(const UpdateArgs<double, float>&, int, cudaStream_t);
 template void launch_update<float, float, float>(const UpdateArgs<float, float>&, int, cudaStream_t);
 template void launch_chom<double>(const ChomArgs<double>&, int, cudaStream_t);

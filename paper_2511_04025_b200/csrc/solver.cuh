@@ -48,9 +48,12 @@ struct ApplyArgs {
   int n0 = 0;        // per-node gather kernels: iterate nodes [n0, n) (z-slab interior / boundary planes)
 };
 
-template <typename TX, typename TV, typename TZ = TV>
+// TXS: storage type of the solution x (FP32 in mixed multigrid: x is only
+// accumulated, x += alpha p, and read once for C^H, whose error is second
+// order in x's rounding since C^H is the energy at its minimiser)
+template <typename TX, typename TV, typename TZ = TV, typename TXS = TX>
 struct UpdateArgs {
-  TX* x;
+  TXS* x;
   TX* r;
   const TV* p;
   const TV* q;
@@ -200,8 +203,8 @@ void launch_coarse_brick_flags(const int* map, int r, int* flag, cudaStream_t s)
 // Grid (block count) launch_apply / launch_level_sweep use for n nodes; the
 // caller sizes its partials buffer as 6 doubles per block.
 int apply_grid(int n, int num_sms);
-template <typename TX, typename TV, typename TZ>
-void launch_update(const UpdateArgs<TX, TV, TZ>& u, int grid, cudaStream_t s);
+template <typename TX, typename TV, typename TZ, typename TXS = TX>
+void launch_update(const UpdateArgs<TX, TV, TZ, TXS>& u, int grid, cudaStream_t s);
 template <typename TX>
 void launch_chom(const ChomArgs<TX>& c, int grid, cudaStream_t s);
 
