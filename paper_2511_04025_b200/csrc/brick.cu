@@ -554,11 +554,20 @@ __global__ void __cluster_dims__(kSumCtas, 1, 1) __launch_bounds__(kSumThreads)
 // load is 4 row segments of consecutive grid-ordered ids) and gathers the
 // neighbours from shared memory.  mode 0: xout = xin + w Dinv (b - A xin);
 // mode 1: xout = b - A xin.  Node 0 (grid index 0) is pinned: output 0.
+// Three threads per brick position (one per neighbour plane dz = -1, 0, +1,
+// 9 stencil blocks each; 384-thread CTAs): the stored levels that take this
+// kernel have few active bricks (32^3: ~220, 1.5 per SM), so one thread per
+// position left 6 warps per SM to cover the stencil loads' latency.  The
+// three partial sums meet in shared memory (fixed order), plane 0's threads
+// finish.
+constexpr int kSBParts = 3;
+constexpr int kSBThreads = kSBParts * kNodes;
 struct alignas(16) StencilBrickShared {
   float xs[18 * kPhys];
+  float2 part[kSBParts][9][kNodes];  // [plane][c * 3 + load-case pair][position]
 };
 
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kSBThreads)
     stencil_brick_sweep_kernel(const GmgLevelView<float> L, const float* __restrict__ b,
                                const float* __restrict__ xin, float* __restrict__ xout, float omega, int mode,
                                const PcgState* st) {
@@ -570,15 +579,13 @@ __global__ void __launch_bounds__(kThreads, 4)
   const int t = blockIdx.x, tid = threadIdx.x, r = L.r;
   int x0, y0, z0;
   brick_origin(B, t, x0, y0, z0);
-  int id[kPer];
-  stage_ids(id, B, t, r, L.node_map);
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int p = tid + j * kThreads;
-    if (p >= kRegion) continue;
-    const int ph = stage_pos<true>(p % kRX, (p / kRX) % kRY, p / (kRX * kRY));
-    if (id[j] >= 0) {
-      const float* src = xin + vbase(id[j], 18);
+  if (tid < kRegion) {  // one staged position per thread
+    const int lx = tid % kRX, ly = (tid / kRX) % kRY, lz = tid / (kRX * kRY);
+    const int gx = wrap3(x0 + lx - 1, r), gy = wrap3(y0 + ly - 1, r), gz = wrap3(z0 + lz - 1, r);
+    const int id = __ldg(L.node_map + (static_cast<size_t>(gz) * r + gy) * r + gx);
+    const int ph = stage_pos<true>(lx, ly, lz);
+    if (id >= 0) {
+      const float* src = xin + vbase(id, 18);
 #pragma unroll
       for (int q = 0; q < 18; ++q) cp_async<4>(&S.xs[xs_index<float, true>(q, ph)], src + q * 32);
     } else {
@@ -587,46 +594,55 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
   }
   cp_async_commit();
-  // this thread's brick position and node (the map load overlaps the staging)
-  const int bx = tid & 7, by = (tid >> 3) & 3, bz = tid >> 5;
+  // this thread's brick position, node and neighbour plane
+  const int part = tid / kNodes, pos = tid % kNodes;
+  const int bx = pos & 7, by = (pos >> 3) & 3, bz = pos >> 5;
   const int gx = x0 + bx, gy = y0 + by, gz = z0 + bz;
   const int G = (gz * r + gy) * r + gx;
   const int idx = __ldg(L.node_map + G);
   cp_async_wait<0>();
   __syncthreads();
-  if (idx < 0) return;  // (no barrier below)
+  const int lx = bx + 1, ly = by + 1, lz = bz + 1;
+  const int pxy = kRowStep * ly + lx;
+  if (idx >= 0 && G != 0) {
+    const float* __restrict__ Sg = L.stencil + vbase(idx, 243);  // 27 x 3x3 blocks per node
+    const float2* __restrict__ x2 = reinterpret_cast<const float2*>(S.xs);
+    float2 acc[9];  // [c][load-case pair]
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = make_float2(0.f, 0.f);
+    const int dz = part - 1;
+#pragma unroll 3
+    for (int mm = 0; mm < 9; ++mm) {
+      const int m = part * 9 + mm;
+      const int dx = mm % 3 - 1, dy = mm / 3 - 1;
+      float Sm[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) Sm[q] = __ldg(Sg + (m * 9 + q) * 32);
+      const float2* xn = x2 + plane_base(lz + dz) + pxy + dy * kRowStep + dx;
+#pragma unroll
+      for (int sp = 0; sp < 3; ++sp) {
+        const float2 z0v = xn[(0 * 3 + sp) * kPhys], z1v = xn[(1 * 3 + sp) * kPhys],
+                     z2v = xn[(2 * 3 + sp) * kPhys];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          float2 v = acc[c * 3 + sp];
+          v = __ffma2_rn(make_float2(Sm[c * 3 + 0], Sm[c * 3 + 0]), z0v, v);
+          v = __ffma2_rn(make_float2(Sm[c * 3 + 1], Sm[c * 3 + 1]), z1v, v);
+          v = __ffma2_rn(make_float2(Sm[c * 3 + 2], Sm[c * 3 + 2]), z2v, v);
+          acc[c * 3 + sp] = v;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) S.part[part][q][pos] = acc[q];
+  }
+  __syncthreads();
+  if (part != 0 || idx < 0) return;
   const size_t ob = vbase(idx, 18);
   if (G == 0) {  // pinned node
 #pragma unroll
     for (int q = 0; q < 18; ++q) xout[ob + q * 32] = 0.f;
     return;
-  }
-  const int lx = bx + 1, ly = by + 1, lz = bz + 1;
-  const int pxy = kRowStep * ly + lx;
-  const float* __restrict__ Sg = L.stencil + vbase(idx, 243);  // 27 x 3x3 blocks per node
-  const float2* __restrict__ x2 = reinterpret_cast<const float2*>(S.xs);
-  float2 acc[9];  // [c][load-case pair]
-#pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] = make_float2(0.f, 0.f);
-#pragma unroll 3
-  for (int m = 0; m < 27; ++m) {
-    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = m / 9 - 1;
-    float Sm[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) Sm[q] = __ldg(Sg + (m * 9 + q) * 32);
-    const float2* xn = x2 + plane_base(lz + dz) + pxy + dy * kRowStep + dx;
-#pragma unroll
-    for (int sp = 0; sp < 3; ++sp) {
-      const float2 z0v = xn[(0 * 3 + sp) * kPhys], z1v = xn[(1 * 3 + sp) * kPhys], z2v = xn[(2 * 3 + sp) * kPhys];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float2 v = acc[c * 3 + sp];
-        v = __ffma2_rn(make_float2(Sm[c * 3 + 0], Sm[c * 3 + 0]), z0v, v);
-        v = __ffma2_rn(make_float2(Sm[c * 3 + 1], Sm[c * 3 + 1]), z1v, v);
-        v = __ffma2_rn(make_float2(Sm[c * 3 + 2], Sm[c * 3 + 2]), z2v, v);
-        acc[c * 3 + sp] = v;
-      }
-    }
   }
   float D[6];
   if (mode != 1) {
@@ -642,7 +658,9 @@ __global__ void __launch_bounds__(kThreads, 4)
       float res[3], xo[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const float y = h ? acc[c * 3 + sp].y : acc[c * 3 + sp].x;
+        const float2 p0 = S.part[0][c * 3 + sp][pos], p1 = S.part[1][c * 3 + sp][pos],
+                     p2 = S.part[2][c * 3 + sp][pos];
+        const float y = h ? (p0.y + p1.y) + p2.y : (p0.x + p1.x) + p2.x;
         res[c] = b[ob + (c * 6 + s_) * 32] - y;
         xo[c] = S.xs[xs_index<float, true>(c * 6 + s_, ph)];
       }
@@ -750,7 +768,7 @@ void launch_stencil_brick_sweep(const GmgLevelView<float>& L, const float* b, co
                                 float omega, int mode, const PcgState* st, cudaStream_t s) {
   static const bool configured = brick_configure(stencil_brick_sweep_kernel, sizeof(StencilBrickShared));
   (void)configured;
-  launch_pdl(stencil_brick_sweep_kernel, L.bricks.nab, kThreads, sizeof(StencilBrickShared), s, L, b, xin, xout,
+  launch_pdl(stencil_brick_sweep_kernel, L.bricks.nab, kSBThreads, sizeof(StencilBrickShared), s, L, b, xin, xout,
              omega, mode, st);
 }
 
