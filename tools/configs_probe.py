@@ -27,6 +27,7 @@ for rep in range(2):
 for pre in ("gmg", "jacobi"):
     o = S.HomogenizeOptions(residual_tol=1e-5, precision="mixed", preconditioner=pre)
     ref = res if pre == "gmg" else S.homogenize(d, S.ShellParams(), S.BaseMaterial(), 256, o, ctx=ctx)
+    S.homogenize_slabs(d, S.ShellParams(), S.BaseMaterial(), 256, 4, o, ctx=ctx)  # warm (allocations, module loads)
     sl = S.homogenize_slabs(d, S.ShellParams(), S.BaseMaterial(), 256, 4, o, ctx=ctx)
     print(f"C5 4 emulated slabs ({pre}): rel diff vs undecomposed "
           f"{np.linalg.norm(sl.tensor - ref.tensor) / np.linalg.norm(ref.tensor):.2e}, "
